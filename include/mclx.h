@@ -1,0 +1,194 @@
+/*
+ * mclx.h -- C ABI of libmclx.so, the B200-native (sm_100a) hot path of HipMCL's
+ * Markov Cluster method (Selvitopi, Hussain, Azad, Buluc; arXiv:2002.10083).
+ *
+ * Citations are to /root/reference/PAPER.md as P:<line> with the enclosing
+ * section / algorithm, and to DESIGN.md readings Q1..Q20 where the paper is
+ * silent.  The path (Alg. 1 lines 3-5) is one MCL iteration:
+ *   expansion B = A*A (SpGEMM), prune (threshold + top-k, P:161, P:187-188,
+ *   recovery Q7), inflation (Hadamard power r) and column
+ *   renormalisation (Q1), plus the cluster extraction of Alg. 1 line 6.
+ *
+ * Conventions common to every call
+ *  - Matrices are CSC (§III-B: CSC in, CSC out, C = AB formed
+ *    column-by-column, no transpose).  All pointers inside mcl_csc_t are DEVICE
+ *    pointers on the context's device.  col_ptr is int64 [ncols+1] with
+ *    col_ptr[0] = 0 and non-decreasing; row_idx is int32 [nnz], strictly
+ *    increasing inside each column; val is fp32 [nnz], finite and > 0.
+ *  - Inputs are BORROWED: owned by the caller, valid in stream order for the
+ *    duration of the call, never modified.
+ *  - Outputs (mcl_csc_t *out arguments) are ALLOCATED BY THE LIBRARY through
+ *    the context's allocator callback and become caller-owned on return; free
+ *    them with mcl_csc_release (which calls the free callback).
+ *  - All device work is enqueued on the context stream.  Calls that must size
+ *    an output (mcl_expand, mcl_spgemm, mcl_prune_inflate, mcl_iterate,
+ *    mcl_merge, mcl_preprocess) synchronise that stream a small, fixed number of
+ *    times to read sizes; results are valid in stream order when the call returns.
+ *  - Every call returns MCL_OK (0) or a negative MCL_ERR_* code.  On error, out
+ *    matrices are zeroed (nnz 0, NULL pointers), nothing leaks, and
+ *    mcl_last_error(ctx) describes the failure.  The library never aborts and
+ *    never prints.
+ *  - There is no CPU fallback: every arithmetic step runs in the library's own
+ *    sm_100a kernels.  A context refuses to be created on a device that is not
+ *    compute capability 10.0 (MCL_ERR_UNSUPPORTED_DEVICE).
+ */
+#ifndef MCLX_H
+#define MCLX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MCLX_VERSION 1
+
+enum {
+    MCL_OK = 0,
+    MCL_ERR_INVALID_ARG = -1,       /* NULL pointer, r <= 1, S < 1, pct outside [0,1], theta < 0, ... */
+    MCL_ERR_DIM = -2,               /* A.ncols != B.nrows, non-square where A*A is needed, bad range */
+    MCL_ERR_FORMAT = -3,            /* only with env MCLX_VALIDATE=1: malformed CSC                    */
+    MCL_ERR_OOM = -4,               /* allocator returned NULL                                          */
+    MCL_ERR_CUDA = -5,              /* a CUDA runtime error (message in mcl_last_error)                 */
+    MCL_ERR_NCCL = -6,              /* an NCCL error                                                    */
+    MCL_ERR_UNSUPPORTED_DEVICE = -7,/* device is not sm_100 (B200)                                      */
+    MCL_ERR_NOT_IMPLEMENTED = -8
+};
+
+/* A CSC block.  (row0, col0, n_global) place the block in a global matrix for the
+ * multi-GPU partition (all 0 / n on one GPU); row0 also offsets the Cohen key
+ * counters so that a block's keys equal the global matrix's keys. */
+typedef struct {
+    int64_t nrows, ncols, nnz;
+    int64_t row0, col0, n_global;
+    int64_t *col_ptr; /* device, [ncols+1] */
+    int32_t *row_idx; /* device, [nnz]     */
+    float *val;       /* device, [nnz]     */
+} mcl_csc_t;
+
+/* Parameters of one MCL iteration.  Defaults (mcl_params_default) in brackets. */
+typedef struct {
+    double inflation;        /* r > 1 [2.0]  Hadamard power, r = 2 at P:770 (Q2)   */
+    double prune_threshold;  /* theta >= 0 [1e-4]  keep v >= theta, "user supplied" (Q3,Q4) */
+    int32_t select_k;        /* S >= 1 [1100]  top-S when more than S survive, P:188 (Q5,Q6)  */
+    int32_t recover_k;       /* R >= 0 [1400]  0 disables recovery (Q7)                        */
+    double recover_pct;      /* pct in [0,1] [0.9]  recover when kept mass < pct (Q7)          */
+    double chaos_eps;        /* [1e-3] convergence threshold used by the caller's loop (Q9)    */
+    int32_t est_keys;        /* r for Cohen, 2..16 [10]                           */
+    double est_cf_threshold; /* [2.0] exact symbolic sizing when estimated cf < this  */
+    uint64_t seed;           /* [0x5eed] Philox key of the Cohen exponential keys (Q14)        */
+    double mem_safety;       /* [0.9] fraction of free HBM the phase planner may use (Q15)     */
+    int32_t estimator;       /* [0] 0 = policy of P:1076-1077, 1 = always exact symbolic,
+                                2 = always Cohen (with overflow retry)                        */
+    int32_t force_bin;       /* [-1] >= 0 forces every non-empty column into that smem bin (or
+                                the global bin, MCL_NUM_BINS) -- for bin-invariance tests      */
+} mcl_params_t;
+
+#define MCL_NUM_BINS 6 /* shared-memory bins; bin index MCL_NUM_BINS is the global-memory bin */
+
+/* Filled by the calls that take it (NULL allowed).  -1 = not computed. */
+typedef struct {
+    int64_t flops;           /* sum_j sum_{k in inds(B_*j)} nnz(A_*k)              */
+    int64_t nnz_in;          /* nnz(A)                                                          */
+    int64_t nnz_unpruned;    /* nnz(A*A) when known (expand, exact symbolic), else -1           */
+    int64_t nnz_out;         /* nnz of the returned matrix                                      */
+    double est_nnz;          /* Cohen estimate of nnz(A*A) (sum over columns), -1 if not run    */
+    double cf;               /* flops / nnz_unpruned (or / est_nnz)                             */
+    float chaos;             /* max_j chaos_j of the pruned, renormalised columns (Q9)          */
+    int32_t phases;          /* column batches used                                             */
+    int32_t retries;         /* columns re-run after a hash-table overflow                      */
+    int32_t estimator_used;  /* 1 exact symbolic, 2 Cohen                                       */
+    int64_t bin_cols[MCL_NUM_BINS + 1];
+    int64_t bin_flops[MCL_NUM_BINS + 1];
+    float ms[8];             /* per stage: 0 flops/bin, 1 estimate, 2 symbolic, 3 numeric
+                                (fused numeric+select+inflate in mcl_iterate), 4 select/inflate
+                                (unfused), 5 assemble, 6 total, 7 numeric launches count      */
+    int64_t peak_bytes;      /* peak scratch bytes held by the context                          */
+} mcl_stats_t;
+
+/* Allocator callbacks: device memory, stream-ordered.  NULL callbacks select the
+ * built-in cudaMallocAsync/cudaFreeAsync pool. */
+typedef void *(*mcl_alloc_fn)(void *state, size_t bytes, void *stream);
+typedef void (*mcl_free_fn)(void *state, void *ptr, size_t bytes, void *stream);
+
+typedef struct mcl_ctx *mcl_ctx_t;
+
+int mcl_version(void);
+void mcl_params_default(mcl_params_t *p);
+
+/* Create a context on `device` enqueuing on `stream` (a cudaStream_t; NULL = the
+ * legacy default stream).  Fails with MCL_ERR_UNSUPPORTED_DEVICE off sm_100. */
+int mcl_ctx_create(mcl_ctx_t *ctx, int device, void *stream, mcl_alloc_fn alloc,
+                   mcl_free_fn free_fn, void *alloc_state);
+int mcl_ctx_set_stream(mcl_ctx_t ctx, void *stream);
+int mcl_ctx_destroy(mcl_ctx_t ctx);
+const char *mcl_last_error(mcl_ctx_t ctx);
+
+/* Free a matrix returned by this library (no-op on an all-zero struct). */
+int mcl_csc_release(mcl_ctx_t ctx, mcl_csc_t *m);
+
+/* Alg. 1 line 1: A = column-stochastic version of the weighted
+ * adjacency matrix G (square, weights > 0).  add_loops != 0 adds a self-loop of
+ * weight 1.0 to every vertex first, summed onto an existing diagonal (Q10).
+ * Empty columns (add_loops == 0) stay empty. */
+int mcl_preprocess(mcl_ctx_t ctx, const mcl_csc_t *G, int add_loops, mcl_csc_t *A_out);
+
+/* flops per column: flops_j = sum_{k in inds(B_*j)} nnz(A_*k).
+ * flops_dev: optional device int64 [B.ncols]; total: optional host int64. */
+int mcl_flops(mcl_ctx_t ctx, const mcl_csc_t *A, const mcl_csc_t *B, int64_t *flops_dev,
+              int64_t *total);
+
+/* Cohen's probabilistic size estimate of C = A*B (§V; lambda = 1 and
+ * r keys per first-layer vertex).  est_dev: device fp32 [B.ncols]
+ * receives (r-1)/sum_s c_j[s] (0 for an unreachable column).  keys_dev (optional,
+ * device fp32 [r * A.nrows], plane-major [s][i]) receives the exponential keys
+ * X[s][i] = (float)(-log((u+0.5) 2^-32)), u = Philox4x32-10(ctr=(i_lo,i_hi,s,0),
+ * key=(seed_lo,seed_hi))[0], i = A.row0 + local row (Q14).  total: optional host sum. */
+int mcl_estimate(mcl_ctx_t ctx, const mcl_csc_t *A, const mcl_csc_t *B, int32_t r,
+                 uint64_t seed, float *est_dev, float *keys_dev, double *total);
+
+/* Exact symbolic pass (§V): nnz_dev (device int64
+ * [B.ncols]) receives |union_{k in inds(B_*j)} inds(A_*k)|. */
+int mcl_symbolic(mcl_ctx_t ctx, const mcl_csc_t *A, const mcl_csc_t *B, int64_t *nnz_dev,
+                 int64_t *total);
+
+/* Unpruned product C[:, b:e) = A * B[:, b:e) (rectangular blocks for the
+ * Sparse-SUMMA stages).  Exact sizes from the symbolic pass; rows
+ * sorted ascending; values fp32 (fp64 accumulation for columns with
+ * nnz(B_*j) > 16384).  C_out->ncols = e - b. */
+int mcl_spgemm(mcl_ctx_t ctx, const mcl_csc_t *A, const mcl_csc_t *B, int64_t col_begin,
+               int64_t col_end, const mcl_params_t *p, mcl_csc_t *C_out, mcl_stats_t *st);
+
+/* The expansion of Alg. 1 line 3: mcl_spgemm(A, A, ...).  A square. */
+int mcl_expand(mcl_ctx_t ctx, const mcl_csc_t *A, int64_t col_begin, int64_t col_end,
+               const mcl_params_t *p, mcl_csc_t *C_out, mcl_stats_t *st);
+
+/* Alg. 1 lines 4-5 on an unpruned C (readings Q1-Q9): per column, threshold,
+ * top-S select / recovery / argmax fallback, renormalise, Hadamard power r,
+ * renormalise.  st->chaos = max_j chaos_j.  chaos_dev (optional, device fp32
+ * [C.ncols]) receives chaos_j. */
+int mcl_prune_inflate(mcl_ctx_t ctx, const mcl_csc_t *C, const mcl_params_t *p,
+                      mcl_csc_t *A_next, float *chaos_dev, mcl_stats_t *st);
+
+/* One fused MCL iteration (Alg. 1 lines 3-5): flop count and binning, size
+ * estimate (Cohen or exact symbolic by the P:1076-1077 policy), numeric hash
+ * SpGEMM whose epilogue selects / prunes / recovers / inflates / renormalises each
+ * column while it is still in shared memory, then assembly of A_next.  The
+ * unpruned product never reaches HBM. */
+int mcl_iterate(mcl_ctx_t ctx, const mcl_csc_t *A, const mcl_params_t *p, mcl_csc_t *A_next,
+                mcl_stats_t *st);
+
+/* Alg. 1 line 6: weak connected components of the pattern of A (Q11).
+ * labels_dev: caller-owned device int32 [A.ncols]; components are numbered in
+ * order of their smallest vertex.  ncl: host. */
+int mcl_clusters(mcl_ctx_t ctx, const mcl_csc_t *A, int32_t *labels_dev, int64_t *ncl);
+
+/* Merge L equally shaped CSC blocks into their sum (the "merge all lists
+ * in L" step of Alg. 2).  Rows sorted, duplicate rows summed. */
+int mcl_merge(mcl_ctx_t ctx, int32_t L, const mcl_csc_t *lists, mcl_csc_t *out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MCLX_H */

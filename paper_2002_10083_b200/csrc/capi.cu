@@ -1,0 +1,832 @@
+// capi.cu -- the C ABI of libmclx.so (include/mclx.h): context, allocation, and the
+// host orchestration of each entry point (which kernels, in what order, which few
+// small read-backs).  No arithmetic of the method happens on the host.
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <unordered_map>
+
+#include "kernels.h"
+#include "mclx.h"
+
+using namespace mclx;
+
+struct Buf {
+    void *p = nullptr;
+    size_t bytes = 0;
+};
+
+struct mcl_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    mcl_alloc_fn alloc = nullptr;
+    mcl_free_fn free_fn = nullptr;
+    void *state = nullptr;
+    std::string err;
+    int sms = 148;
+    std::unordered_map<std::string, Buf> scratch;
+    size_t cur = 0, peak = 0;
+    int occ[3][kNumBins + 1] = {};
+    void *pin = nullptr;  // pinned host staging for small read-backs
+    cudaEvent_t ev[8] = {};
+};
+
+namespace {
+
+int fail(mcl_ctx *c, int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (c) c->err = buf;
+    return code;
+}
+
+#define CK(call)                                                                              \
+    do {                                                                                      \
+        cudaError_t e_ = (call);                                                              \
+        if (e_ != cudaSuccess)                                                                \
+            return fail(c, MCL_ERR_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #call,         \
+                        cudaGetErrorString(e_));                                              \
+    } while (0)
+
+#define RC(call)                   \
+    do {                           \
+        int r_ = (call);           \
+        if (r_ != MCL_OK) return r_; \
+    } while (0)
+
+void *dalloc(mcl_ctx *c, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    void *p = nullptr;
+    if (c->alloc) {
+        p = c->alloc(c->state, bytes, (void *)c->stream);
+    } else if (cudaMallocAsync(&p, bytes, c->stream) != cudaSuccess) {
+        cudaGetLastError();
+        p = nullptr;
+    }
+    return p;
+}
+void dfree(mcl_ctx *c, void *p, size_t bytes) {
+    if (!p) return;
+    if (c->free_fn) c->free_fn(c->state, p, bytes, (void *)c->stream);
+    else cudaFreeAsync(p, c->stream);
+}
+
+// Named, growing scratch buffers owned by the context.
+int scratch(mcl_ctx *c, const char *name, size_t bytes, void **out) {
+    Buf &b = c->scratch[name];
+    if (b.bytes < bytes) {
+        if (b.p) {
+            dfree(c, b.p, b.bytes);
+            c->cur -= b.bytes;
+        }
+        size_t nb = bytes + bytes / 8 + 4096;
+        b.p = dalloc(c, nb);
+        if (!b.p) {
+            b.bytes = 0;
+            return fail(c, MCL_ERR_OOM, "scratch '%s': cannot allocate %zu bytes", name, nb);
+        }
+        b.bytes = nb;
+        c->cur += nb;
+        c->peak = std::max(c->peak, c->cur);
+    }
+    *out = b.p;
+    return MCL_OK;
+}
+template <typename T>
+int scratch_t(mcl_ctx *c, const char *name, size_t count, T **out) {
+    return scratch(c, name, count * sizeof(T), (void **)out);
+}
+
+// Copy `bytes` from device to the pinned buffer and wait for the stream.
+int readback(mcl_ctx *c, const void *dev, size_t bytes, void *host) {
+    CK(cudaMemcpyAsync(c->pin, dev, bytes, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    memcpy(host, c->pin, bytes);
+    return MCL_OK;
+}
+
+void zero_csc(mcl_csc_t *m) {
+    if (m) memset(m, 0, sizeof *m);
+}
+
+int alloc_rows_vals(mcl_ctx *c, mcl_csc_t *m, int64_t nnz) {
+    m->nnz = nnz;
+    m->row_idx = (int32_t *)dalloc(c, (size_t)std::max<int64_t>(nnz, 1) * sizeof(int32_t));
+    m->val = (float *)dalloc(c, (size_t)std::max<int64_t>(nnz, 1) * sizeof(float));
+    if (!m->row_idx || !m->val) return fail(c, MCL_ERR_OOM, "cannot allocate %lld nnz", (long long)nnz);
+    return MCL_OK;
+}
+
+int check_csc(mcl_ctx *c, const mcl_csc_t *m, const char *what) {
+    if (!m) return fail(c, MCL_ERR_INVALID_ARG, "%s is NULL", what);
+    if (m->nrows < 0 || m->ncols < 0 || m->nnz < 0)
+        return fail(c, MCL_ERR_INVALID_ARG, "%s has negative dimensions", what);
+    if (!m->col_ptr) return fail(c, MCL_ERR_INVALID_ARG, "%s.col_ptr is NULL", what);
+    if (m->nnz > 0 && (!m->row_idx || !m->val))
+        return fail(c, MCL_ERR_INVALID_ARG, "%s has nnz > 0 but NULL arrays", what);
+    if (m->nrows > 0x7ffffffeLL) return fail(c, MCL_ERR_DIM, "%s: more than 2^31-2 rows", what);
+    return MCL_OK;
+}
+
+int check_params(mcl_ctx *c, const mcl_params_t *p) {
+    if (!(p->inflation > 1.0)) return fail(c, MCL_ERR_INVALID_ARG, "inflation must be > 1");
+    if (!(p->prune_threshold >= 0.0)) return fail(c, MCL_ERR_INVALID_ARG, "prune_threshold < 0");
+    if (p->select_k < 1) return fail(c, MCL_ERR_INVALID_ARG, "select_k must be >= 1");
+    if (p->recover_k < 0) return fail(c, MCL_ERR_INVALID_ARG, "recover_k must be >= 0");
+    if (!(p->recover_pct >= 0.0 && p->recover_pct <= 1.0))
+        return fail(c, MCL_ERR_INVALID_ARG, "recover_pct outside [0,1]");
+    if (p->est_keys < 2 || p->est_keys > 16)
+        return fail(c, MCL_ERR_INVALID_ARG, "est_keys must be in [2,16]");
+    return MCL_OK;
+}
+
+PruneParams prune_params(const mcl_params_t *p) {
+    PruneParams pp;
+    pp.theta = p->prune_threshold;
+    pp.S = p->select_k;
+    pp.R = p->recover_k;
+    pp.pct = p->recover_pct;
+    pp.r = p->inflation;
+    pp.r_is_2 = p->inflation == 2.0;
+    pp.kmax = std::max(1, std::max(p->select_k, p->recover_k));
+    return pp;
+}
+
+float elapsed(mcl_ctx *c, int a, int b) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, c->ev[a], c->ev[b]) != cudaSuccess) {
+        cudaGetLastError();
+        return -1.f;
+    }
+    return ms;
+}
+
+void init_stats(mcl_stats_t *st) {
+    if (!st) return;
+    memset(st, 0, sizeof *st);
+    st->nnz_unpruned = -1;
+    st->est_nnz = -1;
+    st->cf = -1;
+    st->phases = 1;
+    for (int i = 0; i < 8; i++) st->ms[i] = -1.f;
+}
+
+// Operands of one product C = A * B[:, cb : cb + n).
+struct Prod {
+    const mcl_csc_t *A, *B;
+    int64_t cb, n;
+};
+
+// Cohen estimate for the output columns of a product.
+int cohen(mcl_ctx *c, const Prod &pr, int r, uint64_t seed, float *est, float *keys_out) {
+    float *X, *M;
+    RC(scratch_t(c, "cohen_X", (size_t)std::max<int64_t>(pr.A->nrows, 1) * r, &X));
+    RC(scratch_t(c, "cohen_M", (size_t)std::max<int64_t>(pr.A->ncols, 1) * r, &M));
+    CK(launch_cohen_keys(pr.A->nrows, pr.A->row0, r, seed, X, keys_out, c->stream));
+    CK(launch_cohen_min(pr.A->ncols, pr.A->col_ptr, pr.A->row_idx, 0, X, r, M, nullptr, c->stream));
+    CK(launch_cohen_min(pr.n, pr.B->col_ptr, pr.B->row_idx, pr.cb, M, r, nullptr, est, c->stream));
+    return MCL_OK;
+}
+
+// Classify the columns of a product into bins and run every bin kernel in `mode`;
+// columns whose table overflowed (estimate too small) are re-binned with the exact
+// bound min(f_j, m) and re-run.  `base` carries the mode's outputs.
+int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float *est,
+             const int64_t *exact, int force_bin, BinArgs base, mcl_stats_t *st) {
+    const int64_t n = pr.n;
+    const int NB1 = kNumBins + 1;
+    int *counts, *counters, *retry_count, *err;
+    unsigned long long *bflops;
+    int32_t *lists, *gcap_col, *retry_list, *retry_in;
+    RC(scratch_t(c, "bin_counts", 4 * NB1 + 8, &counts));
+    counters = counts + NB1;
+    retry_count = counters + NB1;
+    err = retry_count + 1;
+    RC(scratch_t(c, "bin_flops", NB1, &bflops));
+    RC(scratch_t(c, "bin_lists", (size_t)NB1 * std::max<int64_t>(n, 1), &lists));
+    RC(scratch_t(c, "gcap_col", (size_t)std::max<int64_t>(n, 1), &gcap_col));
+    RC(scratch_t(c, "retry_list", (size_t)std::max<int64_t>(n, 1), &retry_list));
+    RC(scratch_t(c, "retry_in", (size_t)std::max<int64_t>(n, 1), &retry_in));
+    CK(cudaMemsetAsync(err, 0, sizeof(int), c->stream));
+
+    int64_t ncls = n;
+    const int32_t *cls_list = nullptr;
+    for (int round = 0; round < 2; round++) {
+        CK(cudaMemsetAsync(counts, 0, sizeof(int) * (2 * NB1 + 1), c->stream));
+        CK(cudaMemsetAsync(bflops, 0, sizeof(unsigned long long) * NB1, c->stream));
+        ClassifyArgs ca;
+        memset(&ca, 0, sizeof ca);
+        ca.n = ncls;
+        ca.cols = cls_list;
+        ca.flops = f;
+        ca.bcp = pr.B->col_ptr;
+        ca.cb = pr.cb;
+        ca.est = round == 0 ? est : nullptr;
+        ca.exact = round == 0 ? exact : nullptr;
+        ca.m = pr.A->nrows;
+        ca.alpha = 1.5f;
+        ca.force_bin = force_bin;
+        ca.list_stride = std::max<int64_t>(n, 1);
+        ca.bin_count = counts;
+        ca.lists = lists;
+        ca.gcap_col = gcap_col;
+        ca.bin_flops = bflops;
+        CK(launch_classify(ca, c->stream));
+        int hc[2 * 8 + 1];
+        unsigned long long hf[8];
+        RC(readback(c, counts, sizeof(int) * NB1, hc));
+        RC(readback(c, bflops, sizeof(unsigned long long) * NB1, hf));
+        if (st && round == 0) {
+            for (int b = 0; b < NB1; b++) {
+                st->bin_cols[b] += hc[b];
+                st->bin_flops[b] += (int64_t)hf[b];
+            }
+        }
+        for (int b = kNumBins; b >= 0; b--) {
+            if (hc[b] == 0) continue;
+            BinArgs a = base;
+            a.acp = pr.A->col_ptr;
+            a.arow = pr.A->row_idx;
+            a.aval = pr.A->val;
+            a.m = pr.A->nrows;
+            a.bcp = pr.B->col_ptr;
+            a.brow = pr.B->row_idx;
+            a.bval = pr.B->val;
+            a.cb = pr.cb;
+            a.flops = f;
+            a.list = lists + (int64_t)b * std::max<int64_t>(n, 1);
+            a.count = counts + b;
+            a.counter = counters + b;
+            a.retry_list = retry_list;
+            a.retry_count = retry_count;
+            a.err_flag = err;
+            if (b == kNumBins) {
+                int32_t *gcap;
+                int64_t *gcap64, *goff;
+                void *tmp;
+                RC(scratch_t(c, "gcap", (size_t)hc[b], &gcap));
+                RC(scratch_t(c, "gcap64", (size_t)hc[b], &gcap64));
+                RC(scratch_t(c, "goff", (size_t)hc[b] + 1, &goff));
+                RC(scratch(c, "scan_tmp", scan_tmp_bytes(hc[b]), &tmp));
+                CK(launch_global_layout(hc[b], a.list, gcap_col, gcap, gcap64, c->stream));
+                CK(launch_scan_i64(gcap64, goff, hc[b], tmp, c->stream));
+                int64_t gtot = 0;
+                RC(readback(c, goff + hc[b], sizeof(int64_t), &gtot));
+                int *gkeys;
+                double *gvals;
+                RC(scratch_t(c, "gkeys", (size_t)gtot, &gkeys));
+                RC(scratch_t(c, "gvals", (size_t)gtot, &gvals));
+                a.goff = goff;
+                a.gcap = gcap;
+                a.gkeys = gkeys;
+                a.gvals = gvals;
+            }
+            const int occ = std::max(1, c->occ[mode][b]);
+            const int grid = (int)std::min<int64_t>(hc[b], (int64_t)occ * c->sms);
+            CK(launch_bin(mode, b, a, grid, c->stream));
+        }
+        int nretry = 0;
+        RC(readback(c, retry_count, sizeof(int), &nretry));
+        if (nretry == 0) break;
+        if (round == 1) return fail(c, MCL_ERR_CUDA, "hash table overflow after exact re-binning");
+        if (st) st->retries += nretry;
+        CK(cudaMemcpyAsync(retry_in, retry_list, sizeof(int32_t) * nretry, cudaMemcpyDeviceToDevice,
+                           c->stream));
+        ncls = nretry;
+        cls_list = retry_in;
+    }
+    int herr = 0;
+    RC(readback(c, err, sizeof(int), &herr));
+    if (herr) return fail(c, MCL_ERR_CUDA, "device consistency check failed (code %d)", herr);
+    return MCL_OK;
+}
+
+int validate_product(mcl_ctx *c, const mcl_csc_t *A, const mcl_csc_t *B, int64_t b, int64_t e) {
+    RC(check_csc(c, A, "A"));
+    RC(check_csc(c, B, "B"));
+    if (A->ncols != B->nrows)
+        return fail(c, MCL_ERR_DIM, "A.ncols (%lld) != B.nrows (%lld)", (long long)A->ncols,
+                    (long long)B->nrows);
+    if (b < 0 || e > B->ncols || b > e) return fail(c, MCL_ERR_DIM, "bad column range [%lld,%lld)",
+                                                     (long long)b, (long long)e);
+    return MCL_OK;
+}
+
+// Exact symbolic sizes of a product's output columns (sized by a Cohen estimate).
+int symbolic_sizes(mcl_ctx *c, const Prod &pr, const int64_t *f, const float *est, int force_bin,
+                   int64_t *nnz_out, mcl_stats_t *st) {
+    CK(cudaMemsetAsync(nnz_out, 0, sizeof(int64_t) * std::max<int64_t>(pr.n, 1), c->stream));
+    BinArgs base;
+    memset(&base, 0, sizeof base);
+    base.sym_nnz = nnz_out;
+    return run_bins(c, kSym, pr, f, est, nullptr, force_bin, base, st);
+}
+
+int spgemm_impl(mcl_ctx *c, const mcl_csc_t *A, const mcl_csc_t *B, int64_t cb, int64_t ce,
+                const mcl_params_t *pin, mcl_csc_t *C, mcl_stats_t *st) {
+    mcl_params_t p;
+    if (pin) p = *pin;
+    else mcl_params_default(&p);
+    RC(check_params(c, &p));
+    RC(validate_product(c, A, B, cb, ce));
+    const int64_t n = ce - cb;
+    Prod pr{A, B, cb, n};
+    init_stats(st);
+    CK(cudaEventRecord(c->ev[0], c->stream));
+    int64_t *f, *nnzc;
+    float *est;
+    void *tmp;
+    unsigned long long *tot;
+    RC(scratch_t(c, "flops", (size_t)std::max<int64_t>(n, 1), &f));
+    RC(scratch_t(c, "est", (size_t)std::max<int64_t>(n, 1), &est));
+    RC(scratch_t(c, "nnz_sym", (size_t)std::max<int64_t>(n, 1), &nnzc));
+    RC(scratch_t(c, "tot", 4, &tot));
+    RC(scratch(c, "scan_tmp", scan_tmp_bytes(n + 1), &tmp));
+    CK(launch_flops(n, A->col_ptr, B->col_ptr, B->row_idx, cb, f, c->stream));
+    CK(cudaEventRecord(c->ev[1], c->stream));
+    RC(cohen(c, pr, p.est_keys, p.seed, est, nullptr));
+    CK(cudaEventRecord(c->ev[2], c->stream));
+    RC(symbolic_sizes(c, pr, f, est, p.force_bin, nnzc, st));
+    CK(cudaEventRecord(c->ev[3], c->stream));
+    C->col_ptr = nullptr;
+    mcl_csc_t out;
+    zero_csc(&out);
+    out.col_ptr = (int64_t *)dalloc(c, (size_t)(n + 1) * sizeof(int64_t));
+    if (!out.col_ptr) return fail(c, MCL_ERR_OOM, "cannot allocate col_ptr");
+    int rc = MCL_OK;
+    do {
+        cudaError_t e = launch_scan_i64(nnzc, out.col_ptr, n, tmp, c->stream);
+        if (e != cudaSuccess) { rc = fail(c, MCL_ERR_CUDA, "scan: %s", cudaGetErrorString(e)); break; }
+        int64_t nnz = 0;
+        if ((rc = readback(c, out.col_ptr + n, sizeof(int64_t), &nnz)) != MCL_OK) break;
+        if ((rc = alloc_rows_vals(c, &out, nnz)) != MCL_OK) break;
+        out.nrows = A->nrows;
+        out.ncols = n;
+        out.row0 = A->row0;
+        out.col0 = B->col0 + cb;
+        out.n_global = A->n_global ? A->n_global : A->nrows;
+        BinArgs base;
+        memset(&base, 0, sizeof base);
+        base.c_cp = out.col_ptr;
+        base.c_row = out.row_idx;
+        base.c_val = out.val;
+        if ((rc = run_bins(c, kNum, pr, f, nullptr, nnzc, p.force_bin, base, nullptr)) != MCL_OK) break;
+        CK(cudaEventRecord(c->ev[4], c->stream));
+        e = launch_reduce_i64(f, n, tot, c->stream);
+        if (e != cudaSuccess) { rc = fail(c, MCL_ERR_CUDA, "reduce: %s", cudaGetErrorString(e)); break; }
+        double est_tot = 0;
+        double *dsum = (double *)(tot + 1);
+        e = launch_reduce_f32(est, n, dsum, c->stream);
+        if (e != cudaSuccess) { rc = fail(c, MCL_ERR_CUDA, "reduce: %s", cudaGetErrorString(e)); break; }
+        unsigned long long hv[2];
+        if ((rc = readback(c, tot, 2 * sizeof(unsigned long long), hv)) != MCL_OK) break;
+        memcpy(&est_tot, &hv[1], sizeof(double));
+        if (st) {
+            st->flops = (int64_t)hv[0];
+            st->nnz_in = A->nnz;
+            st->nnz_unpruned = nnz;
+            st->nnz_out = nnz;
+            st->est_nnz = est_tot;
+            st->cf = nnz > 0 ? (double)hv[0] / (double)nnz : 0.0;
+            st->estimator_used = 1;
+            st->ms[0] = elapsed(c, 0, 1);
+            st->ms[1] = elapsed(c, 1, 2);
+            st->ms[2] = elapsed(c, 2, 3);
+            st->ms[3] = elapsed(c, 3, 4);
+            st->ms[6] = elapsed(c, 0, 4);
+            st->peak_bytes = (int64_t)c->peak;
+        }
+        *C = out;
+        return MCL_OK;
+    } while (0);
+    dfree(c, out.col_ptr, 0);
+    dfree(c, out.row_idx, 0);
+    dfree(c, out.val, 0);
+    zero_csc(C);
+    return rc;
+}
+
+// Scan per-column counts into a fresh CSC and copy the staged columns into it.
+int assemble(mcl_ctx *c, int64_t nrows, int64_t n, const int64_t *cnt, const int64_t *soff,
+             const int32_t *srow, const float *sval, mcl_csc_t *out, int64_t *nnz_out) {
+    void *tmp;
+    RC(scratch(c, "scan_tmp", scan_tmp_bytes(n + 1), &tmp));
+    zero_csc(out);
+    out->col_ptr = (int64_t *)dalloc(c, (size_t)(n + 1) * sizeof(int64_t));
+    if (!out->col_ptr) return fail(c, MCL_ERR_OOM, "cannot allocate col_ptr");
+    CK(launch_scan_i64(cnt, out->col_ptr, n, tmp, c->stream));
+    int64_t nnz = 0;
+    RC(readback(c, out->col_ptr + n, sizeof(int64_t), &nnz));
+    int rc = alloc_rows_vals(c, out, nnz);
+    if (rc != MCL_OK) {
+        dfree(c, out->col_ptr, 0);
+        dfree(c, out->row_idx, 0);
+        dfree(c, out->val, 0);
+        zero_csc(out);
+        return rc;
+    }
+    out->nrows = nrows;
+    out->ncols = n;
+    out->n_global = nrows;
+    CK(launch_copy_cols(n, cnt, soff, srow, sval, out->col_ptr, out->row_idx, out->val, c->stream));
+    *nnz_out = nnz;
+    return MCL_OK;
+}
+
+}  // namespace
+
+// ====================================================================== public API
+extern "C" {
+
+int mcl_version(void) { return MCLX_VERSION; }
+
+void mcl_params_default(mcl_params_t *p) {
+    if (!p) return;
+    memset(p, 0, sizeof *p);
+    p->inflation = 2.0;
+    p->prune_threshold = 1e-4;
+    p->select_k = 1100;
+    p->recover_k = 1400;
+    p->recover_pct = 0.9;
+    p->chaos_eps = 1e-3;
+    p->est_keys = 10;
+    p->est_cf_threshold = 2.0;
+    p->seed = 0x5eed;
+    p->mem_safety = 0.9;
+    p->estimator = 0;
+    p->force_bin = -1;
+}
+
+int mcl_ctx_create(mcl_ctx_t *out, int device, void *stream, mcl_alloc_fn alloc,
+                   mcl_free_fn free_fn, void *alloc_state) {
+    if (!out) return MCL_ERR_INVALID_ARG;
+    *out = nullptr;
+    if ((alloc == nullptr) != (free_fn == nullptr)) return MCL_ERR_INVALID_ARG;
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) {
+        cudaGetLastError();
+        return MCL_ERR_CUDA;
+    }
+    if (!(prop.major == 10 && prop.minor == 0)) return MCL_ERR_UNSUPPORTED_DEVICE;
+    if (cudaSetDevice(device) != cudaSuccess) return MCL_ERR_CUDA;
+    mcl_ctx *c = new mcl_ctx();
+    c->device = device;
+    c->stream = (cudaStream_t)stream;
+    c->alloc = alloc;
+    c->free_fn = free_fn;
+    c->state = alloc_state;
+    c->sms = prop.multiProcessorCount;
+    if (cudaMallocHost(&c->pin, 4096) != cudaSuccess) {
+        delete c;
+        return MCL_ERR_CUDA;
+    }
+    for (int i = 0; i < 8; i++) cudaEventCreate(&c->ev[i]);
+    for (int m = 0; m < 3; m++)
+        for (int b = 0; b <= kNumBins; b++) c->occ[m][b] = bin_occupancy(m, b);
+    if (cudaGetLastError() != cudaSuccess) {
+        mcl_ctx_destroy(c);
+        return MCL_ERR_CUDA;
+    }
+    *out = c;
+    return MCL_OK;
+}
+
+int mcl_ctx_set_stream(mcl_ctx_t c, void *stream) {
+    if (!c) return MCL_ERR_INVALID_ARG;
+    c->stream = (cudaStream_t)stream;
+    return MCL_OK;
+}
+
+int mcl_ctx_destroy(mcl_ctx_t c) {
+    if (!c) return MCL_ERR_INVALID_ARG;
+    cudaSetDevice(c->device);
+    for (auto &kv : c->scratch) dfree(c, kv.second.p, kv.second.bytes);
+    cudaStreamSynchronize(c->stream);
+    for (int i = 0; i < 8; i++)
+        if (c->ev[i]) cudaEventDestroy(c->ev[i]);
+    if (c->pin) cudaFreeHost(c->pin);
+    delete c;
+    return MCL_OK;
+}
+
+const char *mcl_last_error(mcl_ctx_t c) { return c ? c->err.c_str() : "null context"; }
+
+int mcl_csc_release(mcl_ctx_t c, mcl_csc_t *m) {
+    if (!c || !m) return MCL_ERR_INVALID_ARG;
+    dfree(c, m->col_ptr, (size_t)(m->ncols + 1) * sizeof(int64_t));
+    dfree(c, m->row_idx, (size_t)m->nnz * sizeof(int32_t));
+    dfree(c, m->val, (size_t)m->nnz * sizeof(float));
+    zero_csc(m);
+    return MCL_OK;
+}
+
+int mcl_preprocess(mcl_ctx_t c, const mcl_csc_t *G, int add_loops, mcl_csc_t *A_out) {
+    if (!c || !A_out) return MCL_ERR_INVALID_ARG;
+    zero_csc(A_out);
+    cudaSetDevice(c->device);
+    RC(check_csc(c, G, "G"));
+    if (G->nrows != G->ncols) return fail(c, MCL_ERR_DIM, "G must be square");
+    const int64_t n = G->ncols;
+    int64_t *cnt;
+    void *tmp;
+    RC(scratch_t(c, "pre_cnt", (size_t)std::max<int64_t>(n, 1), &cnt));
+    RC(scratch(c, "scan_tmp", scan_tmp_bytes(n + 1), &tmp));
+    CK(launch_pre_count(n, G->col_ptr, G->row_idx, add_loops, cnt, c->stream));
+    mcl_csc_t out;
+    zero_csc(&out);
+    out.col_ptr = (int64_t *)dalloc(c, (size_t)(n + 1) * sizeof(int64_t));
+    if (!out.col_ptr) return fail(c, MCL_ERR_OOM, "col_ptr");
+    CK(launch_scan_i64(cnt, out.col_ptr, n, tmp, c->stream));
+    int64_t nnz = 0;
+    RC(readback(c, out.col_ptr + n, sizeof(int64_t), &nnz));
+    RC(alloc_rows_vals(c, &out, nnz));
+    out.nrows = n;
+    out.ncols = n;
+    out.n_global = n;
+    CK(launch_pre_fill(n, G->col_ptr, G->row_idx, G->val, add_loops, out.col_ptr, out.row_idx,
+                       out.val, c->stream));
+    *A_out = out;
+    return MCL_OK;
+}
+
+int mcl_flops(mcl_ctx_t c, const mcl_csc_t *A, const mcl_csc_t *B, int64_t *flops_dev,
+              int64_t *total) {
+    if (!c) return MCL_ERR_INVALID_ARG;
+    cudaSetDevice(c->device);
+    RC(validate_product(c, A, B, 0, B ? B->ncols : 0));
+    const int64_t n = B->ncols;
+    int64_t *f = flops_dev;
+    if (!f) RC(scratch_t(c, "flops", (size_t)std::max<int64_t>(n, 1), &f));
+    CK(launch_flops(n, A->col_ptr, B->col_ptr, B->row_idx, 0, f, c->stream));
+    if (total) {
+        unsigned long long *tot;
+        RC(scratch_t(c, "tot", 4, &tot));
+        CK(launch_reduce_i64(f, n, tot, c->stream));
+        unsigned long long h = 0;
+        RC(readback(c, tot, sizeof h, &h));
+        *total = (int64_t)h;
+    }
+    return MCL_OK;
+}
+
+int mcl_estimate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_csc_t *B, int32_t r, uint64_t seed,
+                 float *est_dev, float *keys_dev, double *total) {
+    if (!c || !est_dev) return c ? fail(c, MCL_ERR_INVALID_ARG, "est_dev is NULL") : MCL_ERR_INVALID_ARG;
+    cudaSetDevice(c->device);
+    if (r < 2 || r > 16) return fail(c, MCL_ERR_INVALID_ARG, "r must be in [2,16]");
+    RC(validate_product(c, A, B, 0, B ? B->ncols : 0));
+    Prod pr{A, B, 0, B->ncols};
+    RC(cohen(c, pr, r, seed, est_dev, keys_dev));
+    if (total) {
+        unsigned long long *tot;
+        RC(scratch_t(c, "tot", 4, &tot));
+        double *d = (double *)tot;
+        CK(launch_reduce_f32(est_dev, B->ncols, d, c->stream));
+        RC(readback(c, d, sizeof(double), total));
+    }
+    return MCL_OK;
+}
+
+int mcl_symbolic(mcl_ctx_t c, const mcl_csc_t *A, const mcl_csc_t *B, int64_t *nnz_dev,
+                 int64_t *total) {
+    if (!c || !nnz_dev) return c ? fail(c, MCL_ERR_INVALID_ARG, "nnz_dev is NULL") : MCL_ERR_INVALID_ARG;
+    cudaSetDevice(c->device);
+    RC(validate_product(c, A, B, 0, B ? B->ncols : 0));
+    mcl_params_t p;
+    mcl_params_default(&p);
+    const int64_t n = B->ncols;
+    Prod pr{A, B, 0, n};
+    int64_t *f;
+    float *est;
+    RC(scratch_t(c, "flops", (size_t)std::max<int64_t>(n, 1), &f));
+    RC(scratch_t(c, "est", (size_t)std::max<int64_t>(n, 1), &est));
+    CK(launch_flops(n, A->col_ptr, B->col_ptr, B->row_idx, 0, f, c->stream));
+    RC(cohen(c, pr, p.est_keys, p.seed, est, nullptr));
+    RC(symbolic_sizes(c, pr, f, est, -1, nnz_dev, nullptr));
+    if (total) {
+        unsigned long long *tot;
+        RC(scratch_t(c, "tot", 4, &tot));
+        CK(launch_reduce_i64(nnz_dev, n, tot, c->stream));
+        unsigned long long h = 0;
+        RC(readback(c, tot, sizeof h, &h));
+        *total = (int64_t)h;
+    }
+    return MCL_OK;
+}
+
+int mcl_spgemm(mcl_ctx_t c, const mcl_csc_t *A, const mcl_csc_t *B, int64_t col_begin,
+               int64_t col_end, const mcl_params_t *p, mcl_csc_t *C_out, mcl_stats_t *st) {
+    if (!c || !C_out) return MCL_ERR_INVALID_ARG;
+    zero_csc(C_out);
+    cudaSetDevice(c->device);
+    return spgemm_impl(c, A, B, col_begin, col_end, p, C_out, st);
+}
+
+int mcl_expand(mcl_ctx_t c, const mcl_csc_t *A, int64_t col_begin, int64_t col_end,
+               const mcl_params_t *p, mcl_csc_t *C_out, mcl_stats_t *st) {
+    if (!c || !C_out) return MCL_ERR_INVALID_ARG;
+    zero_csc(C_out);
+    cudaSetDevice(c->device);
+    RC(check_csc(c, A, "A"));
+    if (A->nrows != A->ncols) return fail(c, MCL_ERR_DIM, "expansion needs a square A");
+    return spgemm_impl(c, A, A, col_begin, col_end, p, C_out, st);
+}
+
+int mcl_prune_inflate(mcl_ctx_t c, const mcl_csc_t *C, const mcl_params_t *pin, mcl_csc_t *A_next,
+                      float *chaos_dev, mcl_stats_t *st) {
+    if (!c) return MCL_ERR_INVALID_ARG;
+    if (!A_next || !pin) return fail(c, MCL_ERR_INVALID_ARG, "NULL argument");
+    zero_csc(A_next);
+    cudaSetDevice(c->device);
+    RC(check_params(c, pin));
+    RC(check_csc(c, C, "C"));
+    init_stats(st);
+    const int64_t n = C->ncols;
+    const PruneParams pp = prune_params(pin);
+    CK(cudaEventRecord(c->ev[0], c->stream));
+    int64_t *kcap, *soff, *cnt;
+    float *chaos, *cmax;
+    int32_t *srow;
+    float *sval;
+    void *tmp;
+    RC(scratch_t(c, "kcap", (size_t)std::max<int64_t>(n, 1), &kcap));
+    RC(scratch_t(c, "soff", (size_t)n + 1, &soff));
+    RC(scratch_t(c, "scnt", (size_t)std::max<int64_t>(n, 1), &cnt));
+    RC(scratch_t(c, "chaos", (size_t)std::max<int64_t>(n, 1), &chaos));
+    RC(scratch_t(c, "chaos_max", 4, &cmax));
+    RC(scratch(c, "scan_tmp", scan_tmp_bytes(n + 1), &tmp));
+    CK(launch_kcap_cp(n, C->col_ptr, pp.kmax, kcap, c->stream));
+    CK(launch_scan_i64(kcap, soff, n, tmp, c->stream));
+    int64_t stot = 0;
+    RC(readback(c, soff + n, sizeof(int64_t), &stot));
+    RC(scratch_t(c, "s_row", (size_t)std::max<int64_t>(stot, 1), &srow));
+    RC(scratch_t(c, "s_val", (size_t)std::max<int64_t>(stot, 1), &sval));
+    CK(cudaMemsetAsync(cmax, 0, sizeof(float), c->stream));
+    const int grid = (int)std::min<int64_t>(std::max<int64_t>(n, 1), (int64_t)c->sms * 8);
+    CK(launch_prune(n, C->col_ptr, C->row_idx, C->val, soff, srow, sval, cnt,
+                    chaos_dev ? chaos_dev : chaos, cmax, pp, grid, c->stream));
+    CK(cudaEventRecord(c->ev[1], c->stream));
+    int64_t nnz = 0;
+    RC(assemble(c, C->nrows, n, cnt, soff, srow, sval, A_next, &nnz));
+    A_next->row0 = C->row0;
+    A_next->col0 = C->col0;
+    A_next->n_global = C->n_global ? C->n_global : C->nrows;
+    CK(cudaEventRecord(c->ev[2], c->stream));
+    float hmax = 0.f;
+    RC(readback(c, cmax, sizeof(float), &hmax));
+    if (st) {
+        st->nnz_in = C->nnz;
+        st->nnz_unpruned = C->nnz;
+        st->nnz_out = nnz;
+        st->chaos = hmax;
+        st->ms[4] = elapsed(c, 0, 1);
+        st->ms[5] = elapsed(c, 1, 2);
+        st->ms[6] = elapsed(c, 0, 2);
+        st->peak_bytes = (int64_t)c->peak;
+    }
+    return MCL_OK;
+}
+
+int mcl_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, mcl_csc_t *A_next,
+                mcl_stats_t *st) {
+    if (!c) return MCL_ERR_INVALID_ARG;
+    if (!A_next || !pin) return fail(c, MCL_ERR_INVALID_ARG, "NULL argument");
+    zero_csc(A_next);
+    cudaSetDevice(c->device);
+    RC(check_params(c, pin));
+    RC(check_csc(c, A, "A"));
+    if (A->nrows != A->ncols) return fail(c, MCL_ERR_DIM, "mcl_iterate needs a square A");
+    init_stats(st);
+    const mcl_params_t &p = *pin;
+    const int64_t n = A->ncols;
+    Prod pr{A, A, 0, n};
+    const PruneParams pp = prune_params(pin);
+    CK(cudaEventRecord(c->ev[0], c->stream));
+    int64_t *f, *kcap, *soff, *cnt, *nnzc = nullptr;
+    float *est, *chaos, *cmax;
+    int32_t *srow;
+    float *sval;
+    unsigned long long *tot;
+    void *tmp;
+    RC(scratch_t(c, "flops", (size_t)std::max<int64_t>(n, 1), &f));
+    RC(scratch_t(c, "est", (size_t)std::max<int64_t>(n, 1), &est));
+    RC(scratch_t(c, "kcap", (size_t)std::max<int64_t>(n, 1), &kcap));
+    RC(scratch_t(c, "soff", (size_t)n + 1, &soff));
+    RC(scratch_t(c, "scnt", (size_t)std::max<int64_t>(n, 1), &cnt));
+    RC(scratch_t(c, "chaos", (size_t)std::max<int64_t>(n, 1), &chaos));
+    RC(scratch_t(c, "chaos_max", 4, &cmax));
+    RC(scratch_t(c, "tot", 4, &tot));
+    RC(scratch(c, "scan_tmp", scan_tmp_bytes(n + 1), &tmp));
+
+    // a1: flops and the total
+    CK(launch_flops(n, A->col_ptr, A->col_ptr, A->row_idx, 0, f, c->stream));
+    CK(launch_reduce_i64(f, n, tot, c->stream));
+    CK(cudaEventRecord(c->ev[1], c->stream));
+    // a2: Cohen estimate, then the P:1076-1077 policy
+    RC(cohen(c, pr, p.est_keys, p.seed, est, nullptr));
+    double *dsum = (double *)(tot + 1);
+    CK(launch_reduce_f32(est, n, dsum, c->stream));
+    unsigned long long hv[2];
+    RC(readback(c, tot, sizeof hv, hv));
+    double est_tot;
+    memcpy(&est_tot, &hv[1], sizeof(double));
+    const int64_t flops = (int64_t)hv[0];
+    const double cf_est = est_tot > 0 ? (double)flops / est_tot : 0.0;
+    int use_exact = p.estimator == 1 || (p.estimator == 0 && cf_est < p.est_cf_threshold);
+    CK(cudaEventRecord(c->ev[2], c->stream));
+    // a3: exact symbolic sizes when the policy asks for them
+    if (use_exact) {
+        RC(scratch_t(c, "nnz_sym", (size_t)std::max<int64_t>(n, 1), &nnzc));
+        RC(symbolic_sizes(c, pr, f, est, p.force_bin, nnzc, nullptr));
+    }
+    CK(cudaEventRecord(c->ev[3], c->stream));
+    // staging slots of the pruned columns
+    CK(launch_kcap(n, f, A->nrows, pp.kmax, kcap, c->stream));
+    CK(launch_scan_i64(kcap, soff, n, tmp, c->stream));
+    int64_t stot = 0;
+    RC(readback(c, soff + n, sizeof(int64_t), &stot));
+    RC(scratch_t(c, "s_row", (size_t)std::max<int64_t>(stot, 1), &srow));
+    RC(scratch_t(c, "s_val", (size_t)std::max<int64_t>(stot, 1), &sval));
+    CK(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * std::max<int64_t>(n, 1), c->stream));
+    CK(cudaMemsetAsync(chaos, 0, sizeof(float) * std::max<int64_t>(n, 1), c->stream));
+    CK(cudaMemsetAsync(cmax, 0, sizeof(float), c->stream));
+    // a4-a7: fused numeric SpGEMM + select / prune / recover / inflate / renormalise
+    BinArgs base;
+    memset(&base, 0, sizeof base);
+    base.soff = soff;
+    base.s_row = srow;
+    base.s_val = sval;
+    base.s_cnt = cnt;
+    base.chaos = chaos;
+    base.chaos_max = cmax;
+    base.pp = pp;
+    if (st) {
+        for (int b = 0; b <= kNumBins; b++) st->bin_cols[b] = st->bin_flops[b] = 0;
+    }
+    RC(run_bins(c, kFused, pr, f, use_exact ? nullptr : est, use_exact ? nnzc : nullptr,
+                p.force_bin, base, st));
+    CK(cudaEventRecord(c->ev[4], c->stream));
+    // a8: assemble A_next
+    int64_t nnz = 0;
+    RC(assemble(c, A->nrows, n, cnt, soff, srow, sval, A_next, &nnz));
+    A_next->row0 = A->row0;
+    A_next->col0 = A->col0;
+    A_next->n_global = A->n_global ? A->n_global : A->nrows;
+    CK(cudaEventRecord(c->ev[5], c->stream));
+    float hmax = 0.f;
+    RC(readback(c, cmax, sizeof(float), &hmax));
+    if (st) {
+        st->flops = flops;
+        st->nnz_in = A->nnz;
+        st->nnz_out = nnz;
+        st->est_nnz = est_tot;
+        st->cf = cf_est;
+        st->chaos = hmax;
+        st->estimator_used = use_exact ? 1 : 2;
+        st->ms[0] = elapsed(c, 0, 1);
+        st->ms[1] = elapsed(c, 1, 2);
+        st->ms[2] = elapsed(c, 2, 3);
+        st->ms[3] = elapsed(c, 3, 4);
+        st->ms[5] = elapsed(c, 4, 5);
+        st->ms[6] = elapsed(c, 0, 5);
+        st->peak_bytes = (int64_t)c->peak;
+    }
+    return MCL_OK;
+}
+
+int mcl_clusters(mcl_ctx_t c, const mcl_csc_t *A, int32_t *labels_dev, int64_t *ncl) {
+    if (!c) return MCL_ERR_INVALID_ARG;
+    if (!labels_dev) return fail(c, MCL_ERR_INVALID_ARG, "labels_dev is NULL");
+    cudaSetDevice(c->device);
+    RC(check_csc(c, A, "A"));
+    if (A->nrows != A->ncols) return fail(c, MCL_ERR_DIM, "clusters need a square A");
+    const int64_t n = A->ncols;
+    int32_t *parent;
+    int64_t *flag, *rank;
+    void *tmp;
+    RC(scratch_t(c, "cc_parent", (size_t)std::max<int64_t>(n, 1), &parent));
+    RC(scratch_t(c, "cc_flag", (size_t)std::max<int64_t>(n, 1), &flag));
+    RC(scratch_t(c, "cc_rank", (size_t)n + 1, &rank));
+    RC(scratch(c, "scan_tmp", scan_tmp_bytes(n + 1), &tmp));
+    CK(launch_cc(n, A->col_ptr, A->row_idx, parent, flag, rank, tmp, labels_dev, c->stream));
+    int64_t k = 0;
+    RC(readback(c, rank + n, sizeof(int64_t), &k));
+    if (ncl) *ncl = k;
+    return MCL_OK;
+}
+
+int mcl_merge(mcl_ctx_t c, int32_t L, const mcl_csc_t *lists, mcl_csc_t *out) {
+    if (!c) return MCL_ERR_INVALID_ARG;
+    (void)L;
+    (void)lists;
+    zero_csc(out);
+    return fail(c, MCL_ERR_NOT_IMPLEMENTED, "mcl_merge: not implemented yet");
+}
+
+}  // extern "C"

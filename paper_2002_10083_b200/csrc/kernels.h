@@ -1,0 +1,119 @@
+// kernels.h -- host-side launch wrappers for the libmclx kernels (internal header).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "mclx_dev.cuh"
+
+namespace mclx {
+
+// Shared-memory bins: table capacity (slots) and CTA size.  Bin kNumBins is the
+// global-memory (fp64) bin.  A column goes to the smallest bin whose table holds
+// its size bound at load factor <= 1/2 (kLoadNum/kLoadDen).
+constexpr int kNumBins = 6;
+constexpr int kBinCap[kNumBins] = {512, 1024, 2048, 4096, 8192, 16384};
+constexpr int kBinThreads[kNumBins] = {64, 64, 128, 256, 256, 512};
+constexpr int kGlobalThreads = 512;
+__host__ __device__ constexpr int bin_cap(int b) {
+    return b == 0 ? 512 : b == 1 ? 1024 : b == 2 ? 2048 : b == 3 ? 4096 : b == 4 ? 8192 : 16384;
+}
+constexpr int kFp64Terms = 16384;  // nnz(B_*j) above which a column accumulates in fp64 (T)
+
+enum Mode { kSym = 0, kNum = 1, kFused = 2 };
+
+struct BinArgs {
+    // operands: C = A * B[:, cb : cb + ncols_out)
+    const int64_t *acp;
+    const int32_t *arow;
+    const float *aval;
+    int64_t m;
+    const int64_t *bcp;
+    const int32_t *brow;
+    const float *bval;
+    int64_t cb;
+    const int64_t *flops;  // [ncols_out]
+    // work list of this bin
+    const int32_t *list;
+    const int *count;
+    int *counter;
+    // global bin layout (per list index)
+    const int64_t *goff;
+    const int32_t *gcap;
+    int *gkeys;
+    double *gvals;
+    // outputs
+    int64_t *sym_nnz;                                   // kSym
+    const int64_t *c_cp;                                // kNum
+    int32_t *c_row;
+    float *c_val;
+    const int64_t *soff;                                // kFused
+    int32_t *s_row;
+    float *s_val;
+    int64_t *s_cnt;
+    float *chaos;
+    float *chaos_max;
+    int32_t *retry_list;
+    int *retry_count;
+    int *err_flag;
+    PruneParams pp;
+};
+
+// One launch of bin `bin` (0..kNumBins) in mode `mode`; grid chosen from occupancy.
+cudaError_t launch_bin(int mode, int bin, const BinArgs &a, int grid, cudaStream_t s);
+// Max resident CTAs per SM for (mode, bin); also sets the dynamic smem attribute.
+int bin_occupancy(int mode, int bin);
+size_t bin_smem_bytes(int mode, int bin);
+
+// misc kernels (kernels_misc.cu)
+cudaError_t launch_flops(int64_t ncols, const int64_t *acp, const int64_t *bcp,
+                         const int32_t *brow, int64_t cb, int64_t *f, cudaStream_t s);
+cudaError_t launch_reduce_i64(const int64_t *x, int64_t n, unsigned long long *out, cudaStream_t s);
+cudaError_t launch_reduce_f32(const float *x, int64_t n, double *out, cudaStream_t s);
+// exclusive scan of in[0,n) into out[0,n], out[n] = total.  tmp: >= scan_tmp_bytes(n)
+size_t scan_tmp_bytes(int64_t n);
+cudaError_t launch_scan_i64(const int64_t *in, int64_t *out, int64_t n, void *tmp, cudaStream_t s);
+struct ClassifyArgs {
+    int64_t n;               // number of columns to classify
+    const int32_t *cols;     // optional explicit column list (retry), else 0..n-1
+    const int64_t *flops;
+    const int64_t *bcp;
+    int64_t cb;
+    const float *est;        // optional
+    const int64_t *exact;    // optional
+    int64_t m;
+    float alpha;
+    int force_bin;
+    int64_t list_stride;     // columns per bin list
+    int *bin_count;          // [kNumBins + 1]
+    int32_t *lists;          // [(kNumBins + 1) * list_stride]
+    int32_t *gcap_col;       // [ncols_out]
+    unsigned long long *bin_flops;  // [kNumBins + 1]
+};
+cudaError_t launch_classify(const ClassifyArgs &c, cudaStream_t s);
+cudaError_t launch_global_layout(int count, const int32_t *list, const int32_t *gcap_col,
+                                 int32_t *gcap, int64_t *gcap64, cudaStream_t s);
+cudaError_t launch_kcap(int64_t ncols, const int64_t *flops, int64_t m, int kmax, int64_t *kcap,
+                        cudaStream_t s);
+cudaError_t launch_kcap_cp(int64_t ncols, const int64_t *cp, int kmax, int64_t *kcap,
+                           cudaStream_t s);
+cudaError_t launch_copy_cols(int64_t ncols, const int64_t *cnt, const int64_t *soff,
+                             const int32_t *srow, const float *sval, const int64_t *cp,
+                             int32_t *orow, float *oval, cudaStream_t s);
+cudaError_t launch_prune(int64_t ncols, const int64_t *ccp, const int32_t *crow, const float *cval,
+                         const int64_t *soff, int32_t *srow, float *sval, int64_t *scnt,
+                         float *chaos, float *chaos_max, const PruneParams &pp, int grid,
+                         cudaStream_t s);
+cudaError_t launch_cohen_keys(int64_t m, int64_t row0, int r, uint64_t seed, float *X,
+                              float *keys_out, cudaStream_t s);
+cudaError_t launch_cohen_min(int64_t ncols, const int64_t *cp, const int32_t *row, int64_t c0,
+                             const float *in, int r, float *out, float *est, cudaStream_t s);
+cudaError_t launch_pre_count(int64_t n, const int64_t *gcp, const int32_t *grow, int add_loops,
+                             int64_t *cnt, cudaStream_t s);
+cudaError_t launch_pre_fill(int64_t n, const int64_t *gcp, const int32_t *grow, const float *gw,
+                            int add_loops, const int64_t *cp, int32_t *row, float *val,
+                            cudaStream_t s);
+cudaError_t launch_cc(int64_t n, const int64_t *cp, const int32_t *row, int32_t *parent,
+                      int64_t *flag, int64_t *rank, void *scan_tmp, int32_t *labels,
+                      cudaStream_t s);
+
+}  // namespace mclx

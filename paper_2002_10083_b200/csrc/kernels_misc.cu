@@ -1,0 +1,615 @@
+// kernels_misc.cu -- the non-SpGEMM kernels of the path:
+//   flop count, binning, scans / reductions, the
+//   standalone prune-inflate pass (Q1-Q9), assembly of the pruned CSC,
+//   Cohen's estimator, Alg. 1 line 1 preprocessing and the
+//   connected components of Alg. 1 line 6.
+#include "kernels.h"
+
+namespace mclx {
+
+// ------------------------------------------------------------------ flops
+// f_j = sum_{k in inds(B_*j)} nnz(A_*k).  One warp per column.
+__global__ void k_flops(int64_t ncols, const int64_t *__restrict__ acp,
+                        const int64_t *__restrict__ bcp, const int32_t *__restrict__ brow,
+                        int64_t cb, int64_t *__restrict__ f) {
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = lane_id();
+    for (int64_t col = w; col < ncols; col += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t q0 = bcp[cb + col], q1 = bcp[cb + col + 1];
+        int64_t s = 0;
+        for (int64_t q = q0 + lane; q < q1; q += 32) {
+            const int k = __ldg(brow + q);
+            s += __ldg(acp + k + 1) - __ldg(acp + k);
+        }
+        s = warp_sum(s);
+        if (lane == 0) f[col] = s;
+    }
+}
+
+cudaError_t launch_flops(int64_t ncols, const int64_t *acp, const int64_t *bcp,
+                         const int32_t *brow, int64_t cb, int64_t *f, cudaStream_t s) {
+    if (ncols <= 0) return cudaSuccess;
+    int64_t blocks = (ncols * 32 + 255) / 256;
+    if (blocks > 148 * 64) blocks = 148 * 64;
+    k_flops<<<(int)blocks, 256, 0, s>>>(ncols, acp, bcp, brow, cb, f);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ reductions
+__global__ void k_reduce_i64(const int64_t *__restrict__ x, int64_t n, unsigned long long *out) {
+    __shared__ int64_t sh[8];
+    int64_t s = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        s += x[i];
+    s = block_sum<256, int64_t>(s, sh);
+    if (threadIdx.x == 0) atomicAdd(out, (unsigned long long)s);
+}
+__global__ void k_reduce_f32(const float *__restrict__ x, int64_t n, double *out) {
+    __shared__ double sh[8];
+    double s = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        s += (double)x[i];
+    s = block_sum<256, double>(s, sh);
+    if (threadIdx.x == 0) atomicAdd(out, s);
+}
+static int red_grid(int64_t n) {
+    int64_t b = (n + 255) / 256;
+    if (b > 148 * 4) b = 148 * 4;
+    return b < 1 ? 1 : (int)b;
+}
+cudaError_t launch_reduce_i64(const int64_t *x, int64_t n, unsigned long long *out, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(out, 0, sizeof(unsigned long long), s);
+    if (e != cudaSuccess) return e;
+    k_reduce_i64<<<red_grid(n), 256, 0, s>>>(x, n, out);
+    return cudaGetLastError();
+}
+cudaError_t launch_reduce_f32(const float *x, int64_t n, double *out, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(out, 0, sizeof(double), s);
+    if (e != cudaSuccess) return e;
+    k_reduce_f32<<<red_grid(n), 256, 0, s>>>(x, n, out);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ exclusive scan (int64)
+// Reduce-then-scan: tiles of 4096 elements (1024 threads x 4), tile sums scanned
+// recursively, then each tile re-scanned with its offset.
+constexpr int kScanNT = 1024, kScanIPT = 4, kScanTile = kScanNT * kScanIPT;
+
+__device__ __forceinline__ int64_t block_excl_scan64(int64_t v, int64_t *sh, int64_t &total) {
+    int64_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane_id() >= o) x += y;
+    }
+    __syncthreads();
+    if (lane_id() == 31) sh[warp_id()] = x;
+    __syncthreads();
+    if (warp_id() == 0) {
+        int64_t w = sh[lane_id()];
+        int64_t z = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int64_t y = __shfl_up_sync(0xffffffffu, z, o);
+            if (lane_id() >= o) z += y;
+        }
+        sh[lane_id()] = z - w;
+        if (lane_id() == 31) sh[32] = z;
+    }
+    __syncthreads();
+    total = sh[32];
+    return sh[warp_id()] + x - v;
+}
+
+__global__ void __launch_bounds__(kScanNT) k_scan_tiles(const int64_t *__restrict__ in, int64_t n,
+                                                        int64_t *__restrict__ tile_sums) {
+    __shared__ int64_t sh[33];
+    const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanIPT;
+    int64_t s = 0;
+#pragma unroll
+    for (int i = 0; i < kScanIPT; i++)
+        if (base + i < n) s += in[base + i];
+    int64_t tot;
+    block_excl_scan64(s, sh, tot);
+    if (threadIdx.x == 0) tile_sums[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(kScanNT) k_scan_apply(const int64_t *__restrict__ in, int64_t n,
+                                                        const int64_t *__restrict__ tile_off,
+                                                        int64_t *__restrict__ out) {
+    __shared__ int64_t sh[33];
+    const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanIPT;
+    int64_t v[kScanIPT];
+    int64_t s = 0;
+#pragma unroll
+    for (int i = 0; i < kScanIPT; i++) {
+        v[i] = (base + i < n) ? in[base + i] : 0;
+        s += v[i];
+    }
+    int64_t tot;
+    int64_t off = block_excl_scan64(s, sh, tot) + tile_off[blockIdx.x];
+#pragma unroll
+    for (int i = 0; i < kScanIPT; i++) {
+        if (base + i < n) out[base + i] = off;
+        off += v[i];
+    }
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == kScanNT - 1) out[n] = off;
+}
+
+size_t scan_tmp_bytes(int64_t n) {
+    size_t b = 0;
+    int64_t t = (n + kScanTile - 1) / kScanTile;
+    while (t > 1) {
+        b += (size_t)(t + 1) * 2 * sizeof(int64_t);
+        t = (t + kScanTile - 1) / kScanTile;
+    }
+    return b + 64;
+}
+
+cudaError_t launch_scan_i64(const int64_t *in, int64_t *out, int64_t n, void *tmp, cudaStream_t s) {
+    if (n <= 0) return cudaMemsetAsync(out, 0, sizeof(int64_t), s);
+    const int64_t tiles = (n + kScanTile - 1) / kScanTile;
+    if (tiles == 1) {
+        int64_t *off = (int64_t *)tmp;
+        cudaError_t e = cudaMemsetAsync(off, 0, sizeof(int64_t), s);
+        if (e != cudaSuccess) return e;
+        k_scan_apply<<<1, kScanNT, 0, s>>>(in, n, off, out);
+        return cudaGetLastError();
+    }
+    int64_t *sums = (int64_t *)tmp;
+    int64_t *offs = sums + tiles + 1;
+    k_scan_tiles<<<(unsigned)tiles, kScanNT, 0, s>>>(in, n, sums);
+    cudaError_t e = launch_scan_i64(sums, offs, tiles, (void *)(offs + tiles + 1), s);
+    if (e != cudaSuccess) return e;
+    k_scan_apply<<<(unsigned)tiles, kScanNT, 0, s>>>(in, n, offs, out);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ binning
+// Size bound of output column j: ub = min(f_j, m) (exact upper bound); need = the
+// exact symbolic size when known, else min(ub, alpha * Cohen estimate + 16), else ub.
+// Bin = smallest shared-memory table with need <= cap/2; columns whose entries sum
+// more than kFp64Terms products per output entry go to the fp64 global bin (T).
+__global__ void k_classify(ClassifyArgs c) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < c.n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t col = c.cols ? c.cols[i] : i;
+        const int64_t f = c.flops[col];
+        if (f == 0) continue;
+        const int64_t ub = f < c.m ? f : c.m;
+        int64_t need = ub;
+        if (c.exact) {
+            need = c.exact[col];
+        } else if (c.est) {
+            double e = ceil((double)c.alpha * (double)c.est[col]) + 16.0;
+            if (e < (double)need) need = (int64_t)e;
+        }
+        const int64_t nb = c.bcp[c.cb + col + 1] - c.bcp[c.cb + col];
+        int b = 0;
+        while (b < kNumBins && need * 2 > bin_cap(b)) b++;
+        if (nb > kFp64Terms) b = kNumBins;
+        if (c.force_bin > b && c.force_bin <= kNumBins) b = c.force_bin;
+        const int pos = atomicAdd(&c.bin_count[b], 1);
+        c.lists[(int64_t)b * c.list_stride + pos] = (int32_t)col;
+        atomicAdd(&c.bin_flops[b], (unsigned long long)f);
+        if (b == kNumBins) {
+            int64_t cap = 64;
+            while (cap < 2 * need) cap <<= 1;
+            c.gcap_col[col] = (int32_t)cap;
+        }
+    }
+}
+
+cudaError_t launch_classify(const ClassifyArgs &c, cudaStream_t s) {
+    if (c.n <= 0) return cudaSuccess;
+    int64_t b = (c.n + 255) / 256;
+    if (b > 148 * 16) b = 148 * 16;
+    k_classify<<<(int)b, 256, 0, s>>>(c);
+    return cudaGetLastError();
+}
+
+__global__ void k_global_layout(int count, const int32_t *list, const int32_t *gcap_col,
+                                int32_t *gcap, int64_t *gcap64) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) {
+        int32_t c = gcap_col[list[i]];
+        gcap[i] = c;
+        gcap64[i] = c;
+    }
+}
+cudaError_t launch_global_layout(int count, const int32_t *list, const int32_t *gcap_col,
+                                 int32_t *gcap, int64_t *gcap64, cudaStream_t s) {
+    if (count <= 0) return cudaSuccess;
+    k_global_layout<<<(count + 255) / 256, 256, 0, s>>>(count, list, gcap_col, gcap, gcap64);
+    return cudaGetLastError();
+}
+
+// staging capacity of a pruned column: min(max(S,R,1), min(f_j, m))
+__global__ void k_kcap(int64_t ncols, const int64_t *f, int64_t m, int kmax, int64_t *kcap) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < ncols;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        int64_t u = f[j] < m ? f[j] : m;
+        kcap[j] = u < kmax ? u : kmax;
+    }
+}
+cudaError_t launch_kcap(int64_t ncols, const int64_t *flops, int64_t m, int kmax, int64_t *kcap,
+                        cudaStream_t s) {
+    if (ncols <= 0) return cudaSuccess;
+    k_kcap<<<red_grid(ncols) * 4, 256, 0, s>>>(ncols, flops, m, kmax, kcap);
+    return cudaGetLastError();
+}
+
+// staging capacity of a column of an unpruned CSC: min(kmax, nnz(C_*j))
+__global__ void k_kcap_cp(int64_t ncols, const int64_t *cp, int kmax, int64_t *kcap) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < ncols;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        int64_t u = cp[j + 1] - cp[j];
+        kcap[j] = u < kmax ? u : kmax;
+    }
+}
+cudaError_t launch_kcap_cp(int64_t ncols, const int64_t *cp, int kmax, int64_t *kcap, cudaStream_t s) {
+    if (ncols <= 0) return cudaSuccess;
+    k_kcap_cp<<<red_grid(ncols) * 4, 256, 0, s>>>(ncols, cp, kmax, kcap);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ assembly
+// Copy each column's cnt entries from its staging slot to the compact CSC.  Warp/column.
+__global__ void k_copy_cols(int64_t ncols, const int64_t *__restrict__ cnt,
+                            const int64_t *__restrict__ soff, const int32_t *__restrict__ srow,
+                            const float *__restrict__ sval, const int64_t *__restrict__ cp,
+                            int32_t *__restrict__ orow, float *__restrict__ oval) {
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = lane_id();
+    for (int64_t col = w; col < ncols; col += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t n = cnt[col], src = soff[col], dst = cp[col];
+        for (int64_t i = lane; i < n; i += 32) {
+            orow[dst + i] = srow[src + i];
+            oval[dst + i] = sval[src + i];
+        }
+    }
+}
+cudaError_t launch_copy_cols(int64_t ncols, const int64_t *cnt, const int64_t *soff,
+                             const int32_t *srow, const float *sval, const int64_t *cp,
+                             int32_t *orow, float *oval, cudaStream_t s) {
+    if (ncols <= 0) return cudaSuccess;
+    int64_t blocks = (ncols * 32 + 255) / 256;
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    k_copy_cols<<<(int)blocks, 256, 0, s>>>(ncols, cnt, soff, srow, sval, cp, orow, oval);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ standalone prune/inflate
+// Alg. 1 lines 4-5 on an unpruned CSC column (rows already sorted): threshold stats,
+// branch (Q5, Q7, Q8), exact top-K by radix select, renormalise + chaos (Q9), Hadamard
+// power r and renormalise (Q1).  The kept entries are extracted in row
+// order with a block scan, so the output stays sorted without a sort.
+constexpr int kPruneNT = 256;
+__global__ void __launch_bounds__(kPruneNT)
+    k_prune(int64_t ncols, const int64_t *__restrict__ ccp, const int32_t *__restrict__ crow,
+            const float *__restrict__ cval, const int64_t *__restrict__ soff,
+            int32_t *__restrict__ srow, float *__restrict__ sval, int64_t *__restrict__ scnt,
+            float *__restrict__ chaos_out, float *chaos_max, PruneParams pp) {
+    __shared__ unsigned hist[256];
+    __shared__ int sint[4];
+    __shared__ double sred[kPruneNT / 32];
+    __shared__ int sscan[kPruneNT / 32];
+    const int tid = threadIdx.x;
+    for (int64_t col = blockIdx.x; col < ncols; col += gridDim.x) {
+        const int64_t base = ccp[col];
+        const int nnz = (int)(ccp[col + 1] - base);
+        const int32_t *rows = crow + base;
+        const float *vals = cval + base;
+        int mloc = 0;
+        double sloc = 0.0;
+        for (int i = tid; i < nnz; i += kPruneNT) {
+            double v = (double)vals[i];
+            if (v >= pp.theta) {
+                mloc++;
+                sloc += v;
+            }
+        }
+        const int m = block_sum<kPruneNT, int>(mloc, sscan);
+        const double s = block_sum<kPruneNT, double>(sloc, sred);
+        int64_t K;
+        const int br = prune_branch(pp, nnz, m, s, K);
+        uint32_t t = 0;
+        int rowcut = 0, sel;
+        if (br == 0) {
+            sel = 0;
+        } else if (K >= nnz) {
+            sel = 2;
+        } else {
+            radix_select_topk<kPruneNT, float>(rows, vals, nnz, (int)K, t, rowcut, hist, sint);
+            sel = 1;
+        }
+        auto keep = [&](int k, float v) {
+            if (sel == 0) return (double)v >= pp.theta;
+            if (sel == 2) return true;
+            uint32_t b = val_bits(v);
+            return b > t || (b == t && k <= rowcut);
+        };
+        double sv = 0.0, mx = 0.0, sq = 0.0, sr = 0.0;
+        for (int i = tid; i < nnz; i += kPruneNT) {
+            float v = vals[i];
+            if (keep(rows[i], v)) {
+                double d = (double)v;
+                sv += d;
+                mx = d > mx ? d : mx;
+                sq += d * d;
+                sr += pow_r(d, pp);
+            }
+        }
+        sv = block_sum<kPruneNT, double>(sv, sred);
+        mx = block_max<kPruneNT, double>(mx, sred);
+        sq = block_sum<kPruneNT, double>(sq, sred);
+        sr = block_sum<kPruneNT, double>(sr, sred);
+        const int64_t dst = soff[col];
+        int kept = 0;
+        for (int c = 0; c < nnz; c += kPruneNT) {
+            const int i = c + tid;
+            int f = 0;
+            int r = 0;
+            float v = 0.f;
+            if (i < nnz) {
+                r = rows[i];
+                v = vals[i];
+                f = keep(r, v) ? 1 : 0;
+            }
+            int tot;
+            const int pos = block_excl_scan<kPruneNT>(f, sscan, tot);
+            if (f) {
+                srow[dst + kept + pos] = r;
+                sval[dst + kept + pos] = (float)(pow_r((double)v, pp) / sr);
+            }
+            kept += tot;
+        }
+        const float chaos = kept > 0 ? (float)((double)kept * (mx / sv - sq / (sv * sv))) : 0.0f;
+        if (tid == 0) {
+            scnt[col] = kept;
+            if (chaos_out) chaos_out[col] = chaos;
+            atomic_max_nonneg_float(chaos_max, chaos);
+        }
+        __syncthreads();
+    }
+}
+
+cudaError_t launch_prune(int64_t ncols, const int64_t *ccp, const int32_t *crow, const float *cval,
+                         const int64_t *soff, int32_t *srow, float *sval, int64_t *scnt,
+                         float *chaos, float *chaos_max, const PruneParams &pp, int grid,
+                         cudaStream_t s) {
+    if (ncols <= 0) return cudaSuccess;
+    k_prune<<<grid, kPruneNT, 0, s>>>(ncols, ccp, crow, cval, soff, srow, sval, scnt, chaos,
+                                      chaos_max, pp);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ Cohen estimator
+// Philox-4x32-10 (Salmon et al., SC'11) -- 10 rounds of the 4x32 S-box with key bumps.
+__device__ __forceinline__ uint4 philox4x32_10(uint4 x, uint2 k) {
+#pragma unroll
+    for (int r = 0; r < 10; r++) {
+        const uint32_t lo0 = 0xD2511F53u * x.x, hi0 = __umulhi(0xD2511F53u, x.x);
+        const uint32_t lo1 = 0xCD9E8D57u * x.z, hi1 = __umulhi(0xCD9E8D57u, x.z);
+        x = make_uint4(hi1 ^ x.y ^ k.x, lo1, hi0 ^ x.w ^ k.y, lo0);
+        k.x += 0x9E3779B9u;
+        k.y += 0xBB67AE85u;
+    }
+    return x;
+}
+
+// Keys X[s][i] ~ Exp(lambda = 1): u = Philox(ctr=(i_lo,i_hi,s,0),
+// key=(seed_lo,seed_hi)).x, X = (float)(-log((u + 0.5) * 2^-32)) evaluated in double.
+// X is stored row-major [m][r] so one row's r keys are contiguous for the gathers.
+__global__ void k_cohen_keys(int64_t m, int64_t row0, int r, uint64_t seed, float *X,
+                             float *keys_out) {
+    const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t gi = (uint64_t)(row0 + i);
+        for (int s = 0; s < r; s++) {
+            uint4 o = philox4x32_10(make_uint4((uint32_t)gi, (uint32_t)(gi >> 32), (uint32_t)s, 0u), key);
+            const float x = (float)(-log(((double)o.x + 0.5) * (1.0 / 4294967296.0)));
+            X[i * r + s] = x;
+            if (keys_out) keys_out[(int64_t)s * m + i] = x;
+        }
+    }
+}
+cudaError_t launch_cohen_keys(int64_t m, int64_t row0, int r, uint64_t seed, float *X,
+                              float *keys_out, cudaStream_t s) {
+    if (m <= 0) return cudaSuccess;
+    int64_t b = (m + 255) / 256;
+    if (b > 148 * 16) b = 148 * 16;
+    k_cohen_keys<<<(int)b, 256, 0, s>>>(m, row0, r, seed, X, keys_out);
+    return cudaGetLastError();
+}
+
+// One layer of min-propagation: out[j][s] = min_{i in inds(M_*j)} in[i][s].
+// With est != nullptr (the output layer) also est_j = (r-1) / sum_s out[j][s], 0 when
+// column j reaches nothing.  One warp per column; r <= 16 keys in registers.
+__global__ void k_cohen_min(int64_t ncols, const int64_t *__restrict__ cp,
+                            const int32_t *__restrict__ row, int64_t c0,
+                            const float *__restrict__ in, int r, float *__restrict__ out,
+                            float *__restrict__ est) {
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = lane_id();
+    for (int64_t col = w; col < ncols; col += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        float mn[16];
+#pragma unroll
+        for (int s = 0; s < 16; s++) mn[s] = INFINITY;
+        const int64_t q0 = cp[c0 + col], q1 = cp[c0 + col + 1];
+        for (int64_t q = q0 + lane; q < q1; q += 32) {
+            const float *src = in + (int64_t)__ldg(row + q) * r;
+#pragma unroll
+            for (int s = 0; s < 16; s++)
+                if (s < r) mn[s] = fminf(mn[s], __ldg(src + s));
+        }
+        double sum = 0.0;
+#pragma unroll
+        for (int s = 0; s < 16; s++) {
+            if (s < r) {
+                float v = warp_min(mn[s]);
+                if (out && lane == 0) out[col * r + s] = v;
+                sum += (double)v;
+            }
+        }
+        if (est && lane == 0) est[col] = isinf(sum) ? 0.0f : (float)((double)(r - 1) / sum);
+    }
+}
+cudaError_t launch_cohen_min(int64_t ncols, const int64_t *cp, const int32_t *row, int64_t c0,
+                             const float *in, int r, float *out, float *est, cudaStream_t s) {
+    if (ncols <= 0) return cudaSuccess;
+    int64_t blocks = (ncols * 32 + 255) / 256;
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    k_cohen_min<<<(int)blocks, 256, 0, s>>>(ncols, cp, row, c0, in, r, out, est);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ preprocessing (Alg. 1 l.1)
+__device__ __forceinline__ int64_t lower_bound_row(const int32_t *rows, int64_t lo, int64_t hi,
+                                                   int32_t key) {
+    while (lo < hi) {
+        int64_t mid = (lo + hi) >> 1;
+        if (rows[mid] < key) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+__global__ void k_pre_count(int64_t n, const int64_t *gcp, const int32_t *grow, int add_loops,
+                            int64_t *cnt) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t a = gcp[j], b = gcp[j + 1];
+        int64_t c = b - a;
+        if (add_loops) {
+            int64_t p = lower_bound_row(grow, a, b, (int32_t)j);
+            if (!(p < b && grow[p] == (int32_t)j)) c += 1;
+        }
+        cnt[j] = c;
+    }
+}
+cudaError_t launch_pre_count(int64_t n, const int64_t *gcp, const int32_t *grow, int add_loops,
+                             int64_t *cnt, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    k_pre_count<<<red_grid(n) * 4, 256, 0, s>>>(n, gcp, grow, add_loops, cnt);
+    return cudaGetLastError();
+}
+// Warp per column: insert / add the self-loop of weight 1 (Q10), sum the column in
+// fp64 and write w / sum (column-stochastic).
+__global__ void k_pre_fill(int64_t n, const int64_t *__restrict__ gcp,
+                           const int32_t *__restrict__ grow, const float *__restrict__ gw,
+                           int add_loops, const int64_t *__restrict__ cp, int32_t *__restrict__ row,
+                           float *__restrict__ val) {
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = lane_id();
+    for (int64_t j = w; j < n; j += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t a = gcp[j], b = gcp[j + 1];
+        int64_t p = b;
+        bool has = false;
+        if (add_loops) {
+            p = lower_bound_row(grow, a, b, (int32_t)j);
+            has = p < b && grow[p] == (int32_t)j;
+        }
+        const bool ins = add_loops && !has;
+        double s = 0.0;
+        for (int64_t t = a + lane; t < b; t += 32) {
+            double x = (double)gw[t];
+            if (add_loops && grow[t] == (int32_t)j) x += 1.0;
+            s += x;
+        }
+        s = warp_sum(s);
+        if (ins) s += 1.0;
+        const int64_t o = cp[j];
+        for (int64_t t = a + lane; t < b; t += 32) {
+            double x = (double)gw[t];
+            if (add_loops && grow[t] == (int32_t)j) x += 1.0;
+            const int64_t d = o + (t - a) + ((ins && t >= p) ? 1 : 0);
+            row[d] = grow[t];
+            val[d] = (float)(x / s);
+        }
+        if (ins && lane == 0) {
+            row[o + (p - a)] = (int32_t)j;
+            val[o + (p - a)] = (float)(1.0 / s);
+        }
+    }
+}
+cudaError_t launch_pre_fill(int64_t n, const int64_t *gcp, const int32_t *grow, const float *gw,
+                            int add_loops, const int64_t *cp, int32_t *row, float *val,
+                            cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    int64_t blocks = (n * 32 + 255) / 256;
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    k_pre_fill<<<(int)blocks, 256, 0, s>>>(n, gcp, grow, gw, add_loops, cp, row, val);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ connected components
+// Union-find with min-index hooking (a root is always its component's smallest vertex)
+// and path halving; then canonical labels = rank of the root among roots (Q11).
+__device__ __forceinline__ int32_t uf_find(int32_t *parent, int32_t x) {
+    volatile int32_t *p = parent;
+    int32_t px = p[x];
+    while (px != x) {
+        int32_t g = p[px];
+        if (g != px) p[x] = g;
+        x = px;
+        px = p[x];
+    }
+    return x;
+}
+__global__ void k_cc_init(int64_t n, int32_t *parent) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        parent[i] = (int32_t)i;
+}
+__global__ void k_cc_hook(int64_t n, const int64_t *__restrict__ cp, const int32_t *__restrict__ row,
+                          int32_t *parent) {
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = lane_id();
+    for (int64_t j = w; j < n; j += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        for (int64_t t = cp[j] + lane; t < cp[j + 1]; t += 32) {
+            int32_t a = row[t], b = (int32_t)j;
+            for (;;) {
+                a = uf_find(parent, a);
+                b = uf_find(parent, b);
+                if (a == b) break;
+                int32_t hi = a > b ? a : b, lo = a > b ? b : a;
+                int32_t old = atomicCAS(&parent[hi], hi, lo);
+                if (old == hi) break;
+                a = hi;
+                b = lo;
+            }
+        }
+    }
+}
+__global__ void k_cc_flag(int64_t n, int32_t *parent, int64_t *flag) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int32_t r = uf_find(parent, (int32_t)i);
+        parent[i] = r;
+        flag[i] = (r == (int32_t)i) ? 1 : 0;
+    }
+}
+__global__ void k_cc_label(int64_t n, const int32_t *parent, const int64_t *rank, int32_t *labels) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        labels[i] = (int32_t)rank[parent[i]];
+}
+cudaError_t launch_cc(int64_t n, const int64_t *cp, const int32_t *row, int32_t *parent,
+                      int64_t *flag, int64_t *rank, void *scan_tmp, int32_t *labels,
+                      cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    const int g = red_grid(n) * 4;
+    k_cc_init<<<g, 256, 0, s>>>(n, parent);
+    int64_t blocks = (n * 32 + 255) / 256;
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    k_cc_hook<<<(int)blocks, 256, 0, s>>>(n, cp, row, parent);
+    k_cc_flag<<<g, 256, 0, s>>>(n, parent, flag);
+    cudaError_t e = launch_scan_i64(flag, rank, n, scan_tmp, s);
+    if (e != cudaSuccess) return e;
+    k_cc_label<<<g, 256, 0, s>>>(n, parent, rank, labels);
+    return cudaGetLastError();
+}
+
+}  // namespace mclx

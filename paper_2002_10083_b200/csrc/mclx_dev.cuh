@@ -1,0 +1,292 @@
+// mclx_dev.cuh -- device primitives shared by the libmclx kernels (sm_100a).
+//
+// Team = one CTA of NT threads working on one matrix column.  Everything here is
+// plain CUDA C++ (warp shuffles/ballots, shared-memory atomics, block scans); the
+// path is sparse gather/hash/select work, not a dense contraction, so there are
+// no tensor-core instructions anywhere in this library (north star).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace mclx {
+
+constexpr int kEmptyKey = -1;          // unoccupied hash slot
+constexpr int kPadKey = 0x7fffffff;    // bitonic padding, sorts after every row id
+constexpr int kMaxWarps = 32;
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+__device__ __forceinline__ int warp_id() { return threadIdx.x >> 5; }
+
+// Fibonacci hashing of a row id onto [0, cap): the top bits of row * 2^32/phi,
+// range-reduced by a multiply-high so that cap need not be a power of two.
+__device__ __forceinline__ uint32_t hash_slot(int row, uint32_t cap) {
+    return __umulhi((uint32_t)row * 0x9E3779B1u, cap);
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+template <typename T>
+__device__ __forceinline__ T warp_max(T v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        T w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = w > v ? w : v;
+    }
+    return v;
+}
+template <typename T>
+__device__ __forceinline__ T warp_min(T v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        T w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = w < v ? w : v;
+    }
+    return v;
+}
+
+// Block-wide sum / max.  `sh` holds >= NT/32 elements of T.  Every thread gets the result.
+template <int NT, typename T>
+__device__ __forceinline__ T block_sum(T v, T *sh) {
+    v = warp_sum(v);
+    if (NT == 32) return v;
+    __syncthreads();
+    if (lane_id() == 0) sh[warp_id()] = v;
+    __syncthreads();
+    T r = T(0);
+#pragma unroll
+    for (int i = 0; i < NT / 32; i++) r += sh[i];
+    return r;
+}
+template <int NT, typename T>
+__device__ __forceinline__ T block_max(T v, T *sh) {
+    v = warp_max(v);
+    if (NT == 32) return v;
+    __syncthreads();
+    if (lane_id() == 0) sh[warp_id()] = v;
+    __syncthreads();
+    T r = sh[0];
+#pragma unroll
+    for (int i = 1; i < NT / 32; i++) r = sh[i] > r ? sh[i] : r;
+    return r;
+}
+
+// Block-wide exclusive scan of small ints; `total` receives the block sum.
+template <int NT>
+__device__ __forceinline__ int block_excl_scan(int v, int *sh, int &total) {
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane_id() >= o) x += y;
+    }
+    if (NT == 32) {
+        total = __shfl_sync(0xffffffffu, x, 31);
+        return x - v;
+    }
+    __syncthreads();
+    if (lane_id() == 31) sh[warp_id()] = x;
+    __syncthreads();
+    int off = 0, tot = 0;
+#pragma unroll
+    for (int i = 0; i < NT / 32; i++) {
+        int s = sh[i];
+        off += (i < warp_id()) ? s : 0;
+        tot += s;
+    }
+    total = tot;
+    return off + x - v;
+}
+
+template <typename V>
+__device__ __forceinline__ uint32_t val_bits(V v) {
+    return __float_as_uint((float)v);  // positive floats order like their bit patterns
+}
+
+// Order-preserving in-place compaction of (keys, vals)[0, len) by predicate keep(key, val).
+// Safe in place: chunk c is fully read before the scan's barrier, and its writes land at
+// indices <= the chunk's own indices, below every unread element.  Returns the kept count.
+template <int NT, typename V, class Pred>
+__device__ int compact_inplace(int *keys, V *vals, int len, Pred keep, int *sh) {
+    int base = 0;
+    for (int c = 0; c < len; c += NT) {
+        int i = c + (int)threadIdx.x;
+        int k = 0;
+        V v = V(0);
+        int f = 0;
+        if (i < len) {
+            k = keys[i];
+            v = vals[i];
+            f = keep(k, v) ? 1 : 0;
+        }
+        int tot;
+        int pos = block_excl_scan<NT>(f, sh, tot);
+        if (f) {
+            keys[base + pos] = k;
+            vals[base + pos] = v;
+        }
+        base += tot;
+    }
+    __syncthreads();
+    return base;
+}
+
+// Bitonic sort of (keys, vals)[0, P) ascending by key; P a power of two, padded by caller.
+template <int NT, typename V>
+__device__ void bitonic_sort(int *keys, V *vals, int P) {
+    for (int k = 2; k <= P; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < P; i += NT) {
+                int ixj = i ^ j;
+                if (ixj > i) {
+                    int a = keys[i], b = keys[ixj];
+                    bool up = ((i & k) == 0);
+                    if ((a > b) == up) {
+                        keys[i] = b;
+                        keys[ixj] = a;
+                        V t = vals[i];
+                        vals[i] = vals[ixj];
+                        vals[ixj] = t;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// Warp 0 only: find the digit d of a 256-bin histogram at which the running count
+// (from the top digit when DESC, from digit 0 otherwise) first reaches `rem`.
+// out[0] = d, out[1] = count strictly before d in that order, out[2] = hist[d].
+template <bool DESC>
+__device__ __forceinline__ void find_digit(const unsigned *hist, int rem, int *out) {
+    const int lane = lane_id();
+    unsigned c[8];
+    unsigned sum = 0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        int d = DESC ? 255 - (lane * 8 + i) : lane * 8 + i;
+        c[i] = hist[d];
+        sum += c[i];
+    }
+    unsigned inc = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        unsigned y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    unsigned excl = inc - sum;
+    if (excl < (unsigned)rem && inc >= (unsigned)rem) {
+        unsigned run = excl;
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            if (run + c[i] >= (unsigned)rem) {
+                out[0] = DESC ? 255 - (lane * 8 + i) : lane * 8 + i;
+                out[1] = (int)run;
+                out[2] = (int)c[i];
+                break;
+            }
+            run += c[i];
+        }
+    }
+}
+
+// Exact top-K of (vals desc, keys asc) over entries [0, n) (every entry valid):
+// radix select on the fp32 bit pattern (8-bit digits), then on the row id among the
+// entries equal to the K-th value.  Entry e is kept iff
+//   bits(e) > t  or  (bits(e) == t and key(e) <= rowcut).
+template <int NT, typename V>
+__device__ void radix_select_topk(const int *keys, const V *vals, int n, int K, uint32_t &t,
+                                  int &rowcut, unsigned *hist, int *sint) {
+    uint32_t prefix = 0, mask = 0;
+    int rem = K, eq = 0;
+    for (int shift = 24; shift >= 0; shift -= 8) {
+        for (int i = threadIdx.x; i < 256; i += NT) hist[i] = 0;
+        __syncthreads();
+        for (int i = threadIdx.x; i < n; i += NT) {
+            uint32_t b = val_bits(vals[i]);
+            if ((b & mask) == prefix) atomicAdd(&hist[(b >> shift) & 255u], 1u);
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) find_digit<true>(hist, rem, sint);
+        __syncthreads();
+        uint32_t d = (uint32_t)sint[0];
+        rem -= sint[1];
+        eq = sint[2];
+        prefix |= d << shift;
+        mask |= 0xFFu << shift;
+        __syncthreads();
+    }
+    t = prefix;
+    if (rem == eq) {
+        rowcut = 0x7fffffff;
+        return;
+    }
+    uint32_t rp = 0, rm = 0;
+    for (int shift = 24; shift >= 0; shift -= 8) {
+        for (int i = threadIdx.x; i < 256; i += NT) hist[i] = 0;
+        __syncthreads();
+        for (int i = threadIdx.x; i < n; i += NT) {
+            uint32_t b = val_bits(vals[i]);
+            uint32_t k = (uint32_t)keys[i];
+            if (b == t && (k & rm) == rp) atomicAdd(&hist[(k >> shift) & 255u], 1u);
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) find_digit<false>(hist, rem, sint);
+        __syncthreads();
+        rp |= (uint32_t)sint[0] << shift;
+        rm |= 0xFFu << shift;
+        rem -= sint[1];
+        __syncthreads();
+    }
+    rowcut = (int)rp;
+}
+
+// Parameters of the prune / select / recover / inflate step (readings Q3-Q9).
+struct PruneParams {
+    double theta;   // keep v >= theta
+    int S;          // select_k
+    int R;          // recover_k (0 = off)
+    double pct;     // recover when kept mass < pct
+    double r;       // inflation exponent
+    int r_is_2;
+    int kmax;       // max(S, R, 1): staging capacity per column
+};
+
+// Branch of a column (same numbering as the oracle): 0 thresh, 1 select, 2 recover,
+// 3 argmax, 4 empty.  K = number of entries kept.
+__device__ __forceinline__ int prune_branch(const PruneParams &pp, int64_t nnz, int64_t m,
+                                            double s, int64_t &K) {
+    if (m > pp.S) {
+        K = pp.S;
+        return 1;
+    }
+    if (pp.R > 0 && m < pp.R && s < pp.pct && nnz > m) {
+        K = pp.R < nnz ? pp.R : nnz;
+        return 2;
+    }
+    if (m > 0) {
+        K = m;
+        return 0;
+    }
+    if (nnz > 0) {
+        K = 1;
+        return 3;
+    }
+    K = 0;
+    return 4;
+}
+
+__device__ __forceinline__ double pow_r(double w, const PruneParams &pp) {
+    return pp.r_is_2 ? w * w : pow(w, pp.r);
+}
+
+__device__ __forceinline__ void atomic_max_nonneg_float(float *addr, float v) {
+    // non-negative floats order like their int bit patterns
+    atomicMax(reinterpret_cast<int *>(addr), __float_as_int(v));
+}
+
+}  // namespace mclx

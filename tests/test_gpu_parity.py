@@ -1,0 +1,315 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on the same
+seeded inputs.
+
+  P1 unpruned structure bit-exact (col_ptr, row_idx);
+  P2 unpruned values |v32 - v64| <= 1e-5 v64 for v64 >= 1e-30;
+  P3 pruned/inflated output: kept sets equal except entries within 1e-6 of the
+     column's cut tau_j; values 1e-5 relative (re-inflated over the GPU's kept set);
+  P4 cluster labels identical;
+  P5 Cohen keys identical (<= 1 ulp, rare), estimates 1e-6 relative.
+Inputs handed to both sides are the SAME fp32 numbers (the oracle promotes them).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import synth
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    import paper_2002_10083_b200 as M
+
+
+def dev(m, **kw):
+    return M.CSC.from_host(m, **kw)
+
+
+def host_mat(g):
+    cp, rw, vl = g.to_host()
+    return O.Mat(g.nrows, g.ncols, cp.astype(np.int64), rw.astype(np.int32), vl.astype(np.float64))
+
+
+def f32(m):
+    """fp32 copy of an oracle Mat (the GPU input); the oracle is then run on the same numbers."""
+    return O.Mat(m.nrows, m.ncols, m.colptr.copy(), m.rows.copy(),
+                 m.vals.astype(np.float32).astype(np.float64))
+
+
+def assert_unpruned_parity(G, Ref, rtol=1e-5):
+    assert G.nrows == Ref.nrows and G.ncols == Ref.ncols
+    assert np.array_equal(G.colptr, Ref.colptr), "P1 col_ptr"
+    assert np.array_equal(G.rows, Ref.rows), "P1 row_idx"
+    big = Ref.vals >= 1e-30
+    rel = np.abs(G.vals[big] - Ref.vals[big]) / Ref.vals[big]
+    assert rel.size == 0 or rel.max() <= rtol, f"P2 max rel err {rel.max()}"
+
+
+def kept_parity(Gm, Cref, info, params, band=1e-6, rtol=1e-5):
+    """P3 for a pruned output Gm (GPU) against oracle info on unpruned Cref (fp64)."""
+    theta, S, R, pct = params
+    stats = dict(band_excluded=0, band_flip_cols=0)
+    Ao, _ = O.prune_inflate(Cref, theta, S, R, pct, 2.0)
+    for j in range(Gm.ncols):
+        gr = Gm.rows[Gm.colptr[j]:Gm.colptr[j + 1]]
+        gv = Gm.vals[Gm.colptr[j]:Gm.colptr[j + 1]]
+        orow = Ao.rows[Ao.colptr[j]:Ao.colptr[j + 1]]
+        assert np.all(np.diff(gr) > 0)
+        if np.array_equal(gr, orow):
+            ov = Ao.vals[Ao.colptr[j]:Ao.colptr[j + 1]]
+            rel = np.abs(gv - ov) / ov
+            assert rel.max() <= rtol, (j, rel.max())
+            continue
+        cr = Cref.rows[Cref.colptr[j]:Cref.colptr[j + 1]]
+        cv = Cref.vals[Cref.colptr[j]:Cref.colptr[j + 1]]
+        diff = np.setxor1d(gr, orow)
+        vals = cv[np.searchsorted(cr, diff)]
+        assert np.all(np.abs(vals - info.tau[j]) <= band), (j, vals, info.tau[j])
+        stats["band_excluded"] += len(diff)
+        stats["band_flip_cols"] += 1
+        # re-inflate the oracle values over the GPU's kept set
+        w = cv[np.searchsorted(cr, gr)]
+        w = w / w.sum()
+        ref = w * w / (w * w).sum()
+        assert np.max(np.abs(gv - ref) / ref) <= rtol
+    return stats
+
+
+# ---------------------------------------------------------------- preprocess
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_preprocess(name):
+    G = synth.config_graph(name)
+    A = host_mat(M.preprocess(dev(G)))
+    R = O.preprocess(G)
+    assert np.array_equal(A.colptr, R.colptr) and np.array_equal(A.rows, R.rows)
+    np.testing.assert_allclose(A.vals, R.vals, rtol=1e-6)
+
+
+def test_preprocess_empty_and_loops():
+    G = synth.Csc(4, 4, np.array([0, 0, 1, 1, 3], np.int64), np.array([3, 0, 2], np.int32),
+                  np.array([2.0, 1.0, 3.0], np.float32))
+    A = host_mat(M.preprocess(dev(G)))
+    R = O.preprocess(G)
+    assert np.array_equal(A.colptr, R.colptr) and np.array_equal(A.rows, R.rows)
+    np.testing.assert_allclose(A.vals, R.vals, rtol=1e-6)
+
+
+# ---------------------------------------------------------------- expansion (P1, P2)
+@pytest.mark.parametrize("seed", range(8))
+def test_expand_random(seed):
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(1, 3000))
+    A = synth.random_sparse(n, n, float(rng.uniform(0.001, 0.05)), seed=seed,
+                            empty_cols=0.05, degree_skew=bool(seed % 2))
+    Cg, st = M.expand(dev(A))
+    Cr, fl = O.expand(A)
+    assert_unpruned_parity(host_mat(Cg), Cr)
+    assert st["flops"] == int(fl.sum())
+    assert st["nnz_unpruned"] == Cr.nnz
+
+
+@pytest.mark.parametrize("bin_", list(range(7)))
+def test_expand_forced_bins(bin_):
+    """Bin invariance (T2): every column forced into bin >= b gives the same product."""
+    A = synth.random_sparse(700, 700, 0.02, seed=11, empty_cols=0.1)
+    p = M.Params(force_bin=bin_)
+    Cg, st = M.expand(dev(A), params=p)
+    Cr, _ = O.expand(A)
+    assert_unpruned_parity(host_mat(Cg), Cr)
+    assert sum(st["bin_cols"][:bin_]) == 0
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_spgemm_rectangular_and_ranges(seed):
+    rng = np.random.default_rng(40 + seed)
+    m, p, n = (int(x) for x in rng.integers(1, 1500, size=3))
+    A = synth.random_sparse(m, p, 0.01, seed=seed)
+    B = synth.random_sparse(p, n, 0.01, seed=seed + 7, empty_cols=0.2)
+    b = int(rng.integers(0, n))
+    e = int(rng.integers(b, n + 1))
+    Cg, _ = M.spgemm(dev(A), dev(B), (b, e))
+    Cr, _ = O.spgemm(A, B, b, e)
+    assert_unpruned_parity(host_mat(Cg), Cr)
+
+
+def test_expand_empty_and_degenerate():
+    Z = synth.Csc(5, 5, np.zeros(6, np.int64), np.zeros(0, np.int32), np.zeros(0, np.float32))
+    Cg, st = M.expand(dev(Z))
+    assert Cg.nnz == 0 and st["flops"] == 0
+    one = synth.Csc(1, 1, np.array([0, 1], np.int64), np.array([0], np.int32),
+                    np.array([0.5], np.float32))
+    Cg, _ = M.expand(dev(one))
+    assert host_mat(Cg).vals.tolist() == [0.25]
+    Cg, _ = M.expand(dev(one), cols=(0, 0))
+    assert Cg.ncols == 0 and Cg.nnz == 0
+
+
+def test_expand_hub_column_global_bin():
+    """A dense hub (column with > 16384 terms -> fp64 global bin)."""
+    n = 40000
+    rng = np.random.default_rng(5)
+    hub = np.sort(rng.choice(n, size=20000, replace=False))
+    cols = [np.array([j]) for j in range(n)]
+    cols[7] = np.union1d(hub, [7])
+    cnt = np.array([len(c) for c in cols])
+    cp = np.zeros(n + 1, np.int64)
+    np.cumsum(cnt, out=cp[1:])
+    rows = np.concatenate(cols).astype(np.int32)
+    vals = rng.uniform(0.01, 1, size=rows.size).astype(np.float32)
+    A = synth.Csc(n, n, cp, rows, vals)
+    Cg, st = M.expand(dev(A))
+    Cr, _ = O.expand(A)
+    assert_unpruned_parity(host_mat(Cg), Cr)
+    assert st["bin_cols"][6] >= 1
+
+
+def test_symbolic_and_flops():
+    A = synth.random_sparse(2000, 2000, 0.01, seed=3, degree_skew=True)
+    nnz, tot = M.symbolic(dev(A))
+    Cr, fl = O.expand(A)
+    assert np.array_equal(nnz.cpu().numpy(), np.diff(Cr.colptr))
+    assert tot == Cr.nnz
+    f, ftot = M.flops(dev(A))
+    assert np.array_equal(f.cpu().numpy(), fl) and ftot == int(fl.sum())
+
+
+# ---------------------------------------------------------------- Cohen (P5)
+@pytest.mark.parametrize("r,seed", [(3, 1), (10, 7), (16, 123456789)])
+def test_cohen_keys_and_estimates(r, seed):
+    A = synth.random_sparse(3000, 2500, 0.003, seed=seed % 1000, empty_cols=0.05)
+    B = synth.random_sparse(2500, 2000, 0.003, seed=seed % 1000 + 1, empty_cols=0.05)
+    est, tot, keys = M.estimate(dev(A), dev(B), r=r, seed=seed, return_keys=True)
+    eo, ko, _ = O.cohen(A, B, r=r, seed=seed, return_keys=True)
+    kg = keys.cpu().numpy()
+    mism = kg != ko
+    assert mism.mean() < 1e-4
+    if mism.any():
+        ulps = np.abs(kg.view(np.int32)[mism] - ko.view(np.int32)[mism])
+        assert ulps.max() <= 1
+    eg = est.cpu().numpy().astype(np.float64)
+    np.testing.assert_allclose(eg, eo, rtol=1e-6)
+    assert tot == pytest.approx(eo.sum(), rel=1e-6)
+
+
+# ---------------------------------------------------------------- prune / inflate (P3)
+PRUNE_CASES = [(1e-4, 1100, 1400, 0.9), (1e-4, 100, 100, 0.9), (1e-3, 20, 0, 0.9),
+               (0.05, 3, 30, 0.5), (0.0, 7, 0, 0.9)]
+
+
+@pytest.mark.parametrize("params", PRUNE_CASES)
+def test_prune_inflate_identical_inputs(params):
+    """Same fp32 C on both sides: selection is exact on both, so kept sets must be equal."""
+    theta, S, R, pct = params
+    A = O.preprocess(synth.planted_partition())
+    Cr, _ = O.expand(A)
+    # plant exact ties and a few empty columns
+    idx = np.arange(0, Cr.vals.size - 1, 97)
+    Cr.vals[idx] = Cr.vals[idx + 1]
+    C32 = f32(Cr)
+    Ag, st, chaos = M.prune_inflate(dev(C32), M.Params(prune_threshold=theta, select_k=S,
+                                                       recover_k=R, recover_pct=pct),
+                                    return_chaos=True)
+    Ao, info = O.prune_inflate(C32, theta, S, R, pct, 2.0)
+    G = host_mat(Ag)
+    assert np.array_equal(G.colptr, Ao.colptr) and np.array_equal(G.rows, Ao.rows)
+    np.testing.assert_allclose(G.vals, Ao.vals, rtol=1e-5)
+    np.testing.assert_allclose(chaos.cpu().numpy(), info.chaos, rtol=1e-4, atol=1e-6)
+    assert st["chaos"] == pytest.approx(info.chaos.max(), rel=1e-4, abs=1e-6)
+
+
+def test_prune_big_columns():
+    """Columns far larger than any shared-memory bin (standalone prune reads global)."""
+    rng = np.random.default_rng(9)
+    n, ncol = 200000, 6
+    cols = [np.sort(rng.choice(n, size=s, replace=False)) for s in (1, 50, 5000, 60000, 150000, 0)]
+    cnt = np.array([len(c) for c in cols])
+    cp = np.zeros(ncol + 1, np.int64)
+    np.cumsum(cnt, out=cp[1:])
+    vals = (rng.exponential(size=cnt.sum()) ** 4).astype(np.float32)
+    Cm = synth.Csc(n, ncol, cp, np.concatenate(cols).astype(np.int32), vals)
+    for params in PRUNE_CASES:
+        theta, S, R, pct = params
+        Ag, _ = M.prune_inflate(dev(Cm), M.Params(prune_threshold=theta, select_k=S, recover_k=R,
+                                                  recover_pct=pct))
+        Ao, _ = O.prune_inflate(O.as_mat(Cm), theta, S, R, pct, 2.0)
+        G = host_mat(Ag)
+        assert np.array_equal(G.colptr, Ao.colptr) and np.array_equal(G.rows, Ao.rows)
+        np.testing.assert_allclose(G.vals, Ao.vals, rtol=1e-5)
+
+
+# ---------------------------------------------------------------- fused iterate (P1-P3)
+@pytest.mark.parametrize("estimator", [1, 2])
+@pytest.mark.parametrize("name,params", [("C1", (1e-4, 1100, 1400, 0.9)),
+                                         ("C2", (1e-4, 100, 100, 0.9))])
+def test_iterate_step_parity(name, params, estimator):
+    theta, S, R, pct = params
+    A = f32(O.preprocess(synth.config_graph(name)))
+    Ag, st = M.iterate(dev(A), M.Params(prune_threshold=theta, select_k=S, recover_k=R,
+                                        recover_pct=pct, estimator=estimator))
+    Cr, fl = O.expand(A)
+    _, info = O.prune_inflate(Cr, theta, S, R, pct, 2.0)
+    stats = kept_parity(host_mat(Ag), Cr, info, params)
+    assert st["flops"] == int(fl.sum())
+    assert st["chaos"] == pytest.approx(info.chaos.max(), rel=1e-3, abs=1e-5)
+    assert stats["band_flip_cols"] <= max(2, A.ncols // 1000)
+
+
+def test_iterate_c1_second_iteration_all_bins():
+    """Iteration 1 of C1 expands to ~1e6 nnz (dense columns); force each bin."""
+    A0 = O.preprocess(synth.planted_partition())
+    Cr, _ = O.expand(A0)
+    A1, _ = O.prune_inflate(Cr, 1e-4, 1100, 1400, 0.9, 2.0)
+    A1 = f32(A1)
+    Cr1, _ = O.expand(A1)
+    _, info = O.prune_inflate(Cr1, 1e-4, 1100, 1400, 0.9, 2.0)
+    for b in (-1, 3, 5, 6):
+        Ag, st = M.iterate(dev(A1), M.Params(force_bin=b, estimator=2))
+        kept_parity(host_mat(Ag), Cr1, info, (1e-4, 1100, 1400, 0.9))
+
+
+# ---------------------------------------------------------------- clusters (P4)
+@pytest.mark.parametrize("seed", range(4))
+def test_clusters_random(seed):
+    Mx = synth.random_sparse(5000, 5000, 0.0003, seed=seed, empty_cols=0.3)
+    lab, k = M.clusters(dev(Mx))
+    lo, ko = O.clusters(Mx)
+    assert k == ko and np.array_equal(lab.cpu().numpy(), lo)
+
+
+@pytest.mark.parametrize("name,params", [("C1", (1e-4, 1100, 1400, 0.9)),
+                                         ("C2", (1e-4, 100, 100, 0.9))])
+def test_full_mcl_clusters_equal(name, params):
+    theta, S, R, pct = params
+    G = synth.config_graph(name)
+    p = M.Params(prune_threshold=theta, select_k=S, recover_k=R, recover_pct=pct)
+    labels, k, hist, _ = M.run(dev(G), p)
+    ref = O.mcl(G, theta=theta, S=S, R=R, pct=pct, eps=1e-3)
+    assert k == ref.nclusters
+    assert np.array_equal(labels.cpu().numpy(), ref.labels)
+    assert abs(len(hist) - ref.iterations) <= 1
+
+
+# ---------------------------------------------------------------- C3 at full size, sampled
+@pytest.mark.slow
+def test_c3_full_size_sampled_columns():
+    G = synth.config_graph("C3")
+    A = O.preprocess(G)
+    A32 = f32(A)
+    Ad = dev(A32)
+    Ag, st = M.iterate(Ad, M.Params())
+    G_ = host_mat(Ag)
+    rng = np.random.default_rng(0)
+    fl_all, _ = M.flops(Ad)
+    heavy = np.argsort(fl_all.cpu().numpy())[-20:]
+    cols = np.unique(np.concatenate([rng.choice(A.ncols, 200, replace=False), heavy]))
+    for j in cols:
+        Cj, _ = O.expand(A32, int(j), int(j) + 1)
+        _, info = O.prune_inflate(Cj, 1e-4, 1100, 1400, 0.9, 2.0)
+        sub = O.Mat(G_.nrows, 1, np.array([0, G_.colptr[j + 1] - G_.colptr[j]], np.int64),
+                    G_.rows[G_.colptr[j]:G_.colptr[j + 1]], G_.vals[G_.colptr[j]:G_.colptr[j + 1]])
+        kept_parity(sub, Cj, info, (1e-4, 1100, 1400, 0.9))
+    # whole-matrix invariants at full size: columns sum to 1, |kept| <= max(S,R)
+    sums = np.add.reduceat(G_.vals.astype(np.float64), G_.colptr[:-1])
+    np.testing.assert_allclose(sums, 1.0, atol=1e-5)
+    assert np.diff(G_.colptr).max() <= 1400
