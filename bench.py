@@ -1,0 +1,410 @@
+#!/usr/bin/env python
+"""bench.py -- expansion-step throughput of the B200 MCL hot path (arXiv:2002.10083).
+
+A "step" is one full pass of the hot path over the
+config's iterate A_0: mcl_iterate = flop count + binning, Cohen estimate (+ exact
+symbolic when the P:1076-1077 policy asks), the fused numeric hash SpGEMM whose
+epilogue thresholds / selects / recovers / inflates / renormalises each column, and
+the assembly of A_1.  With N > 1 GPUs (torchrun), the columns are partitioned across
+ranks (A replicated, the paper's intra-node scheme P:401-406) and every step ends
+with the NCCL all-gather that rebuilds A_1 on every rank (strong scaling).
+
+metric / unit: BASELINE.json's metric, made concrete as the expansion throughput in
+GFLOP/s where one flop is one nontrivial multiply-add a_ik*b_kj of A*A as PAPER.md
+P:173-175 counts flops(AB).  Timing: CUDA events on the stream the library launches
+on, W untimed warm-up steps, K timed steps, barrier + synchronize on both sides, max
+over ranks.  A_0 (333 MB for C3) is larger than the 126 MB L2, so no flush is used.
+
+--impl reference times the CPU oracle (oracle/, plain fp64 C) on a bounded column
+sample of the same workload on the host cores (the tier's reference arm).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+CONFIG_PARAMS = {
+    "C1": dict(prune_threshold=1e-4, select_k=1100, recover_k=1400, recover_pct=0.9),
+    "C2": dict(prune_threshold=1e-4, select_k=100, recover_k=100, recover_pct=0.9),
+    "C3": dict(prune_threshold=1e-4, select_k=1100, recover_k=1400, recover_pct=0.9),
+    "C4": dict(prune_threshold=1e-4, select_k=1100, recover_k=1400, recover_pct=0.9),
+    "C5": dict(prune_threshold=1e-4, select_k=1100, recover_k=1400, recover_pct=0.9),
+}
+METRIC = "expansion SpGEMM GFLOP/s + HBM GB/s (% roofline), MCL iter time at 1/2/4/8 B200"
+UNIT = "GFLOP/s"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ------------------------------------------------------------------ clocks sampler
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception as e:  # pragma: no cover
+            log("clock sampler unavailable:", e)
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["sampler unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ CPU oracle sample
+def oracle_sample(A, target_flops: float, seed: int, params: dict):
+    """Time the CPU oracle (expand + prune/inflate, single-threaded fp64) on a seeded
+    random column sample of A whose flops sum to about target_flops."""
+    import oracle as O
+    rng = np.random.default_rng(seed)
+    deg = np.diff(A.colptr)
+    fl = np.bincount(np.repeat(np.arange(A.ncols), deg), weights=deg[A.rows].astype(np.float64),
+                     minlength=A.ncols)
+    order = rng.permutation(A.ncols)
+    cum = np.cumsum(fl[order])
+    k = int(np.searchsorted(cum, target_flops)) + 1
+    cols = np.sort(order[:k])
+    cnt = deg[cols]
+    cp = np.zeros(len(cols) + 1, np.int64)
+    np.cumsum(cnt, out=cp[1:])
+    idx = np.concatenate([np.arange(A.colptr[c], A.colptr[c + 1]) for c in cols]) \
+        if len(cols) else np.zeros(0, np.int64)
+    B = O.Mat(A.nrows, len(cols), cp, A.rows[idx], A.vals[idx])
+    t0 = time.perf_counter()
+    Cm, f = O.spgemm(A, B)
+    O.prune_inflate(Cm, params["prune_threshold"], params["select_k"], params["recover_k"],
+                    params["recover_pct"], 2.0)
+    dt = time.perf_counter() - t0
+    return float(f.sum()), dt, len(cols)
+
+
+def workload_name(cfg, n, nnz):
+    return f"{cfg} (SURVEY §8(d)) n={n} nnz(A0)={nnz}, MCL iteration 0, fused mcl_iterate"
+
+
+def run_reference(args):
+    """The tier's reference arm: the CPU oracle, as it stands, on host cores."""
+    import oracle as O
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    G = synth.config_graph(args.config, args.scale)
+    A = O.preprocess(G)
+    params = CONFIG_PARAMS[args.config]
+    per_step = args.ref_flops
+    times, flops = [], []
+    for i in range(args.warmup + args.steps):
+        f, dt, ncols = oracle_sample(A, per_step, 1000 + i, params)
+        if i >= args.warmup:
+            times.append(dt)
+            flops.append(f)
+    value = sum(flops) / sum(times) / 1e9
+    sample = (f"{args.steps} steps x seeded random column sample of {args.config} A0 with "
+              f"~{per_step:.2g} flops each (expand + prune/inflate, single thread, fp64)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_name(args.config, A.ncols, A.nnz), "config": args.config,
+                   "parallelism": "1 host core"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ GPU arm
+def load_traffic(kernel_key: str):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        d = json.load(open(p))
+        return d.get(kernel_key)
+    except Exception:
+        return None
+
+
+def allgather_csc(dist, M, blk, n_total, nrows, device):
+    """Rebuild the full next iterate from per-rank column blocks (NCCL all_gather)."""
+    import torch
+    world = dist.get_world_size()
+    nnz = torch.tensor([blk.nnz], dtype=torch.int64, device=device)
+    sizes = [torch.zeros_like(nnz) for _ in range(world)]
+    dist.all_gather(sizes, nnz)
+    sizes = [int(s.item()) for s in sizes]
+    mx = max(sizes + [1])
+    rows = torch.zeros(mx, dtype=torch.int32, device=device)
+    vals = torch.zeros(mx, dtype=torch.float32, device=device)
+    rows[: blk.nnz] = blk.rows
+    vals[: blk.nnz] = blk.vals
+    rg = torch.empty(world * mx, dtype=torch.int32, device=device)
+    vg = torch.empty(world * mx, dtype=torch.float32, device=device)
+    dist.all_gather_into_tensor(rg, rows)
+    dist.all_gather_into_tensor(vg, vals)
+    ncols_each = [(n_total * (r + 1)) // world - (n_total * r) // world for r in range(world)]
+    cmx = max(ncols_each) + 1
+    cpl = torch.zeros(cmx, dtype=torch.int64, device=device)
+    cpl[: blk.ncols + 1] = blk.colptr
+    cpg = torch.empty(world * cmx, dtype=torch.int64, device=device)
+    dist.all_gather_into_tensor(cpg, cpl)
+    parts_r, parts_v, parts_c = [], [], []
+    off = 0
+    for r in range(world):
+        parts_r.append(rg[r * mx: r * mx + sizes[r]])
+        parts_v.append(vg[r * mx: r * mx + sizes[r]])
+        c = cpg[r * cmx: r * cmx + ncols_each[r] + 1]
+        parts_c.append((c[:-1] if r < world - 1 else c) + off)
+        off += sizes[r]
+    return M.CSC(nrows, n_total, torch.cat(parts_c), torch.cat(parts_r), torch.cat(parts_v))
+
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2002_10083_b200 as M
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+
+    t0 = time.time()
+    G = synth.config_graph(args.config, args.scale)
+    log(f"[rank {rank}] generated {args.config}: n={G.ncols} nnz={G.nnz} in {time.time()-t0:.1f}s")
+    Gd = M.CSC.from_host(G, device=dev)
+    ctx = M.context()
+    A = ctx.preprocess(Gd)
+    del Gd
+    n = A.ncols
+    params = M.Params(**CONFIG_PARAMS[args.config])
+    b = (n * rank) // world
+    e = (n * (rank + 1)) // world
+
+    def step():
+        if world == 1:
+            out, st = ctx.iterate(A, params)
+            return out, st
+        blk, st = ctx.iterate(A, params, cols=(b, e))
+        full = allgather_csc(dist, M, blk, n, A.nrows, dev)
+        return full, st
+
+    for _ in range(args.warmup):
+        out, st = step()
+        del out
+    torch.cuda.synchronize()
+
+    clocks = Clocks(local)
+    clocks.start()
+    stream = torch.cuda.current_stream()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    stats = []
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev[0].record(stream)
+    for i in range(args.steps):
+        out, st = step()
+        ev[i + 1].record(stream)
+        stats.append(st)
+        del out
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    total_ms = ev[0].elapsed_time(ev[-1])
+    step_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
+    clk = clocks.stop()
+
+    flops_rank = stats[0]["flops"]
+    flops_total = flops_rank
+    if world > 1:
+        t = torch.tensor([total_ms, float(flops_rank)], dtype=torch.float64, device=dev)
+        tl = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(tl, t)
+        total_ms = max(float(x[0]) for x in tl)
+        flops_total = sum(int(x[1]) for x in tl)
+    ms_per_step = total_ms / args.steps
+    value = flops_total / (ms_per_step / 1e3) / 1e9
+
+    # ---- roofline of the dominant kernel (the heaviest SpGEMM bin), live CUDA events
+    nb = len(stats[0]["bin_ms"])
+    bin_ms = [sum(s["bin_ms"][b_] for s in stats) / len(stats) for b_ in range(nb)]
+    dom = int(np.argmax(bin_ms))
+    s0 = stats[0]
+    alg_bytes = (8 * s0["bin_flops"][dom] + 24 * s0["bin_nnzb"][dom] + 8 * s0["bin_out"][dom]
+                 + 16 * s0["bin_cols"][dom])
+    achieved = alg_bytes / (bin_ms[dom] / 1e3) / 1e9 if bin_ms[dom] > 0 else 0.0
+    peak, peak_src = measured_peaks()
+    kname = f"k_bin<fused,bin{dom}>"
+    traffic = load_traffic(f"{args.config}:{kname}")
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": traffic, "kernel": kname,
+            "kernel_ms": bin_ms[dom], "share_of_step": bin_ms[dom] / (ms_per_step),
+            "alg_bytes": alg_bytes, "peak_source": peak_src,
+            "alg_bytes_formula": "8*flops_bin + 24*nnz(B cols of bin) + 8*kept_out + 16*cols"}
+
+    # ---- e2e: host buffers in, host buffers out, through the public API
+    e2e = None
+    if world == 1 and args.e2e_steps > 0:
+        hc = A.colptr.cpu().pin_memory()
+        hr = A.rows.cpu().pin_memory()
+        hv = A.vals.cpu().pin_memory()
+        h2d = hc.numel() * 8 + hr.numel() * 4 + hv.numel() * 4
+        d2h = 0
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.e2e_steps):
+            Ah = M.CSC(A.nrows, A.ncols, hc.to(dev, non_blocking=True), hr.to(dev, non_blocking=True),
+                       hv.to(dev, non_blocking=True))
+            out, _ = ctx.iterate(Ah, params)
+            oc = torch.empty(out.colptr.shape, dtype=torch.int64, pin_memory=True)
+            orw = torch.empty(out.rows.shape, dtype=torch.int32, pin_memory=True)
+            ov = torch.empty(out.vals.shape, dtype=torch.float32, pin_memory=True)
+            oc.copy_(out.colptr, non_blocking=True)
+            orw.copy_(out.rows, non_blocking=True)
+            ov.copy_(out.vals, non_blocking=True)
+            d2h = oc.numel() * 8 + orw.numel() * 4 + ov.numel() * 4
+            del out, Ah
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = e0.elapsed_time(e1) / args.e2e_steps
+        e2e = {"value": flops_total / (e2e_ms / 1e3) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": e2e_ms}
+
+    # ---- CPU oracle baseline on a bounded sample (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle as O
+        Ah = O.Mat(A.nrows, A.ncols, A.colptr.cpu().numpy(), A.rows.cpu().numpy(),
+                   A.vals.cpu().numpy().astype(np.float64))
+        f, dt, ncols = oracle_sample(Ah, args.cpu_flops, 7, CONFIG_PARAMS[args.config])
+        cpu = {"value": f / dt / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"{ncols} seeded random columns of {args.config} A0 ({f:.3g} flops), "
+                         f"expand + prune/inflate, fp64, single thread, {dt:.1f}s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": workload_name(args.config, n, A.nnz), "config": args.config,
+                       "global_batch": n, "flops_per_step": flops_total,
+                       "nnz_out": int(s0["nnz_out"]) if world == 1 else None,
+                       "parallelism": "1 GPU" if world == 1 else
+                       f"column partition x{world} (A replicated) + NCCL all-gather of A_next",
+                       "l2": "inputs larger than L2 (A0 > 126 MB), no flush",
+                       "estimator_used": int(s0["estimator_used"]),
+                       "stage_ms": {"flops": s0["ms"][0], "estimate": s0["ms"][1],
+                                    "symbolic": s0["ms"][2], "fused_numeric": s0["ms"][3],
+                                    "assemble": s0["ms"][5]},
+                       "bin_cols": s0["bin_cols"], "bin_ms": bin_ms,
+                       "step_ms_min": min(step_ms), "step_ms_max": max(step_ms)},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(sum(s["launches"] for s in stats)),
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C3", choices=list(CONFIG_PARAMS))
+    ap.add_argument("--scale", type=float, default=1.0)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-flops", type=float, default=5e8)
+    ap.add_argument("--ref-flops", type=float, default=2e8)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

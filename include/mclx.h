@@ -105,6 +105,10 @@ typedef struct {
                                 (fused numeric+select+inflate in mcl_iterate), 4 select/inflate
                                 (unfused), 5 assemble, 6 total, 7 numeric launches count      */
     int64_t peak_bytes;      /* peak scratch bytes held by the context                          */
+    int64_t launches;        /* kernels this call launched                                      */
+    float bin_ms[MCL_NUM_BINS + 1];          /* device time of each bin's kernel(s) (events)    */
+    int64_t bin_nnzb[MCL_NUM_BINS + 1];      /* sum of nnz(B_*j) over the bin's columns         */
+    int64_t bin_out[MCL_NUM_BINS + 1];       /* entries the bin wrote (fused: kept entries)     */
 } mcl_stats_t;
 
 /* Allocator callbacks: device memory, stream-ordered.  NULL callbacks select the
@@ -178,6 +182,14 @@ int mcl_prune_inflate(mcl_ctx_t ctx, const mcl_csc_t *C, const mcl_params_t *p,
  * unpruned product never reaches HBM. */
 int mcl_iterate(mcl_ctx_t ctx, const mcl_csc_t *A, const mcl_params_t *p, mcl_csc_t *A_next,
                 mcl_stats_t *st);
+
+/* mcl_iterate restricted to the output columns [col_begin, col_end) (A square):
+ * A_next = the pruned, inflated columns b..e-1 of the next iterate (ncols = e - b,
+ * col0 = A.col0 + b).  Columns are independent given A (pruning is per column,
+ * P:208; inflation per entry), which is what the phases of P:212-218 and the
+ * column partition across GPUs of P:401-406 rely on. */
+int mcl_iterate_range(mcl_ctx_t ctx, const mcl_csc_t *A, int64_t col_begin, int64_t col_end,
+                      const mcl_params_t *p, mcl_csc_t *A_next, mcl_stats_t *st);
 
 /* Alg. 1 line 6: weak connected components of the pattern of A (Q11).
  * labels_dev: caller-owned device int32 [A.ncols]; components are numbered in

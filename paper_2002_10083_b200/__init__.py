@@ -66,11 +66,13 @@ class StatsT(C.Structure):
                 ("chaos", C.c_float), ("phases", C.c_int32), ("retries", C.c_int32),
                 ("estimator_used", C.c_int32), ("bin_cols", C.c_int64 * (NUM_BINS + 1)),
                 ("bin_flops", C.c_int64 * (NUM_BINS + 1)), ("ms", C.c_float * 8),
-                ("peak_bytes", C.c_int64)]
+                ("peak_bytes", C.c_int64), ("launches", C.c_int64),
+                ("bin_ms", C.c_float * (NUM_BINS + 1)), ("bin_nnzb", C.c_int64 * (NUM_BINS + 1)),
+                ("bin_out", C.c_int64 * (NUM_BINS + 1))]
 
     def as_dict(self) -> dict:
         d = {k: getattr(self, k) for k, _ in self._fields_}
-        for k in ("bin_cols", "bin_flops", "ms"):
+        for k in ("bin_cols", "bin_flops", "ms", "bin_ms", "bin_nnzb", "bin_out"):
             d[k] = list(d[k])
         return d
 
@@ -101,6 +103,8 @@ _sig = {
                            C.POINTER(StatsT)], C.c_int),
     "mcl_iterate": ([_P, C.POINTER(CscT), C.POINTER(ParamsT), C.POINTER(CscT),
                      C.POINTER(StatsT)], C.c_int),
+    "mcl_iterate_range": ([_P, C.POINTER(CscT), _i64, _i64, C.POINTER(ParamsT), C.POINTER(CscT),
+                           C.POINTER(StatsT)], C.c_int),
     "mcl_clusters": ([_P, C.POINTER(CscT), _P, C.POINTER(_i64)], C.c_int),
     "mcl_merge": ([_P, C.c_int32, C.POINTER(CscT), C.POINTER(CscT)], C.c_int),
 }
@@ -307,11 +311,17 @@ class Context:
         res = self._adopt(out), st.as_dict()
         return (*res, chaos) if return_chaos else res
 
-    def iterate(self, A: CSC, params: Params | None = None):
+    def iterate(self, A: CSC, params: Params | None = None, cols=None):
         self._sync_stream()
         out, st = CscT(), StatsT()
-        self._check(_lib.mcl_iterate(self.h, C.byref(A.c()), C.byref((params or Params()).c()),
-                                     C.byref(out), C.byref(st)))
+        if cols is None:
+            rc = _lib.mcl_iterate(self.h, C.byref(A.c()), C.byref((params or Params()).c()),
+                                  C.byref(out), C.byref(st))
+        else:
+            rc = _lib.mcl_iterate_range(self.h, C.byref(A.c()), int(cols[0]), int(cols[1]),
+                                        C.byref((params or Params()).c()), C.byref(out),
+                                        C.byref(st))
+        self._check(rc)
         return self._adopt(out), st.as_dict()
 
     def clusters(self, A: CSC):
@@ -386,8 +396,8 @@ def prune_inflate(Cm, params=None, return_chaos=False):
     return context().prune_inflate(Cm, params, return_chaos)
 
 
-def iterate(A, params=None):
-    return context().iterate(A, params)
+def iterate(A, params=None, cols=None):
+    return context().iterate(A, params, cols)
 
 
 def clusters(A):

@@ -32,6 +32,7 @@ struct mcl_ctx {
     int occ[3][kNumBins + 1] = {};
     void *pin = nullptr;  // pinned host staging for small read-backs
     cudaEvent_t ev[8] = {};
+    cudaEvent_t bev[2 * (kNumBins + 1)] = {};
 };
 
 namespace {
@@ -208,7 +209,8 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
     counters = counts + NB1;
     retry_count = counters + NB1;
     err = retry_count + 1;
-    RC(scratch_t(c, "bin_flops", NB1, &bflops));
+    RC(scratch_t(c, "bin_flops", 3 * NB1, &bflops));
+    unsigned long long *bnnzb = bflops + NB1, *bout = bflops + 2 * NB1;
     RC(scratch_t(c, "bin_lists", (size_t)NB1 * std::max<int64_t>(n, 1), &lists));
     RC(scratch_t(c, "gcap_col", (size_t)std::max<int64_t>(n, 1), &gcap_col));
     RC(scratch_t(c, "retry_list", (size_t)std::max<int64_t>(n, 1), &retry_list));
@@ -219,7 +221,7 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
     const int32_t *cls_list = nullptr;
     for (int round = 0; round < 2; round++) {
         CK(cudaMemsetAsync(counts, 0, sizeof(int) * (2 * NB1 + 1), c->stream));
-        CK(cudaMemsetAsync(bflops, 0, sizeof(unsigned long long) * NB1, c->stream));
+        CK(cudaMemsetAsync(bflops, 0, sizeof(unsigned long long) * 3 * NB1, c->stream));
         ClassifyArgs ca;
         memset(&ca, 0, sizeof ca);
         ca.n = ncls;
@@ -237,17 +239,20 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
         ca.lists = lists;
         ca.gcap_col = gcap_col;
         ca.bin_flops = bflops;
+        ca.bin_nnzb = bnnzb;
         CK(launch_classify(ca, c->stream));
         int hc[2 * 8 + 1];
-        unsigned long long hf[8];
+        unsigned long long hf[3 * 8];
         RC(readback(c, counts, sizeof(int) * NB1, hc));
-        RC(readback(c, bflops, sizeof(unsigned long long) * NB1, hf));
+        RC(readback(c, bflops, sizeof(unsigned long long) * 2 * NB1, hf));
         if (st && round == 0) {
             for (int b = 0; b < NB1; b++) {
                 st->bin_cols[b] += hc[b];
                 st->bin_flops[b] += (int64_t)hf[b];
+                st->bin_nnzb[b] += (int64_t)hf[NB1 + b];
             }
         }
+        bool launched[8] = {};
         for (int b = kNumBins; b >= 0; b--) {
             if (hc[b] == 0) continue;
             BinArgs a = base;
@@ -266,6 +271,7 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
             a.retry_list = retry_list;
             a.retry_count = retry_count;
             a.err_flag = err;
+            a.bin_out = bout + b;
             if (b == kNumBins) {
                 int32_t *gcap;
                 int64_t *gcap64, *goff;
@@ -289,10 +295,21 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
             }
             const int occ = std::max(1, c->occ[mode][b]);
             const int grid = (int)std::min<int64_t>(hc[b], (int64_t)occ * c->sms);
+            CK(cudaEventRecord(c->bev[2 * b], c->stream));
             CK(launch_bin(mode, b, a, grid, c->stream));
+            CK(cudaEventRecord(c->bev[2 * b + 1], c->stream));
+            launched[b] = true;
         }
         int nretry = 0;
         RC(readback(c, retry_count, sizeof(int), &nretry));
+        if (st) {
+            for (int b = 0; b < NB1; b++) {
+                if (!launched[b]) continue;
+                float ms = 0.f;
+                CK(cudaEventElapsedTime(&ms, c->bev[2 * b], c->bev[2 * b + 1]));
+                st->bin_ms[b] += ms;
+            }
+        }
         if (nretry == 0) break;
         if (round == 1) return fail(c, MCL_ERR_CUDA, "hash table overflow after exact re-binning");
         if (st) st->retries += nretry;
@@ -300,6 +317,11 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
                            c->stream));
         ncls = nretry;
         cls_list = retry_in;
+    }
+    if (st) {
+        unsigned long long ho[8];
+        RC(readback(c, bout, sizeof(unsigned long long) * NB1, ho));
+        for (int b = 0; b < NB1; b++) st->bin_out[b] += (int64_t)ho[b];
     }
     int herr = 0;
     RC(readback(c, err, sizeof(int), &herr));
@@ -338,6 +360,7 @@ int spgemm_impl(mcl_ctx *c, const mcl_csc_t *A, const mcl_csc_t *B, int64_t cb, 
     const int64_t n = ce - cb;
     Prod pr{A, B, cb, n};
     init_stats(st);
+    const int64_t launches0 = g_launches;
     CK(cudaEventRecord(c->ev[0], c->stream));
     int64_t *f, *nnzc;
     float *est;
@@ -401,6 +424,7 @@ int spgemm_impl(mcl_ctx *c, const mcl_csc_t *A, const mcl_csc_t *B, int64_t cb, 
             st->ms[3] = elapsed(c, 3, 4);
             st->ms[6] = elapsed(c, 0, 4);
             st->peak_bytes = (int64_t)c->peak;
+            st->launches = g_launches - launches0;
         }
         *C = out;
         return MCL_OK;
@@ -487,6 +511,7 @@ int mcl_ctx_create(mcl_ctx_t *out, int device, void *stream, mcl_alloc_fn alloc,
         return MCL_ERR_CUDA;
     }
     for (int i = 0; i < 8; i++) cudaEventCreate(&c->ev[i]);
+    for (int i = 0; i < 2 * (kNumBins + 1); i++) cudaEventCreate(&c->bev[i]);
     for (int m = 0; m < 3; m++)
         for (int b = 0; b <= kNumBins; b++) c->occ[m][b] = bin_occupancy(m, b);
     if (cudaGetLastError() != cudaSuccess) {
@@ -510,6 +535,8 @@ int mcl_ctx_destroy(mcl_ctx_t c) {
     cudaStreamSynchronize(c->stream);
     for (int i = 0; i < 8; i++)
         if (c->ev[i]) cudaEventDestroy(c->ev[i]);
+    for (int i = 0; i < 2 * (kNumBins + 1); i++)
+        if (c->bev[i]) cudaEventDestroy(c->bev[i]);
     if (c->pin) cudaFreeHost(c->pin);
     delete c;
     return MCL_OK;
@@ -649,6 +676,7 @@ int mcl_prune_inflate(mcl_ctx_t c, const mcl_csc_t *C, const mcl_params_t *pin, 
     init_stats(st);
     const int64_t n = C->ncols;
     const PruneParams pp = prune_params(pin);
+    const int64_t launches0 = g_launches;
     CK(cudaEventRecord(c->ev[0], c->stream));
     int64_t *kcap, *soff, *cnt;
     float *chaos, *cmax;
@@ -689,6 +717,7 @@ int mcl_prune_inflate(mcl_ctx_t c, const mcl_csc_t *C, const mcl_params_t *pin, 
         st->ms[5] = elapsed(c, 1, 2);
         st->ms[6] = elapsed(c, 0, 2);
         st->peak_bytes = (int64_t)c->peak;
+        st->launches = g_launches - launches0;
     }
     return MCL_OK;
 }
@@ -696,16 +725,27 @@ int mcl_prune_inflate(mcl_ctx_t c, const mcl_csc_t *C, const mcl_params_t *pin, 
 int mcl_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, mcl_csc_t *A_next,
                 mcl_stats_t *st) {
     if (!c) return MCL_ERR_INVALID_ARG;
+    if (!A) return fail(c, MCL_ERR_INVALID_ARG, "A is NULL");
+    return mcl_iterate_range(c, A, 0, A->ncols, pin, A_next, st);
+}
+
+int mcl_iterate_range(mcl_ctx_t c, const mcl_csc_t *A, int64_t col_begin, int64_t col_end,
+                      const mcl_params_t *pin, mcl_csc_t *A_next, mcl_stats_t *st) {
+    if (!c) return MCL_ERR_INVALID_ARG;
     if (!A_next || !pin) return fail(c, MCL_ERR_INVALID_ARG, "NULL argument");
     zero_csc(A_next);
     cudaSetDevice(c->device);
     RC(check_params(c, pin));
     RC(check_csc(c, A, "A"));
     if (A->nrows != A->ncols) return fail(c, MCL_ERR_DIM, "mcl_iterate needs a square A");
+    if (col_begin < 0 || col_end > A->ncols || col_begin > col_end)
+        return fail(c, MCL_ERR_DIM, "bad column range [%lld,%lld)", (long long)col_begin,
+                    (long long)col_end);
     init_stats(st);
+    const int64_t launches0 = g_launches;
     const mcl_params_t &p = *pin;
-    const int64_t n = A->ncols;
-    Prod pr{A, A, 0, n};
+    const int64_t n = col_end - col_begin;
+    Prod pr{A, A, col_begin, n};
     const PruneParams pp = prune_params(pin);
     CK(cudaEventRecord(c->ev[0], c->stream));
     int64_t *f, *kcap, *soff, *cnt, *nnzc = nullptr;
@@ -725,7 +765,7 @@ int mcl_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, mcl_cs
     RC(scratch(c, "scan_tmp", scan_tmp_bytes(n + 1), &tmp));
 
     // a1: flops and the total
-    CK(launch_flops(n, A->col_ptr, A->col_ptr, A->row_idx, 0, f, c->stream));
+    CK(launch_flops(n, A->col_ptr, A->col_ptr, A->row_idx, col_begin, f, c->stream));
     CK(launch_reduce_i64(f, n, tot, c->stream));
     CK(cudaEventRecord(c->ev[1], c->stream));
     // a2: Cohen estimate, then the P:1076-1077 policy
@@ -776,7 +816,7 @@ int mcl_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, mcl_cs
     int64_t nnz = 0;
     RC(assemble(c, A->nrows, n, cnt, soff, srow, sval, A_next, &nnz));
     A_next->row0 = A->row0;
-    A_next->col0 = A->col0;
+    A_next->col0 = A->col0 + col_begin;
     A_next->n_global = A->n_global ? A->n_global : A->nrows;
     CK(cudaEventRecord(c->ev[5], c->stream));
     float hmax = 0.f;
@@ -796,6 +836,7 @@ int mcl_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, mcl_cs
         st->ms[5] = elapsed(c, 4, 5);
         st->ms[6] = elapsed(c, 0, 5);
         st->peak_bytes = (int64_t)c->peak;
+        st->launches = g_launches - launches0;
     }
     return MCL_OK;
 }

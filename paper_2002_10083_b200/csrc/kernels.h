@@ -21,6 +21,9 @@ constexpr int kFp64Terms = 16384;  // nnz(B_*j) above which a column accumulates
 
 enum Mode { kSym = 0, kNum = 1, kFused = 2 };
 
+// Host-side count of kernel launches issued by this library (reported in mcl_stats_t).
+extern int64_t g_launches;
+
 struct BinArgs {
     // operands: C = A * B[:, cb : cb + ncols_out)
     const int64_t *acp;
@@ -55,6 +58,7 @@ struct BinArgs {
     int32_t *retry_list;
     int *retry_count;
     int *err_flag;
+    unsigned long long *bin_out;  // this bin's output-entry counter (kFused)
     PruneParams pp;
 };
 
@@ -88,6 +92,7 @@ struct ClassifyArgs {
     int32_t *lists;          // [(kNumBins + 1) * list_stride]
     int32_t *gcap_col;       // [ncols_out]
     unsigned long long *bin_flops;  // [kNumBins + 1]
+    unsigned long long *bin_nnzb;   // [kNumBins + 1] sum of nnz(B_*j)
 };
 cudaError_t launch_classify(const ClassifyArgs &c, cudaStream_t s);
 cudaError_t launch_global_layout(int count, const int32_t *list, const int32_t *gcap_col,

@@ -7,6 +7,8 @@
 
 namespace mclx {
 
+int64_t g_launches = 0;
+
 // ------------------------------------------------------------------ flops
 // f_j = sum_{k in inds(B_*j)} nnz(A_*k).  One warp per column.
 __global__ void k_flops(int64_t ncols, const int64_t *__restrict__ acp,
@@ -31,6 +33,7 @@ cudaError_t launch_flops(int64_t ncols, const int64_t *acp, const int64_t *bcp,
     if (ncols <= 0) return cudaSuccess;
     int64_t blocks = (ncols * 32 + 255) / 256;
     if (blocks > 148 * 64) blocks = 148 * 64;
+    ++g_launches;
     k_flops<<<(int)blocks, 256, 0, s>>>(ncols, acp, bcp, brow, cb, f);
     return cudaGetLastError();
 }
@@ -62,12 +65,14 @@ static int red_grid(int64_t n) {
 cudaError_t launch_reduce_i64(const int64_t *x, int64_t n, unsigned long long *out, cudaStream_t s) {
     cudaError_t e = cudaMemsetAsync(out, 0, sizeof(unsigned long long), s);
     if (e != cudaSuccess) return e;
+    ++g_launches;
     k_reduce_i64<<<red_grid(n), 256, 0, s>>>(x, n, out);
     return cudaGetLastError();
 }
 cudaError_t launch_reduce_f32(const float *x, int64_t n, double *out, cudaStream_t s) {
     cudaError_t e = cudaMemsetAsync(out, 0, sizeof(double), s);
     if (e != cudaSuccess) return e;
+    ++g_launches;
     k_reduce_f32<<<red_grid(n), 256, 0, s>>>(x, n, out);
     return cudaGetLastError();
 }
@@ -155,14 +160,17 @@ cudaError_t launch_scan_i64(const int64_t *in, int64_t *out, int64_t n, void *tm
         int64_t *off = (int64_t *)tmp;
         cudaError_t e = cudaMemsetAsync(off, 0, sizeof(int64_t), s);
         if (e != cudaSuccess) return e;
+        ++g_launches;
         k_scan_apply<<<1, kScanNT, 0, s>>>(in, n, off, out);
         return cudaGetLastError();
     }
     int64_t *sums = (int64_t *)tmp;
     int64_t *offs = sums + tiles + 1;
+    ++g_launches;
     k_scan_tiles<<<(unsigned)tiles, kScanNT, 0, s>>>(in, n, sums);
     cudaError_t e = launch_scan_i64(sums, offs, tiles, (void *)(offs + tiles + 1), s);
     if (e != cudaSuccess) return e;
+    ++g_launches;
     k_scan_apply<<<(unsigned)tiles, kScanNT, 0, s>>>(in, n, offs, out);
     return cudaGetLastError();
 }
@@ -194,6 +202,7 @@ __global__ void k_classify(ClassifyArgs c) {
         const int pos = atomicAdd(&c.bin_count[b], 1);
         c.lists[(int64_t)b * c.list_stride + pos] = (int32_t)col;
         atomicAdd(&c.bin_flops[b], (unsigned long long)f);
+        atomicAdd(&c.bin_nnzb[b], (unsigned long long)nb);
         if (b == kNumBins) {
             int64_t cap = 64;
             while (cap < 2 * need) cap <<= 1;
@@ -206,6 +215,7 @@ cudaError_t launch_classify(const ClassifyArgs &c, cudaStream_t s) {
     if (c.n <= 0) return cudaSuccess;
     int64_t b = (c.n + 255) / 256;
     if (b > 148 * 16) b = 148 * 16;
+    ++g_launches;
     k_classify<<<(int)b, 256, 0, s>>>(c);
     return cudaGetLastError();
 }
@@ -221,6 +231,7 @@ __global__ void k_global_layout(int count, const int32_t *list, const int32_t *g
 cudaError_t launch_global_layout(int count, const int32_t *list, const int32_t *gcap_col,
                                  int32_t *gcap, int64_t *gcap64, cudaStream_t s) {
     if (count <= 0) return cudaSuccess;
+    ++g_launches;
     k_global_layout<<<(count + 255) / 256, 256, 0, s>>>(count, list, gcap_col, gcap, gcap64);
     return cudaGetLastError();
 }
@@ -236,6 +247,7 @@ __global__ void k_kcap(int64_t ncols, const int64_t *f, int64_t m, int kmax, int
 cudaError_t launch_kcap(int64_t ncols, const int64_t *flops, int64_t m, int kmax, int64_t *kcap,
                         cudaStream_t s) {
     if (ncols <= 0) return cudaSuccess;
+    ++g_launches;
     k_kcap<<<red_grid(ncols) * 4, 256, 0, s>>>(ncols, flops, m, kmax, kcap);
     return cudaGetLastError();
 }
@@ -250,6 +262,7 @@ __global__ void k_kcap_cp(int64_t ncols, const int64_t *cp, int kmax, int64_t *k
 }
 cudaError_t launch_kcap_cp(int64_t ncols, const int64_t *cp, int kmax, int64_t *kcap, cudaStream_t s) {
     if (ncols <= 0) return cudaSuccess;
+    ++g_launches;
     k_kcap_cp<<<red_grid(ncols) * 4, 256, 0, s>>>(ncols, cp, kmax, kcap);
     return cudaGetLastError();
 }
@@ -276,6 +289,7 @@ cudaError_t launch_copy_cols(int64_t ncols, const int64_t *cnt, const int64_t *s
     if (ncols <= 0) return cudaSuccess;
     int64_t blocks = (ncols * 32 + 255) / 256;
     if (blocks > 148 * 32) blocks = 148 * 32;
+    ++g_launches;
     k_copy_cols<<<(int)blocks, 256, 0, s>>>(ncols, cnt, soff, srow, sval, cp, orow, oval);
     return cudaGetLastError();
 }
@@ -380,6 +394,7 @@ cudaError_t launch_prune(int64_t ncols, const int64_t *ccp, const int32_t *crow,
                          float *chaos, float *chaos_max, const PruneParams &pp, int grid,
                          cudaStream_t s) {
     if (ncols <= 0) return cudaSuccess;
+    ++g_launches;
     k_prune<<<grid, kPruneNT, 0, s>>>(ncols, ccp, crow, cval, soff, srow, sval, scnt, chaos,
                                       chaos_max, pp);
     return cudaGetLastError();
@@ -421,6 +436,7 @@ cudaError_t launch_cohen_keys(int64_t m, int64_t row0, int r, uint64_t seed, flo
     if (m <= 0) return cudaSuccess;
     int64_t b = (m + 255) / 256;
     if (b > 148 * 16) b = 148 * 16;
+    ++g_launches;
     k_cohen_keys<<<(int)b, 256, 0, s>>>(m, row0, r, seed, X, keys_out);
     return cudaGetLastError();
 }
@@ -462,6 +478,7 @@ cudaError_t launch_cohen_min(int64_t ncols, const int64_t *cp, const int32_t *ro
     if (ncols <= 0) return cudaSuccess;
     int64_t blocks = (ncols * 32 + 255) / 256;
     if (blocks > 148 * 32) blocks = 148 * 32;
+    ++g_launches;
     k_cohen_min<<<(int)blocks, 256, 0, s>>>(ncols, cp, row, c0, in, r, out, est);
     return cudaGetLastError();
 }
@@ -492,6 +509,7 @@ __global__ void k_pre_count(int64_t n, const int64_t *gcp, const int32_t *grow, 
 cudaError_t launch_pre_count(int64_t n, const int64_t *gcp, const int32_t *grow, int add_loops,
                              int64_t *cnt, cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
+    ++g_launches;
     k_pre_count<<<red_grid(n) * 4, 256, 0, s>>>(n, gcp, grow, add_loops, cnt);
     return cudaGetLastError();
 }
@@ -540,6 +558,7 @@ cudaError_t launch_pre_fill(int64_t n, const int64_t *gcp, const int32_t *grow, 
     if (n <= 0) return cudaSuccess;
     int64_t blocks = (n * 32 + 255) / 256;
     if (blocks > 148 * 32) blocks = 148 * 32;
+    ++g_launches;
     k_pre_fill<<<(int)blocks, 256, 0, s>>>(n, gcp, grow, gw, add_loops, cp, row, val);
     return cudaGetLastError();
 }
@@ -601,13 +620,17 @@ cudaError_t launch_cc(int64_t n, const int64_t *cp, const int32_t *row, int32_t 
                       cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
     const int g = red_grid(n) * 4;
+    ++g_launches;
     k_cc_init<<<g, 256, 0, s>>>(n, parent);
     int64_t blocks = (n * 32 + 255) / 256;
     if (blocks > 148 * 32) blocks = 148 * 32;
+    ++g_launches;
     k_cc_hook<<<(int)blocks, 256, 0, s>>>(n, cp, row, parent);
+    ++g_launches;
     k_cc_flag<<<g, 256, 0, s>>>(n, parent, flag);
     cudaError_t e = launch_scan_i64(flag, rank, n, scan_tmp, s);
     if (e != cudaSuccess) return e;
+    ++g_launches;
     k_cc_label<<<g, 256, 0, s>>>(n, parent, rank, labels);
     return cudaGetLastError();
 }

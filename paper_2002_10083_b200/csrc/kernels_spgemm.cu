@@ -236,6 +236,7 @@ __global__ void __launch_bounds__(NT) k_bin(BinArgs a) {
         if (tid == 0) {
             a.s_cnt[col] = kept;
             a.chaos[col] = chaos;
+            atomicAdd(a.bin_out, (unsigned long long)kept);
             atomic_max_nonneg_float(a.chaos_max, chaos);
         }
         __syncthreads();
@@ -260,6 +261,7 @@ static int occ_of() {
 
 template <int CAP, int NT, int MODE, bool GLOBAL>
 static cudaError_t launch_of(const BinArgs &a, int grid, cudaStream_t s) {
+    ++g_launches;
     k_bin<CAP, NT, MODE, GLOBAL><<<grid, NT, smem_of<CAP, NT, MODE, GLOBAL>(), s>>>(a);
     return cudaGetLastError();
 }
