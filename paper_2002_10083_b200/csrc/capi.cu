@@ -216,10 +216,19 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
     RC(scratch_t(c, "retry_list", (size_t)std::max<int64_t>(n, 1), &retry_list));
     RC(scratch_t(c, "retry_in", (size_t)std::max<int64_t>(n, 1), &retry_in));
     CK(cudaMemsetAsync(err, 0, sizeof(int), c->stream));
+    int *rowpart;
+    RC(scratch_t(c, "rowpart", (size_t)std::max<int64_t>(pr.A->ncols, 1) * 33, &rowpart));
+    CK(launch_rowpart(pr.A->ncols, pr.A->col_ptr, pr.A->row_idx, pr.A->nrows, rowpart, c->stream));
+    base.rowpart = rowpart;
 
+    // Rounds: 0 sizes by the caller's estimate / exact sizes; 1 re-runs overflowed
+    // columns with 4x the estimate; 2 with the exact upper bound min(f_j, m); 3 puts
+    // what is left (rows concentrated in few row ranges) in the global bin with every
+    // warp slice large enough for the whole column, which cannot overflow.
     int64_t ncls = n;
     const int32_t *cls_list = nullptr;
-    for (int round = 0; round < 2; round++) {
+    const int nrounds = 4;
+    for (int round = 0; round < nrounds; round++) {
         CK(cudaMemsetAsync(counts, 0, sizeof(int) * (2 * NB1 + 1), c->stream));
         CK(cudaMemsetAsync(bflops, 0, sizeof(unsigned long long) * 3 * NB1, c->stream));
         ClassifyArgs ca;
@@ -229,10 +238,11 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
         ca.flops = f;
         ca.bcp = pr.B->col_ptr;
         ca.cb = pr.cb;
-        ca.est = round == 0 ? est : nullptr;
+        ca.est = round < 2 ? est : nullptr;
+        ca.skew_safe = round == 3;
         ca.exact = round == 0 ? exact : nullptr;
         ca.m = pr.A->nrows;
-        ca.alpha = 1.5f;
+        ca.alpha = round == 0 ? 1.2f : 4.8f;
         ca.force_bin = force_bin;
         ca.list_stride = std::max<int64_t>(n, 1);
         ca.bin_count = counts;
@@ -311,7 +321,8 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
             }
         }
         if (nretry == 0) break;
-        if (round == 1) return fail(c, MCL_ERR_CUDA, "hash table overflow after exact re-binning");
+        if (round == nrounds - 1)
+            return fail(c, MCL_ERR_CUDA, "hash table overflow after exact re-binning");
         if (st) st->retries += nretry;
         CK(cudaMemcpyAsync(retry_in, retry_list, sizeof(int32_t) * nretry, cudaMemcpyDeviceToDevice,
                            c->stream));

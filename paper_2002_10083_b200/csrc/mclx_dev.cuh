@@ -158,6 +158,95 @@ __device__ void bitonic_sort(int *keys, V *vals, int P) {
     }
 }
 
+// Sort the K entries (keys, vals)[0, K) by key and write them, values mapped by
+// xf(v) -> float, to out_row / out_val[0, K) in global memory.
+// Interpolation bucket sort: rows are spread over [min, max] (vertex ids carry no
+// order), so nbk ~ K/2 buckets by (row - min) * nbk / (max - min + 1) hold ~2 entries
+// each.  Counters live in the table's free slots keys[K, cap).  Entries are scattered
+// to their bucket's slice of the output, then each bucket (tiny) is insertion-sorted in
+// place.  If some bucket is large (clustered rows), fall back to a shared-memory
+// bitonic sort.  Requires K <= cap (cap a power of two) and K < cap for the counters.
+template <int NT, typename V, class XF>
+__device__ void sort_write(int *keys, V *vals, int K, int cap, int32_t *out_row, float *out_val,
+                           XF xf, int *sh) {
+    if (K <= 0) return;
+    int lo = 0x7fffffff, hi = 0;
+    for (int i = threadIdx.x; i < K; i += NT) {
+        const int r = keys[i];
+        lo = r < lo ? r : lo;
+        hi = r > hi ? r : hi;
+    }
+    lo = -block_max<NT, int>(-lo, sh);
+    hi = block_max<NT, int>(hi, sh);
+    int free_slots = cap - K;
+    int nbk = 1;
+    while (nbk * 2 <= free_slots && nbk * 4 <= K) nbk *= 2;
+    int *cnt = keys + K;
+    if (free_slots >= 1) {
+        for (int i = threadIdx.x; i < nbk; i += NT) cnt[i] = 0;
+        __syncthreads();
+        const uint64_t range = (uint64_t)(hi - lo) + 1;
+        for (int i = threadIdx.x; i < K; i += NT)
+            atomicAdd(&cnt[(int)(((uint64_t)(keys[i] - lo) * nbk) / range)], 1);
+        __syncthreads();
+        // exclusive scan of the counters (contiguous chunks per thread) + largest bucket
+        const int per = (nbk + NT - 1) / NT;
+        const int b0 = threadIdx.x * per;
+        int loc = 0, mx = 0;
+        for (int b = b0; b < b0 + per && b < nbk; b++) {
+            loc += cnt[b];
+            mx = cnt[b] > mx ? cnt[b] : mx;
+        }
+        int tot;
+        int off = block_excl_scan<NT>(loc, sh, tot);
+        mx = block_max<NT, int>(mx, sh);
+        if (mx <= 48) {
+            for (int b = b0; b < b0 + per && b < nbk; b++) {
+                const int c = cnt[b];
+                cnt[b] = off;
+                off += c;
+            }
+            __syncthreads();
+            for (int i = threadIdx.x; i < K; i += NT) {
+                const int r = keys[i];
+                const int pos = atomicAdd(&cnt[(int)(((uint64_t)(r - lo) * nbk) / range)], 1);
+                out_row[pos] = r;
+                out_val[pos] = xf(vals[i]);
+            }
+            __syncthreads();
+            for (int b = threadIdx.x; b < nbk; b += NT) {
+                const int start = b ? cnt[b - 1] : 0, end = cnt[b];
+                for (int i = start + 1; i < end; i++) {
+                    const int r = __ldcg(out_row + i);
+                    const float v = __ldcg(out_val + i);
+                    int j = i - 1;
+                    while (j >= start && __ldcg(out_row + j) > r) {
+                        out_row[j + 1] = __ldcg(out_row + j);
+                        out_val[j + 1] = __ldcg(out_val + j);
+                        j--;
+                    }
+                    out_row[j + 1] = r;
+                    out_val[j + 1] = v;
+                }
+            }
+            __syncthreads();
+            return;
+        }
+        __syncthreads();
+    }
+    // fallback: bitonic sort in place (K <= cap, cap a power of two)
+    int P = 1;
+    while (P < K) P <<= 1;
+    for (int i = K + threadIdx.x; i < P; i += NT) keys[i] = kPadKey;
+    __syncthreads();
+    bitonic_sort<NT, V>(keys, vals, P);
+    for (int i = threadIdx.x; i < K; i += NT) {
+        out_row[i] = keys[i];
+        out_val[i] = xf(vals[i]);
+    }
+    __syncthreads();
+}
+
 // Warp 0 only: find the digit d of a 256-bin histogram at which the running count
 // (from the top digit when DESC, from digit 0 otherwise) first reaches `rem`.
 // out[0] = d, out[1] = count strictly before d in that order, out[2] = hist[d].
