@@ -216,18 +216,14 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
     RC(scratch_t(c, "retry_list", (size_t)std::max<int64_t>(n, 1), &retry_list));
     RC(scratch_t(c, "retry_in", (size_t)std::max<int64_t>(n, 1), &retry_in));
     CK(cudaMemsetAsync(err, 0, sizeof(int), c->stream));
-    int *rowpart;
-    RC(scratch_t(c, "rowpart", (size_t)std::max<int64_t>(pr.A->ncols, 1) * 33, &rowpart));
-    CK(launch_rowpart(pr.A->ncols, pr.A->col_ptr, pr.A->row_idx, pr.A->nrows, rowpart, c->stream));
-    base.rowpart = rowpart;
+
 
     // Rounds: 0 sizes by the caller's estimate / exact sizes; 1 re-runs overflowed
-    // columns with 4x the estimate; 2 with the exact upper bound min(f_j, m); 3 puts
-    // what is left (rows concentrated in few row ranges) in the global bin with every
-    // warp slice large enough for the whole column, which cannot overflow.
+    // columns with 4x the estimate; 2 with the exact upper bound min(f_j, m), which
+    // cannot overflow (load <= 1/2 < the 7/8 fill limit).
     int64_t ncls = n;
     const int32_t *cls_list = nullptr;
-    const int nrounds = 4;
+    const int nrounds = 3;
     for (int round = 0; round < nrounds; round++) {
         CK(cudaMemsetAsync(counts, 0, sizeof(int) * (2 * NB1 + 1), c->stream));
         CK(cudaMemsetAsync(bflops, 0, sizeof(unsigned long long) * 3 * NB1, c->stream));
@@ -239,7 +235,6 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
         ca.bcp = pr.B->col_ptr;
         ca.cb = pr.cb;
         ca.est = round < 2 ? est : nullptr;
-        ca.skew_safe = round == 3;
         ca.exact = round == 0 ? exact : nullptr;
         ca.m = pr.A->nrows;
         ca.alpha = round == 0 ? 1.2f : 4.8f;

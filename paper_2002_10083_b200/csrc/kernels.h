@@ -17,9 +17,7 @@ constexpr int kGlobalThreads = 512;
 __host__ __device__ constexpr int bin_cap(int b) {
     return b == 0 ? 512 : b == 1 ? 1024 : b == 2 ? 2048 : b == 3 ? 4096 : b == 4 ? 8192 : 16384;
 }
-__host__ __device__ constexpr int bin_warps(int b) {
-    return b == 0 ? 2 : b == 1 ? 2 : b == 2 ? 4 : b == 3 ? 8 : b == 4 ? 16 : b == 5 ? 32 : 16;
-}
+
 constexpr int kFp64Terms = 16384;  // nnz(B_*j) above which a column accumulates in fp64 (T)
 
 enum Mode { kSym = 0, kNum = 1, kFused = 2 };
@@ -38,7 +36,6 @@ struct BinArgs {
     const float *bval;
     int64_t cb;
     const int64_t *flops;  // [ncols_out]
-    const int *rowpart;    // [A.ncols][33] row-range index of A (see kernels_spgemm.cu)
     // work list of this bin
     const int32_t *list;
     const int *count;
@@ -72,10 +69,6 @@ cudaError_t launch_bin(int mode, int bin, const BinArgs &a, int grid, cudaStream
 int bin_occupancy(int mode, int bin);
 size_t bin_smem_bytes(int mode, int bin);
 
-// rowpart[k][i] = first position in A_*k whose row >= ceil(i*m/32), i = 0..32
-cudaError_t launch_rowpart(int64_t ncols, const int64_t *cp, const int32_t *row, int64_t m,
-                           int *rowpart, cudaStream_t s);
-
 // misc kernels (kernels_misc.cu)
 cudaError_t launch_flops(int64_t ncols, const int64_t *acp, const int64_t *bcp,
                          const int32_t *brow, int64_t cb, int64_t *f, cudaStream_t s);
@@ -95,7 +88,6 @@ struct ClassifyArgs {
     int64_t m;
     float alpha;
     int force_bin;
-    int skew_safe;           // last resort: global bin, every warp slice holds the whole column
     int64_t list_stride;     // columns per bin list
     int *bin_count;          // [kNumBins + 1]
     int32_t *lists;          // [(kNumBins + 1) * list_stride]

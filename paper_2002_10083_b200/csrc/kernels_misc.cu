@@ -38,36 +38,6 @@ cudaError_t launch_flops(int64_t ncols, const int64_t *acp, const int64_t *bcp,
     return cudaGetLastError();
 }
 
-// ------------------------------------------------------------------ row-range index of A
-// rowpart[k][i] = lower_bound(rows of A_*k, ceil(i*m/32)) - col_ptr[k], i = 0..32.  One
-// warp per column; lane i binary-searches boundary i (independent searches).
-__global__ void k_rowpart(int64_t ncols, const int64_t *__restrict__ cp,
-                          const int32_t *__restrict__ row, int64_t m, int *__restrict__ P) {
-    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = lane_id();
-    for (int64_t k = w; k < ncols; k += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-        const int64_t a = cp[k], b = cp[k + 1];
-        const int64_t bound = ((int64_t)lane * m + 31) / 32;
-        int64_t lo = a, hi = b;
-        while (lo < hi) {
-            const int64_t mid = (lo + hi) >> 1;
-            if ((int64_t)__ldg(row + mid) < bound) lo = mid + 1;
-            else hi = mid;
-        }
-        P[k * 33 + lane] = (int)(lo - a);
-        if (lane == 0) P[k * 33 + 32] = (int)(b - a);
-    }
-}
-cudaError_t launch_rowpart(int64_t ncols, const int64_t *cp, const int32_t *row, int64_t m,
-                           int *rowpart, cudaStream_t s) {
-    if (ncols <= 0) return cudaSuccess;
-    int64_t blocks = (ncols * 32 + 255) / 256;
-    if (blocks > 148 * 32) blocks = 148 * 32;
-    ++g_launches;
-    k_rowpart<<<(int)blocks, 256, 0, s>>>(ncols, cp, row, m, rowpart);
-    return cudaGetLastError();
-}
-
 // ------------------------------------------------------------------ reductions
 __global__ void k_reduce_i64(const int64_t *__restrict__ x, int64_t n, unsigned long long *out) {
     __shared__ int64_t sh[8];
@@ -225,25 +195,17 @@ __global__ void k_classify(ClassifyArgs c) {
             if (e < (double)need) need = (int64_t)e;
         }
         const int64_t nb = c.bcp[c.cb + col + 1] - c.bcp[c.cb + col];
-        // load <= 1/2 plus slack for the spread of rows over the W warp slices
         int b = 0;
-        while (b < kNumBins && need * 2 + 32 * bin_warps(b) > bin_cap(b)) b++;
-        if (nb > kFp64Terms || c.skew_safe) b = kNumBins;
+        while (b < kNumBins && need * 2 > bin_cap(b)) b++;
+        if (nb > kFp64Terms) b = kNumBins;
         if (c.force_bin > b && c.force_bin <= kNumBins) b = c.force_bin;
         const int pos = atomicAdd(&c.bin_count[b], 1);
         c.lists[(int64_t)b * c.list_stride + pos] = (int32_t)col;
         atomicAdd(&c.bin_flops[b], (unsigned long long)f);
         atomicAdd(&c.bin_nnzb[b], (unsigned long long)nb);
         if (b == kNumBins) {
-            const int64_t W = bin_warps(kNumBins);
-            int64_t cap = 64 * W;
-            if (c.skew_safe) {
-                int64_t sc = 64;
-                while (sc < 2 * need) sc <<= 1;
-                cap = sc * W;
-            } else {
-                while (cap < 2 * need + 32 * W) cap <<= 1;
-            }
+            int64_t cap = 64;
+            while (cap < 2 * need) cap <<= 1;
             c.gcap_col[col] = (int32_t)cap;
         }
     }

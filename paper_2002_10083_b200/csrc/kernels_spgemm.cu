@@ -11,72 +11,74 @@
 // C_*j = sum_{k in inds(B_*j)} b_kj A_*k (Gustavson in CSC).  One CTA owns
 // one output column at a time (persistent CTAs pull columns from the bin's work list).
 //
-// ATOMIC-FREE ACCUMULATION.  On sm_100 a shared-memory float atomicAdd is a CAS spin
-// loop (ATOMS.CAST.SPIN) and shared atomics issue at ~2 cycles/lane, which caps an
-// atomic-per-product hash at ~0.3 products/cycle/SM.  Instead, the row space [0, m)
-// is cut into 32 ranges (rowpart index P[k][0..32] of A, computed once per call:
-// P[k][i] = first position in A_*k whose row is >= ceil(i*m/32)).  The CTA's W = NT/32
-// warps each own W-th of the ranges and a private W-th slice of the hash table, and
-// gather only their sub-segment of every A_*k.  A warp therefore never shares a slot
-// with another warp; inside the warp, the claim of an empty slot is resolved
-// warp-synchronously (__match_any_sync on the slot) and the value update is a plain
-// LDS/FADD/STS.  Lanes holding the same row in one instruction (possible when a warp
-// gathers several short sub-segments at once) are serialised by their match rank.
-// Because ranges are ordered, the compacted table is grouped by row range.
+// ACCUMULATION.  One CTA owns one output column.  Its lanes are split into groups of
+// g in {4,8,16,32} lanes (g from the average segment length flops_j / nnz(B_*j)); each
+// group gathers one operand segment A_*k at a time with kUnroll independent (row, val)
+// loads per lane in flight, then inserts a_ik * b_kj into an open-addressing table
+// keyed by row (shared memory in bins 0..5; global memory + fp64 in bin 6).  Slots are
+// claimed with an integer CAS and values added with atomicAdd.  Measured on B200
+// (tools/ubench.cu): a shared-memory float atomicAdd -- a CAS loop (ATOMS.CAST.SPIN) on
+// sm_100 -- sustains ~2.5 lane-ops/cycle/SM, plain LDS/FADD/STS ~4.5 and MATCH.ANY only
+// ~0.5, so atomics are kept and warp-synchronous conflict resolution is not used.  What
+// matters is convergence: every batch loop is warp-uniform (the trip count is the warp
+// max over its groups) and each insert ends with __syncwarp(), otherwise independent
+// thread scheduling fragments the warp after the first divergent probe (profiled at
+// 3-8 active lanes per instruction before this).
 #include <type_traits>
 
 #include "kernels.h"
 
 namespace mclx {
 
-constexpr int kParts = 32;  // row ranges of the rowpart index
 constexpr int kUnroll = 4;  // independent (row, val) gathers per lane in flight
 
-__device__ __forceinline__ unsigned lanemask_lt() {
-    unsigned m;
-    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
-    return m;
+// Open addressing with linear probing.  `fill` counts occupied slots; an insert that
+// would push the load above `limit` (7/8 of cap) reports overflow (-1) at once, so an
+// under-estimated column fails fast instead of probing a full table, and is re-run
+// in a bigger bin.  Returns 1 for a new key, 0 for an existing one.
+template <typename V>
+__device__ __forceinline__ int hash_accum(int *keys, V *vals, uint32_t cap, int row, V v,
+                                          int *fill, int limit) {
+    uint32_t s = hash_slot(row, cap);
+    volatile int *vk = keys;
+    int k = vk[s];
+    int fresh = 0;
+    while (k != row) {  // rare: collision or new key; the common hit skips the loop
+        if (k == kEmptyKey) {
+            if (atomicAdd(fill, 1) >= limit) return -1;
+            const int old = atomicCAS(&keys[s], kEmptyKey, row);
+            if (old == kEmptyKey) {
+                fresh = 1;
+                break;
+            }
+            atomicSub(fill, 1);
+            k = old;  // another lane claimed the slot: re-examine it
+            continue;
+        }
+        s = (s + 1 == cap) ? 0u : s + 1;
+        k = vk[s];
+    }
+    atomicAdd(&vals[s], v);
+    return fresh;
 }
 
-// Warp-synchronous insert of one (row, v) per valid lane into this warp's private
-// slice (keys, vals)[0, scap).  All 32 lanes must call it (uniform control flow).
-// Returns false (warp-uniform) when the slice's fill would pass `limit`.
-template <int MODE, typename V>
-__device__ __forceinline__ bool warp_insert(int *keys, V *vals, uint32_t scap, bool valid, int row,
-                                            V v, bool may_dup, int &fill, int limit) {
-    const unsigned FULL = 0xffffffffu;
-    const int lane = lane_id();
-    if (!__any_sync(FULL, valid)) return true;
-    int rank = 0;
-    unsigned maxrank = 0;
-    if (may_dup) {
-        const unsigned m = __match_any_sync(FULL, valid ? row : -1 - lane);
-        rank = __popc(m & lanemask_lt());
-        maxrank = __reduce_max_sync(FULL, valid ? (unsigned)rank : 0u);
-    }
-    uint32_t s = hash_slot(row, scap);
-    for (unsigned r = 0; r <= maxrank; r++) {
-        bool me = valid && rank == (int)r;
-        while (__any_sync(FULL, me)) {
-            const int k = me ? keys[s] : 0;
-            const bool hit = me && k == row;
-            const bool emp = me && k == kEmptyKey;
-            bool claimed = false;
-            const unsigned em = __ballot_sync(FULL, emp);
-            if (em) {
-                const unsigned grp = __match_any_sync(FULL, emp ? (int)s : -1 - lane);
-                claimed = emp && (__ffs(grp) - 1) == lane;
-                if (claimed) keys[s] = row;
-                fill += __popc(__ballot_sync(FULL, claimed));
-                if (fill > limit) return false;
-            }
-            if (MODE != kSym && (hit || claimed)) vals[s] += v;
-            if (me && !hit && !emp) s = (s + 1 == scap) ? 0u : s + 1;
-            __syncwarp();
-            if (hit || claimed) me = false;
+__device__ __forceinline__ int hash_key(int *keys, uint32_t cap, int row, int *fill, int limit) {
+    uint32_t s = hash_slot(row, cap);
+    volatile int *vk = keys;
+    int k = vk[s];
+    while (k != row) {
+        if (k == kEmptyKey) {
+            if (atomicAdd(fill, 1) >= limit) return -1;
+            const int old = atomicCAS(&keys[s], kEmptyKey, row);
+            if (old == kEmptyKey) return 1;
+            atomicSub(fill, 1);
+            k = old;
+            continue;
         }
+        s = (s + 1 == cap) ? 0u : s + 1;
+        k = vk[s];
     }
-    return true;
+    return 0;
 }
 
 __device__ __forceinline__ int group_size_for(int64_t avg) {
@@ -86,14 +88,12 @@ __device__ __forceinline__ int group_size_for(int64_t avg) {
 template <int CAP, int NT, int MODE, bool GLOBAL>
 __global__ void __launch_bounds__(NT, 1024 / NT) k_bin(BinArgs a) {
     using V = typename std::conditional<GLOBAL, double, float>::type;
-    constexpr int W = NT / 32;            // warps = row-range owners
-    constexpr int PSTEP = kParts / W;     // rowpart boundaries per warp
     extern __shared__ __align__(16) unsigned char dsm[];
     __shared__ unsigned hist[256];
     __shared__ int sint[4];
     __shared__ double sred[NT / 32];
     __shared__ int sscan[NT / 32];
-    __shared__ int s_col, s_idx, s_ovf;
+    __shared__ int s_col, s_idx, s_ovf, s_fill;
     __shared__ int64_t st_start[NT];
     __shared__ int st_k[NT];
     __shared__ float st_b[NT];
@@ -108,6 +108,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_bin(BinArgs a) {
             s_idx = idx;
             s_col = idx < count ? a.list[idx] : -1;
             s_ovf = 0;
+            s_fill = 0;
         }
         __syncthreads();
         const int col = s_col;
@@ -132,67 +133,75 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_bin(BinArgs a) {
         }
         __syncthreads();
 
-        // ---- accumulate: warp `warp` gathers rows in its ranges [warp*PSTEP, +PSTEP)
-        const uint32_t scap = cap / W;
-        int *wkeys = keys + (size_t)warp * scap;
-        V *wvals = vals + (size_t)warp * scap;
-        const int limit = (int)(scap - (scap >> 3));
+        // ---- accumulate C_*j = sum_k b_kj A_*k
+        const int limit = (int)(cap - (cap >> 3));
         const int64_t bj = a.cb + col;
         const int64_t q0 = a.bcp[bj], q1 = a.bcp[bj + 1];
         const int64_t nb = q1 - q0;
-        const int g = group_size_for(nb > 0 ? a.flops[col] / (nb * W) : 0);
+        const int g = group_size_for(nb > 0 ? a.flops[col] / nb : 0);
         const int lane_g = lane & (g - 1);
-        const int grp = lane / g;
-        const int G = 32 / g;  // segments a warp gathers side by side
-        const bool may_dup = G > 1;
-        int fill = 0;
+        const int grp = tid / g;        // group index in the CTA
+        const int ngrp = NT / g;
+        int fresh = 0;
         bool ok = true;
+        volatile int *vovf = &s_ovf;
         for (int64_t c0 = q0; c0 < q1; c0 += NT) {
             const int cnt = (int)((q1 - c0) < NT ? (q1 - c0) : NT);
             if (tid < cnt) {
                 const int k = __ldg(a.brow + c0 + tid);
-                st_k[tid] = k;
-                st_start[tid] = __ldg(a.acp + k);
+                const int64_t st = __ldg(a.acp + k);
+                st_start[tid] = st;
+                st_k[tid] = (int)(__ldg(a.acp + k + 1) - st);  // segment length
                 st_b[tid] = __ldg(a.bval + c0 + tid);
             }
             __syncthreads();
-            if (ok) {
-                for (int e0 = 0; e0 < cnt; e0 += G) {
-                    const int e = e0 + grp;
-                    int64_t lo = 0;
-                    int len = 0;
-                    float bkj = 0.f;
-                    if (e < cnt) {
-                        const int k = st_k[e];
-                        const int *pk = a.rowpart + (int64_t)k * (kParts + 1) + warp * PSTEP;
-                        const int p0 = __ldg(pk), p1 = __ldg(pk + PSTEP);
-                        lo = st_start[e] + p0;
-                        len = p1 - p0;
-                        bkj = st_b[e];
-                    }
-                    const unsigned nbatch = (unsigned)((len + g * kUnroll - 1) / (g * kUnroll));
-                    const unsigned maxb = __reduce_max_sync(0xffffffffu, nbatch);
-                    for (unsigned bi = 0; bi < maxb && ok; bi++) {
-                        int rr[kUnroll];
-                        V vv[kUnroll];
-#pragma unroll
-                        for (int u = 0; u < kUnroll; u++) {
-                            const int t = (int)bi * g * kUnroll + u * g + lane_g;
-                            rr[u] = t < len ? __ldg(a.arow + lo + t) : -1;
-                            float av = (MODE != kSym && t < len) ? __ldg(a.aval + lo + t) : 0.f;
-                            vv[u] = GLOBAL ? (V)av * (V)bkj : (V)(av * bkj);
-                        }
-#pragma unroll
-                        for (int u = 0; u < kUnroll; u++) {
-                            if (!warp_insert<MODE, V>(wkeys, wvals, scap, rr[u] >= 0, rr[u], vv[u],
-                                                      may_dup, fill, limit)) {
-                                ok = false;
-                                break;
-                            }
-                        }
-                    }
-                    if (!ok) break;
+            // warp-uniform sweep: the warp's groups take segments e = e0 + grp
+            const int wgrp0 = warp * (32 / g);
+            for (int e0 = 0; e0 < cnt && ok; e0 += ngrp) {
+                if (e0 + wgrp0 >= cnt) break;  // warp-uniform: none of this warp's groups has work
+                if (*vovf) {
+                    ok = false;
+                    break;
                 }
+                const int e = e0 + grp;
+                int64_t t0 = 0;
+                int len = 0;
+                float bkj = 0.f;
+                if (e < cnt) {
+                    t0 = st_start[e];
+                    len = st_k[e];
+                    bkj = st_b[e];
+                }
+                const unsigned nbatch = (unsigned)((len + g * kUnroll - 1) / (g * kUnroll));
+                const unsigned maxb = __reduce_max_sync(0xffffffffu, nbatch);
+                for (unsigned bi = 0; bi < maxb; bi++) {
+                    int rr[kUnroll];
+                    V vv[kUnroll];
+#pragma unroll
+                    for (int u = 0; u < kUnroll; u++) {
+                        const int t = (int)bi * g * kUnroll + u * g + lane_g;
+                        rr[u] = t < len ? __ldg(a.arow + t0 + t) : -1;
+                        float av = (MODE != kSym && t < len) ? __ldg(a.aval + t0 + t) : 0.f;
+                        vv[u] = GLOBAL ? (V)av * (V)bkj : (V)(av * bkj);
+                    }
+#pragma unroll
+                    for (int u = 0; u < kUnroll; u++) {
+                        if (rr[u] >= 0 && ok) {
+                            const int rc = MODE == kSym
+                                               ? hash_key(keys, cap, rr[u], &s_fill, limit)
+                                               : hash_accum<V>(keys, vals, cap, rr[u], vv[u],
+                                                               &s_fill, limit);
+                            if (rc < 0) {
+                                ok = false;
+                                *vovf = 1;
+                            }
+                            fresh += rc > 0;
+                        }
+                        __syncwarp();  // reconverge after the divergent probe / CAS loops
+                    }
+                    if (!__all_sync(0xffffffffu, ok)) break;
+                }
+                ok = __all_sync(0xffffffffu, ok);
             }
             __syncthreads();
         }
@@ -204,7 +213,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_bin(BinArgs a) {
         }
 
         if (MODE == kSym) {
-            const int nnz = block_sum<NT, int>(lane == 0 ? fill : 0, sscan);
+            const int nnz = block_sum<NT, int>(fresh, sscan);
             if (tid == 0) a.sym_nnz[col] = nnz;
             __syncthreads();
             continue;
