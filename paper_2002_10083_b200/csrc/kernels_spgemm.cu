@@ -30,55 +30,62 @@
 
 namespace mclx {
 
-constexpr int kUnroll = 4;  // independent (row, val) gathers per lane in flight
-
-// Open addressing with linear probing.  `fill` counts occupied slots; an insert that
-// would push the load above `limit` (7/8 of cap) reports overflow (-1) at once, so an
-// under-estimated column fails fast instead of probing a full table, and is re-run
-// in a bigger bin.  Returns 1 for a new key, 0 for an existing one.
-template <typename V>
-__device__ __forceinline__ int hash_accum(int *keys, V *vals, uint32_t cap, int row, V v,
-                                          int *fill, int limit) {
-    uint32_t s = hash_slot(row, cap);
+// Open addressing with linear probing, four keys per lane at a time.  Phase 1 finds
+// the slot of every (row) -- the first probe of all four is issued back to back, and
+// lanes that collide or insert a new key resolve in a warp-uniform loop (claims by
+// integer CAS; `fill` counts occupied slots and an insert that would push the load
+// past `limit` = 7/8 cap reports overflow, so an under-estimated column fails fast
+// and is re-run in a bigger bin).  Phase 2, after the warp reconverges, adds all
+// values together, so the float atomicAdd (a CAS loop on sm_100) runs with full warps.
+// Returns false (warp-uniform) on overflow.  `fresh` counts keys this lane created.
+template <int MODE, typename V>
+__device__ __forceinline__ bool insert4(int *keys, V *vals, uint32_t cap, const int (&row)[4],
+                                        const V (&v)[4], const bool (&valid)[4], int *fill,
+                                        int limit, int &fresh) {
     volatile int *vk = keys;
-    int k = vk[s];
-    int fresh = 0;
-    while (k != row) {  // rare: collision or new key; the common hit skips the loop
-        if (k == kEmptyKey) {
-            if (atomicAdd(fill, 1) >= limit) return -1;
-            const int old = atomicCAS(&keys[s], kEmptyKey, row);
-            if (old == kEmptyKey) {
-                fresh = 1;
-                break;
+    uint32_t s[4];
+    int k[4];
+    bool need[4];
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+        s[j] = hash_slot(row[j], cap);
+        k[j] = valid[j] ? vk[s[j]] : row[j];
+        need[j] = k[j] != row[j];
+    }
+    bool ok = true;
+    while (__any_sync(0xffffffffu, need[0] | need[1] | need[2] | need[3])) {
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            if (!need[j]) continue;
+            if (k[j] == kEmptyKey) {
+                if (atomicAdd(fill, 1) >= limit) {
+                    ok = false;
+                    need[j] = false;
+                    continue;
+                }
+                const int old = atomicCAS(&keys[s[j]], kEmptyKey, row[j]);
+                if (old == kEmptyKey) {
+                    fresh++;
+                    need[j] = false;
+                } else {
+                    atomicSub(fill, 1);
+                    k[j] = old;  // another lane claimed the slot: re-examine it
+                    need[j] = old != row[j];
+                }
+            } else {
+                s[j] = (s[j] + 1 == cap) ? 0u : s[j] + 1;
+                k[j] = vk[s[j]];
+                need[j] = k[j] != row[j];
             }
-            atomicSub(fill, 1);
-            k = old;  // another lane claimed the slot: re-examine it
-            continue;
         }
-        s = (s + 1 == cap) ? 0u : s + 1;
-        k = vk[s];
     }
-    atomicAdd(&vals[s], v);
-    return fresh;
-}
-
-__device__ __forceinline__ int hash_key(int *keys, uint32_t cap, int row, int *fill, int limit) {
-    uint32_t s = hash_slot(row, cap);
-    volatile int *vk = keys;
-    int k = vk[s];
-    while (k != row) {
-        if (k == kEmptyKey) {
-            if (atomicAdd(fill, 1) >= limit) return -1;
-            const int old = atomicCAS(&keys[s], kEmptyKey, row);
-            if (old == kEmptyKey) return 1;
-            atomicSub(fill, 1);
-            k = old;
-            continue;
-        }
-        s = (s + 1 == cap) ? 0u : s + 1;
-        k = vk[s];
+    ok = __all_sync(0xffffffffu, ok);
+    if (MODE != kSym && ok) {
+#pragma unroll
+        for (int j = 0; j < 4; j++)
+            if (valid[j]) atomicAdd(&vals[s[j]], v[j]);
     }
-    return 0;
+    return ok;
 }
 
 __device__ __forceinline__ int group_size_for(int64_t avg) {
@@ -133,12 +140,14 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_bin(BinArgs a) {
         }
         __syncthreads();
 
-        // ---- accumulate C_*j = sum_k b_kj A_*k
+        // ---- accumulate C_*j = sum_k b_kj A_*k.  Each lane gathers 4 consecutive
+        // (row, val) pairs of a segment with one 16-byte load each (segment starts are
+        // aligned down to 4 elements and the head / tail masked).
         const int limit = (int)(cap - (cap >> 3));
         const int64_t bj = a.cb + col;
         const int64_t q0 = a.bcp[bj], q1 = a.bcp[bj + 1];
         const int64_t nb = q1 - q0;
-        const int g = group_size_for(nb > 0 ? a.flops[col] / nb : 0);
+        const int g = group_size_for(nb > 0 ? a.flops[col] / (4 * nb) : 0);
         const int lane_g = lane & (g - 1);
         const int grp = tid / g;        // group index in the CTA
         const int ngrp = NT / g;
@@ -155,49 +164,48 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_bin(BinArgs a) {
                 st_b[tid] = __ldg(a.bval + c0 + tid);
             }
             __syncthreads();
-            // warp-uniform sweep: the warp's groups take segments e = e0 + grp
             const int wgrp0 = warp * (32 / g);
             for (int e0 = 0; e0 < cnt && ok; e0 += ngrp) {
-                if (e0 + wgrp0 >= cnt) break;  // warp-uniform: none of this warp's groups has work
+                if (e0 + wgrp0 >= cnt) break;  // warp-uniform: no work for this warp's groups
                 if (*vovf) {
                     ok = false;
                     break;
                 }
                 const int e = e0 + grp;
-                int64_t t0 = 0;
-                int len = 0;
+                int lo = 0, hi = 0;     // valid element window relative to the aligned base
                 float bkj = 0.f;
+                const int *rp = a.arow;
+                const float *vp = a.aval;
                 if (e < cnt) {
-                    t0 = st_start[e];
-                    len = st_k[e];
+                    const int64_t t0 = st_start[e];
+                    const int64_t ab = t0 & ~(int64_t)3;
+                    rp = a.arow + ab;
+                    vp = a.aval + ab;
+                    lo = (int)(t0 - ab);
+                    hi = lo + st_k[e];
                     bkj = st_b[e];
                 }
-                const unsigned nbatch = (unsigned)((len + g * kUnroll - 1) / (g * kUnroll));
-                const unsigned maxb = __reduce_max_sync(0xffffffffu, nbatch);
-                for (unsigned bi = 0; bi < maxb; bi++) {
-                    int rr[kUnroll];
-                    V vv[kUnroll];
-#pragma unroll
-                    for (int u = 0; u < kUnroll; u++) {
-                        const int t = (int)bi * g * kUnroll + u * g + lane_g;
-                        rr[u] = t < len ? __ldg(a.arow + t0 + t) : -1;
-                        float av = (MODE != kSym && t < len) ? __ldg(a.aval + t0 + t) : 0.f;
-                        vv[u] = GLOBAL ? (V)av * (V)bkj : (V)(av * bkj);
+                const unsigned nstep = (unsigned)((hi + 4 * g - 1) / (4 * g));
+                const unsigned maxs = __reduce_max_sync(0xffffffffu, nstep);
+                for (unsigned si = 0; si < maxs; si++) {
+                    const int i0 = 4 * ((int)si * g + lane_g);
+                    int4 r4 = make_int4(-1, -1, -1, -1);
+                    float4 v4 = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (i0 < hi) {
+                        r4 = __ldg(reinterpret_cast<const int4 *>(rp + i0));
+                        if (MODE != kSym) v4 = __ldg(reinterpret_cast<const float4 *>(vp + i0));
                     }
+                    const int rr[4] = {r4.x, r4.y, r4.z, r4.w};
+                    V pv[4];
+                    bool vld[4];
 #pragma unroll
-                    for (int u = 0; u < kUnroll; u++) {
-                        if (rr[u] >= 0 && ok) {
-                            const int rc = MODE == kSym
-                                               ? hash_key(keys, cap, rr[u], &s_fill, limit)
-                                               : hash_accum<V>(keys, vals, cap, rr[u], vv[u],
-                                                               &s_fill, limit);
-                            if (rc < 0) {
-                                ok = false;
-                                *vovf = 1;
-                            }
-                            fresh += rc > 0;
-                        }
-                        __syncwarp();  // reconverge after the divergent probe / CAS loops
+                    for (int j = 0; j < 4; j++) {
+                        vld[j] = i0 + j >= lo && i0 + j < hi;
+                        pv[j] = GLOBAL ? (V)(&v4.x)[j] * (V)bkj : (V)((&v4.x)[j] * bkj);
+                    }
+                    if (!insert4<MODE, V>(keys, vals, cap, rr, pv, vld, &s_fill, limit, fresh)) {
+                        ok = false;
+                        *vovf = 1;
                     }
                     if (!__all_sync(0xffffffffu, ok)) break;
                 }

@@ -35,6 +35,9 @@ __global__ void kbench(float *out, unsigned seed, long long *cyc) {
             if (k == (int)s) vals[s] += 1.0f;
         } else if (MODE == 5) {     // int CAS
             atomicCAS(&keys[s], (int)s, (int)s);
+        } else if (MODE == 6) {     // 64-bit int atomicAdd (fixed-point accumulator)
+            atomicAdd(reinterpret_cast<unsigned long long *>(vals) + (s >> 1),
+                      (unsigned long long)(x & 0xffff) + 1ull);
         }
     }
     long long t1 = clock64();
@@ -54,8 +57,8 @@ int main() {
     cudaMalloc(&cyc, sizeof(long long) * grid);
     const char *names[] = {"float atomicAdd smem (CAS loop)", "int atomicAdd smem (ATOMS.ADD)",
                            "plain LDS+FADD+STS", "match_any + leader RMW", "LDS key probe + RMW",
-                           "int atomicCAS smem"};
-    for (int mode = 0; mode < 6; mode++) {
+                           "int atomicCAS smem", "u64 atomicAdd smem"};
+    for (int mode = 0; mode < 7; mode++) {
         cudaEvent_t e0, e1;
         cudaEventCreate(&e0);
         cudaEventCreate(&e1);
@@ -68,6 +71,7 @@ int main() {
                 case 3: kbench<3><<<grid, NT>>>(out, 1, cyc); break;
                 case 4: kbench<4><<<grid, NT>>>(out, 1, cyc); break;
                 case 5: kbench<5><<<grid, NT>>>(out, 1, cyc); break;
+                case 6: kbench<6><<<grid, NT>>>(out, 1, cyc); break;
             }
             cudaEventRecord(e1);
             cudaEventSynchronize(e1);
