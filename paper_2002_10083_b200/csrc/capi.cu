@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <unordered_map>
@@ -33,6 +34,8 @@ struct mcl_ctx {
     void *pin = nullptr;  // pinned host staging for small read-backs
     cudaEvent_t ev[8] = {};
     cudaEvent_t bev[2 * (kNumBins + 1)] = {};
+    float alpha = 1.2f;     // table sizing: need = alpha * Cohen estimate + 16
+    float max_load = 0.5f;  // bin when need <= max_load * cap
 };
 
 namespace {
@@ -237,7 +240,8 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
         ca.est = round < 2 ? est : nullptr;
         ca.exact = round == 0 ? exact : nullptr;
         ca.m = pr.A->nrows;
-        ca.alpha = round == 0 ? 1.2f : 4.8f;
+        ca.alpha = round == 0 ? c->alpha : 4.0f * c->alpha;
+        ca.max_load = round == 2 ? 0.5f : c->max_load;
         ca.force_bin = force_bin;
         ca.list_stride = std::max<int64_t>(n, 1);
         ca.bin_count = counts;
@@ -512,6 +516,8 @@ int mcl_ctx_create(mcl_ctx_t *out, int device, void *stream, mcl_alloc_fn alloc,
     c->free_fn = free_fn;
     c->state = alloc_state;
     c->sms = prop.multiProcessorCount;
+    if (const char *e = getenv("MCLX_ALPHA")) c->alpha = (float)atof(e);
+    if (const char *e = getenv("MCLX_MAX_LOAD")) c->max_load = (float)atof(e);
     if (cudaMallocHost(&c->pin, 4096) != cudaSuccess) {
         delete c;
         return MCL_ERR_CUDA;

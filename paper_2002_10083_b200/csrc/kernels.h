@@ -87,6 +87,7 @@ struct ClassifyArgs {
     const int64_t *exact;    // optional
     int64_t m;
     float alpha;
+    float max_load;          // table load factor bound used for binning (<= 0.5 default)
     int force_bin;
     int64_t list_stride;     // columns per bin list
     int *bin_count;          // [kNumBins + 1]

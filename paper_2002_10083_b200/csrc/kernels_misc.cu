@@ -196,7 +196,7 @@ __global__ void k_classify(ClassifyArgs c) {
         }
         const int64_t nb = c.bcp[c.cb + col + 1] - c.bcp[c.cb + col];
         int b = 0;
-        while (b < kNumBins && need * 2 > bin_cap(b)) b++;
+        while (b < kNumBins && (double)need > c.max_load * bin_cap(b)) b++;
         if (nb > kFp64Terms) b = kNumBins;
         if (c.force_bin > b && c.force_bin <= kNumBins) b = c.force_bin;
         const int pos = atomicAdd(&c.bin_count[b], 1);
@@ -205,7 +205,7 @@ __global__ void k_classify(ClassifyArgs c) {
         atomicAdd(&c.bin_nnzb[b], (unsigned long long)nb);
         if (b == kNumBins) {
             int64_t cap = 64;
-            while (cap < 2 * need) cap <<= 1;
+            while ((double)need > c.max_load * cap) cap <<= 1;
             c.gcap_col[col] = (int32_t)cap;
         }
     }
