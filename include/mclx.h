@@ -109,6 +109,8 @@ typedef struct {
     float bin_ms[MCL_NUM_BINS + 1];          /* device time of each bin's kernel(s) (events)    */
     int64_t bin_nnzb[MCL_NUM_BINS + 1];      /* sum of nnz(B_*j) over the bin's columns         */
     int64_t bin_out[MCL_NUM_BINS + 1];       /* entries the bin wrote (fused: kept entries)     */
+    int64_t comm_bytes;      /* bytes this rank received in SUMMA broadcasts                    */
+    int64_t peak_partial;    /* peak live nnz of SUMMA stage partials (Alg. 2 schedule)         */
 } mcl_stats_t;
 
 /* Allocator callbacks: device memory, stream-ordered.  NULL callbacks select the
@@ -199,6 +201,32 @@ int mcl_clusters(mcl_ctx_t ctx, const mcl_csc_t *A, int32_t *labels_dev, int64_t
 /* Merge L equally shaped CSC blocks into their sum (the "merge all lists
  * in L" step of Alg. 2).  Rows sorted, duplicate rows summed. */
 int mcl_merge(mcl_ctx_t ctx, int32_t L, const mcl_csc_t *lists, mcl_csc_t *out);
+
+/* ---------------------------------------------------------------- 2D Sparse SUMMA
+ * P:222-246 §II "Overview of Sparse SUMMA", generalised to a pr x pc grid (Q17): rank
+ * r = i*pc + j owns block (i, j) = rows [i n/pr, (i+1) n/pr) x cols [j n/pc, (j+1) n/pc)
+ * of every iterate.  The inner dimension is cut into s = lcm(pr, pc) panels K_q; at stage
+ * q rank (i, floor(q pc/s)) broadcasts A[rows_i, K_q] along its row communicator and rank
+ * (floor(q pr/s), j) broadcasts A[K_q, cols_j] along its column communicator (NCCL over
+ * NVLink), every rank multiplies the two panels (mcl_spgemm) and the stage partials are
+ * merged on the device under Alg. 2 (binary merge).  The pruning of a column
+ * split over pr ranks exchanges only fixed-size all-reduces (per-column counts and sums,
+ * radix-select digit histograms for the exact top-k cut).
+ */
+
+/* out = A[r0:r1, c0:c1] (local index ranges) as a block: row ids rebased to r0, row0 / col0
+ * advanced by r0 / c0, n_global kept.  Used to distribute an iterate over the grid. */
+int mcl_block(mcl_ctx_t ctx, const mcl_csc_t *A, int64_t r0, int64_t r1, int64_t c0, int64_t c1,
+              mcl_csc_t *out);
+/* rank 0 creates the id and shares it (e.g. through torch.distributed) */
+int mcl_nccl_unique_id(unsigned char out[128]);
+/* collective over the pr*pc ranks: creates the world, row and column communicators */
+int mcl_ctx_set_grid(mcl_ctx_t ctx, int pr, int pc, int rank, const unsigned char id[128]);
+/* One MCL iteration (Alg. 1 lines 3-5) on the distributed iterate.  A: this rank's block
+ * (row0/col0/n_global set as above); A_next: its block of the next iterate.  Collective;
+ * st->chaos is the global chaos. */
+int mcl_summa_iterate(mcl_ctx_t ctx, const mcl_csc_t *A, const mcl_params_t *p, mcl_csc_t *A_next,
+                      mcl_stats_t *st);
 
 #ifdef __cplusplus
 }

@@ -68,7 +68,8 @@ class StatsT(C.Structure):
                 ("bin_flops", C.c_int64 * (NUM_BINS + 1)), ("ms", C.c_float * 8),
                 ("peak_bytes", C.c_int64), ("launches", C.c_int64),
                 ("bin_ms", C.c_float * (NUM_BINS + 1)), ("bin_nnzb", C.c_int64 * (NUM_BINS + 1)),
-                ("bin_out", C.c_int64 * (NUM_BINS + 1))]
+                ("bin_out", C.c_int64 * (NUM_BINS + 1)), ("comm_bytes", C.c_int64),
+                ("peak_partial", C.c_int64)]
 
     def as_dict(self) -> dict:
         d = {k: getattr(self, k) for k, _ in self._fields_}
@@ -107,6 +108,11 @@ _sig = {
                            C.POINTER(StatsT)], C.c_int),
     "mcl_clusters": ([_P, C.POINTER(CscT), _P, C.POINTER(_i64)], C.c_int),
     "mcl_merge": ([_P, C.c_int32, C.POINTER(CscT), C.POINTER(CscT)], C.c_int),
+    "mcl_block": ([_P, C.POINTER(CscT), _i64, _i64, _i64, _i64, C.POINTER(CscT)], C.c_int),
+    "mcl_nccl_unique_id": ([C.c_char * 128], C.c_int),
+    "mcl_ctx_set_grid": ([_P, C.c_int, C.c_int, C.c_int, C.c_char * 128], C.c_int),
+    "mcl_summa_iterate": ([_P, C.POINTER(CscT), C.POINTER(ParamsT), C.POINTER(CscT),
+                           C.POINTER(StatsT)], C.c_int),
 }
 for _name, (_args, _res) in _sig.items():
     _f = getattr(_lib, _name)
@@ -331,6 +337,38 @@ class Context:
         self._check(_lib.mcl_clusters(self.h, C.byref(A.c()), labels.data_ptr(), C.byref(k)))
         return labels, int(k.value)
 
+    def merge(self, lists):
+        """Sum of equally shaped CSC blocks (the merge of Alg. 2 / P:246) on the device."""
+        self._sync_stream()
+        arr = (CscT * len(lists))(*[m.c() for m in lists])
+        out = CscT()
+        self._check(_lib.mcl_merge(self.h, len(lists), arr, C.byref(out)))
+        return self._adopt(out)
+
+    def block(self, A: CSC, rows, cols) -> CSC:
+        """A[r0:r1, c0:c1] as a block (row ids rebased, row0/col0 advanced)."""
+        self._sync_stream()
+        out = CscT()
+        self._check(_lib.mcl_block(self.h, C.byref(A.c()), int(rows[0]), int(rows[1]),
+                                   int(cols[0]), int(cols[1]), C.byref(out)))
+        return self._adopt(out)
+
+    def set_grid(self, pr: int, pc: int, rank: int, uid: bytes):
+        """Collective over pr*pc ranks: NCCL world / row / column communicators."""
+        buf = (C.c_char * 128).from_buffer_copy(uid)
+        with torch.cuda.device(self.device):
+            self._check(_lib.mcl_ctx_set_grid(self.h, pr, pc, rank, buf))
+        self.grid = (pr, pc, rank)
+
+    def summa_iterate(self, A_blk: CSC, params: Params | None = None):
+        """One MCL iteration on the 2D-distributed iterate (collective)."""
+        self._sync_stream()
+        out, st = CscT(), StatsT()
+        self._check(_lib.mcl_summa_iterate(self.h, C.byref(A_blk.c()),
+                                           C.byref((params or Params()).c()), C.byref(out),
+                                           C.byref(st)))
+        return self._adopt(out), st.as_dict()
+
     def run(self, G: CSC, params: Params | None = None, max_iter: int = 100, callback=None):
         """Alg. 1 driven from Python: preprocess, iterate until chaos <
         chaos_eps (Q9) or max_iter, then the components.  Returns (labels, ncl, stats list)."""
@@ -402,6 +440,18 @@ def iterate(A, params=None, cols=None):
 
 def clusters(A):
     return context().clusters(A)
+
+
+def merge(lists):
+    return context().merge(lists)
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_char * 128)()
+    rc = _lib.mcl_nccl_unique_id(buf)
+    if rc != MCL_OK:
+        raise MclError(rc, "ncclGetUniqueId failed")
+    return bytes(buf.raw)
 
 
 def run(G, params=None, max_iter=100, callback=None):

@@ -10,7 +10,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libmclx.so")
-SOURCES = ["kernels_spgemm.cu", "kernels_misc.cu", "capi.cu"]
+SOURCES = ["kernels_spgemm.cu", "kernels_misc.cu", "kernels_summa.cu", "capi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall", "-I", os.path.join(ROOT, "include"),
@@ -43,7 +43,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         objs = list(ex.map(compile_one, SOURCES))
     tmp = LIB + ".tmp"
     subprocess.check_call([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
-                           "-o", tmp, *objs])
+                           "-o", tmp, *objs, "-lnccl"])
     os.replace(tmp, LIB)
     return LIB
 

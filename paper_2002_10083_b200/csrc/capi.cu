@@ -9,6 +9,9 @@
 #include <cstring>
 #include <string>
 #include <unordered_map>
+#include <vector>
+
+#include <nccl.h>
 
 #include "kernels.h"
 #include "mclx.h"
@@ -34,6 +37,9 @@ struct mcl_ctx {
     void *pin = nullptr;  // pinned host staging for small read-backs
     cudaEvent_t ev[8] = {};
     cudaEvent_t bev[2 * (kNumBins + 1)] = {};
+    // 2D Sparse-SUMMA grid (mcl_ctx_set_grid): world / row / column communicators
+    int pr = 1, pc = 1, rank = 0;
+    ncclComm_t world = nullptr, rowc = nullptr, colc = nullptr;
     float alpha = 1.2f;     // table sizing: need = alpha * Cohen estimate + 16
     float max_load = 0.5f;  // bin when need <= max_load * cap
 };
@@ -473,6 +479,168 @@ int assemble(mcl_ctx *c, int64_t nrows, int64_t n, const int64_t *cnt, const int
     return MCL_OK;
 }
 
+int merge_impl(mcl_ctx_t c, int32_t L, const mcl_csc_t *lists, mcl_csc_t *out) {
+    const int64_t m = lists[0].nrows, n = lists[0].ncols;
+    int64_t tot = 0;
+    for (int l = 0; l < L; l++) {
+        RC(check_csc(c, &lists[l], "list"));
+        if (lists[l].nrows != m || lists[l].ncols != n)
+            return fail(c, MCL_ERR_DIM, "merge: list %d has a different shape", l);
+        tot += lists[l].nnz;
+    }
+    // X = [P_0 | ... | P_{L-1}] (m x L*n) and E = stacked identities (L*n x n): X*E = sum_l P_l
+    int64_t *xcp, *ecp;
+    int32_t *xrow, *erow;
+    float *xval, *eval;
+    RC(scratch_t(c, "merge_xcp", (size_t)(L * n + 1), &xcp));
+    RC(scratch_t(c, "merge_xrow", (size_t)std::max<int64_t>(tot, 1), &xrow));
+    RC(scratch_t(c, "merge_xval", (size_t)std::max<int64_t>(tot, 1), &xval));
+    RC(scratch_t(c, "merge_ecp", (size_t)(n + 1), &ecp));
+    RC(scratch_t(c, "merge_erow", (size_t)std::max<int64_t>(L * n, 1), &erow));
+    RC(scratch_t(c, "merge_eval", (size_t)std::max<int64_t>(L * n, 1), &eval));
+    int64_t off = 0;
+    for (int l = 0; l < L; l++) {
+        CK(launch_offset_colptr(n + 1, lists[l].col_ptr, off, xcp + (int64_t)l * n, c->stream));
+        if (lists[l].nnz) {
+            CK(cudaMemcpyAsync(xrow + off, lists[l].row_idx, sizeof(int32_t) * lists[l].nnz,
+                               cudaMemcpyDeviceToDevice, c->stream));
+            CK(cudaMemcpyAsync(xval + off, lists[l].val, sizeof(float) * lists[l].nnz,
+                               cudaMemcpyDeviceToDevice, c->stream));
+        }
+        off += lists[l].nnz;
+    }
+    CK(launch_stack_identity(n, L, ecp, erow, eval, c->stream));
+    mcl_csc_t X, E;
+    zero_csc(&X);
+    zero_csc(&E);
+    X.nrows = m;
+    X.ncols = (int64_t)L * n;
+    X.nnz = tot;
+    X.row0 = lists[0].row0;
+    X.n_global = lists[0].n_global;
+    X.col_ptr = xcp;
+    X.row_idx = xrow;
+    X.val = xval;
+    E.nrows = (int64_t)L * n;
+    E.ncols = n;
+    E.nnz = (int64_t)L * n;
+    E.col_ptr = ecp;
+    E.row_idx = erow;
+    E.val = eval;
+    mcl_params_t p;
+    mcl_params_default(&p);
+    p.estimator = 1;
+    RC(spgemm_impl(c, &X, &E, 0, n, &p, out, nullptr));
+    out->row0 = lists[0].row0;
+    out->col0 = lists[0].col0;
+    out->n_global = lists[0].n_global;
+    return MCL_OK;
+}
+
+
+
+#define NC(call)                                                                              \
+    do {                                                                                      \
+        ncclResult_t r_ = (call);                                                             \
+        if (r_ != ncclSuccess)                                                                \
+            return fail(c, MCL_ERR_NCCL, "%s:%d %s: %s", __FILE__, __LINE__, #call,         \
+                        ncclGetErrorString(r_));                                              \
+    } while (0)
+
+// Stripe / panel boundaries of a 1D cut of [0, n) into `parts` near-equal ranges.  With
+// s = lcm(pr, pc) inner panels every panel lies inside one row stripe and one column
+// stripe (the boundaries coincide exactly, q*n/s = c*n/pc for q = c*s/pc).
+int64_t cut(int64_t n, int parts, int k) { return (int64_t)((__int128)k * n / parts); }
+int gcd_i(int a, int b) { return b ? gcd_i(b, a % b) : a; }
+
+// Distributed prune / select / recover / inflate of a block column set whose columns are
+// split over the ranks of `comm` (the column communicator; nullptr = whole columns).
+int dist_prune(mcl_ctx *c, const mcl_csc_t *C, ncclComm_t comm, const PruneParams &pp,
+               mcl_csc_t *out, float *chaos_out) {
+    const int64_t n = C->ncols;
+    const int64_t n1 = std::max<int64_t>(n, 1);
+    const int grid = (int)std::min<int64_t>(n1, (int64_t)c->sms * 8);
+    int64_t *nnz, *m, *K, *kcnt, *soff, *kcap, *scnt;
+    double *sm, *sums;
+    int8_t *mode;
+    int32_t *rem, *done, *rowcut, *srow;
+    uint32_t *vpre, *rpre;
+    unsigned *hist;
+    float *sval, *cmax;
+    void *tmp;
+    RC(scratch_t(c, "dp_nnz", 3 * n1, &nnz));  // nnz | m | kcnt
+    m = nnz + n1;
+    kcnt = nnz + 2 * n1;
+    RC(scratch_t(c, "dp_K", n1, &K));
+    RC(scratch_t(c, "dp_sm", n1, &sm));
+    RC(scratch_t(c, "dp_sums", 4 * n1, &sums));
+    RC(scratch_t(c, "dp_mode", n1, &mode));
+    RC(scratch_t(c, "dp_i32", 3 * n1, &rem));
+    done = rem + n1;
+    rowcut = rem + 2 * n1;
+    RC(scratch_t(c, "dp_pre", 2 * n1, &vpre));
+    rpre = vpre + n1;
+    RC(scratch_t(c, "dp_hist", 256 * n1, &hist));
+    RC(scratch_t(c, "kcap", n1, &kcap));
+    RC(scratch_t(c, "soff", n1 + 1, &soff));
+    RC(scratch_t(c, "scnt", n1, &scnt));
+    RC(scratch_t(c, "chaos_max", 4, &cmax));
+    RC(scratch(c, "scan_tmp", scan_tmp_bytes(n + 1), &tmp));
+    CK(launch_dp_stats(n, C->col_ptr, C->val, pp.theta, nnz, m, sm, grid, c->stream));
+    if (comm) {
+        NC(ncclGroupStart());
+        NC(ncclAllReduce(nnz, nnz, 2 * n1, ncclInt64, ncclSum, comm, c->stream));
+        NC(ncclAllReduce(sm, sm, n1, ncclFloat64, ncclSum, comm, c->stream));
+        NC(ncclGroupEnd());
+    }
+    CK(launch_dp_branch(n, nnz, m, sm, pp, K, mode, rem, vpre, rowcut, c->stream));
+    CK(cudaMemsetAsync(done, 0, sizeof(int32_t) * n1, c->stream));
+    CK(cudaMemsetAsync(rpre, 0, sizeof(uint32_t) * n1, c->stream));
+    for (int pass = 0; pass < 8; pass++) {
+        CK(launch_dp_hist(n, C->col_ptr, C->row_idx, C->val, C->row0, mode, vpre, rpre, done, pass,
+                          hist, grid, c->stream));
+        if (comm) NC(ncclAllReduce(hist, hist, 256 * n1, ncclUint32, ncclSum, comm, c->stream));
+        CK(launch_dp_digit(n, mode, hist, pass, vpre, rpre, rem, done, rowcut, c->stream));
+    }
+    CK(launch_dp_keepstats(n, C->col_ptr, C->row_idx, C->val, C->row0, mode, vpre, rowcut, pp, kcnt,
+                           sums, grid, c->stream));
+    // staging capacity per local column: the local nnz (kept <= local nnz)
+    CK(launch_kcap_cp(n, C->col_ptr, pp.kmax, kcap, c->stream));
+    if (comm) {
+        NC(ncclGroupStart());
+        NC(ncclAllReduce(kcnt, kcnt, n1, ncclInt64, ncclSum, comm, c->stream));
+        NC(ncclAllReduce(sums, sums, n1, ncclFloat64, ncclSum, comm, c->stream));
+        NC(ncclAllReduce(sums + n1, sums + n1, n1, ncclFloat64, ncclMax, comm, c->stream));
+        NC(ncclAllReduce(sums + 2 * n1, sums + 2 * n1, 2 * n1, ncclFloat64, ncclSum, comm,
+                         c->stream));
+        NC(ncclGroupEnd());
+    }
+    CK(launch_scan_i64(kcap, soff, n, tmp, c->stream));
+    int64_t stot = 0;
+    RC(readback(c, soff + n, sizeof(int64_t), &stot));
+    RC(scratch_t(c, "s_row", (size_t)std::max<int64_t>(stot, 1), &srow));
+    RC(scratch_t(c, "s_val", (size_t)std::max<int64_t>(stot, 1), &sval));
+    CK(cudaMemsetAsync(cmax, 0, sizeof(float), c->stream));
+    CK(launch_dp_write(n, C->col_ptr, C->row_idx, C->val, C->row0, mode, vpre, rowcut, pp, sums,
+                       kcnt, soff, srow, sval, scnt, nullptr, cmax, grid, c->stream));
+    int64_t nnz_out = 0;
+    RC(assemble(c, C->nrows, n, scnt, soff, srow, sval, out, &nnz_out));
+    out->row0 = C->row0;
+    out->col0 = C->col0;
+    out->n_global = C->n_global;
+    float h = 0.f;
+    RC(readback(c, cmax, sizeof(float), &h));
+    *chaos_out = h;
+    return MCL_OK;
+}
+
+void free_csc(mcl_ctx *c, mcl_csc_t *m) {
+    dfree(c, m->col_ptr, 0);
+    dfree(c, m->row_idx, 0);
+    dfree(c, m->val, 0);
+    zero_csc(m);
+}
+
 }  // namespace
 
 // ====================================================================== public API
@@ -543,6 +711,11 @@ int mcl_ctx_set_stream(mcl_ctx_t c, void *stream) {
 int mcl_ctx_destroy(mcl_ctx_t c) {
     if (!c) return MCL_ERR_INVALID_ARG;
     cudaSetDevice(c->device);
+    if (c->world) {
+        ncclCommDestroy(c->rowc);
+        ncclCommDestroy(c->colc);
+        ncclCommDestroy(c->world);
+    }
     for (auto &kv : c->scratch) dfree(c, kv.second.p, kv.second.bytes);
     cudaStreamSynchronize(c->stream);
     for (int i = 0; i < 8; i++)
@@ -876,10 +1049,275 @@ int mcl_clusters(mcl_ctx_t c, const mcl_csc_t *A, int32_t *labels_dev, int64_t *
 
 int mcl_merge(mcl_ctx_t c, int32_t L, const mcl_csc_t *lists, mcl_csc_t *out) {
     if (!c) return MCL_ERR_INVALID_ARG;
-    (void)L;
-    (void)lists;
+    if (!out || !lists || L < 1) return fail(c, MCL_ERR_INVALID_ARG, "bad merge arguments");
     zero_csc(out);
-    return fail(c, MCL_ERR_NOT_IMPLEMENTED, "mcl_merge: not implemented yet");
+    cudaSetDevice(c->device);
+    return merge_impl(c, L, lists, out);
+}
+
+int mcl_block(mcl_ctx_t c, const mcl_csc_t *A, int64_t r0, int64_t r1, int64_t c0, int64_t c1,
+              mcl_csc_t *out) {
+    if (!c) return MCL_ERR_INVALID_ARG;
+    if (!out) return fail(c, MCL_ERR_INVALID_ARG, "out is NULL");
+    zero_csc(out);
+    cudaSetDevice(c->device);
+    RC(check_csc(c, A, "A"));
+    if (r0 < 0 || r1 > A->nrows || r0 > r1 || c0 < 0 || c1 > A->ncols || c0 > c1)
+        return fail(c, MCL_ERR_DIM, "block out of range");
+    const int64_t nc = c1 - c0;
+    int64_t *first, *cnt;
+    void *tmp;
+    RC(scratch_t(c, "blk_first", (size_t)std::max<int64_t>(nc, 1), &first));
+    RC(scratch_t(c, "blk_cnt", (size_t)std::max<int64_t>(nc, 1), &cnt));
+    RC(scratch(c, "scan_tmp", scan_tmp_bytes(nc + 1), &tmp));
+    mcl_csc_t o;
+    zero_csc(&o);
+    o.col_ptr = (int64_t *)dalloc(c, sizeof(int64_t) * (nc + 1));
+    if (!o.col_ptr) return fail(c, MCL_ERR_OOM, "col_ptr");
+    CK(launch_rowslice_count(nc, A->col_ptr + c0, A->row_idx, r0, r1, first, cnt, c->stream));
+    CK(launch_scan_i64(cnt, o.col_ptr, nc, tmp, c->stream));
+    int64_t nnz = 0;
+    RC(readback(c, o.col_ptr + nc, sizeof(int64_t), &nnz));
+    RC(alloc_rows_vals(c, &o, nnz));
+    CK(launch_rowslice_copy(nc, first, o.col_ptr, A->row_idx, A->val, r0, o.row_idx, o.val,
+                            c->stream));
+    o.nrows = r1 - r0;
+    o.ncols = nc;
+    o.row0 = A->row0 + r0;
+    o.col0 = A->col0 + c0;
+    o.n_global = A->n_global ? A->n_global : A->nrows;
+    *out = o;
+    return MCL_OK;
+}
+
+int mcl_nccl_unique_id(unsigned char out[128]) {
+    if (!out) return MCL_ERR_INVALID_ARG;
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return MCL_ERR_NCCL;
+    memcpy(out, id.internal, 128);
+    return MCL_OK;
+}
+
+int mcl_ctx_set_grid(mcl_ctx_t c, int pr, int pc, int rank, const unsigned char id[128]) {
+    if (!c) return MCL_ERR_INVALID_ARG;
+    if (pr < 1 || pc < 1 || rank < 0 || rank >= pr * pc || !id)
+        return fail(c, MCL_ERR_INVALID_ARG, "bad grid %dx%d rank %d", pr, pc, rank);
+    cudaSetDevice(c->device);
+    if (c->world) {
+        ncclCommDestroy(c->rowc);
+        ncclCommDestroy(c->colc);
+        ncclCommDestroy(c->world);
+        c->world = c->rowc = c->colc = nullptr;
+    }
+    ncclUniqueId uid;
+    memcpy(uid.internal, id, 128);
+    NC(ncclCommInitRank(&c->world, pr * pc, uid, rank));
+    const int gi = rank / pc, gj = rank % pc;
+    NC(ncclCommSplit(c->world, gi, gj, &c->rowc, nullptr));
+    NC(ncclCommSplit(c->world, gj, gi, &c->colc, nullptr));
+    c->pr = pr;
+    c->pc = pc;
+    c->rank = rank;
+    return MCL_OK;
+}
+
+int mcl_summa_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, mcl_csc_t *A_next,
+                      mcl_stats_t *st) {
+    if (!c) return MCL_ERR_INVALID_ARG;
+    if (!A_next || !pin) return fail(c, MCL_ERR_INVALID_ARG, "NULL argument");
+    zero_csc(A_next);
+    cudaSetDevice(c->device);
+    if (!c->world) return fail(c, MCL_ERR_INVALID_ARG, "mcl_ctx_set_grid has not been called");
+    RC(check_params(c, pin));
+    RC(check_csc(c, A, "A"));
+    init_stats(st);
+    const int64_t launches0 = g_launches;
+    const int pr = c->pr, pc = c->pc, gi = c->rank / pc, gj = c->rank % pc;
+    const int64_t n = A->n_global;
+    if (A->row0 != cut(n, pr, gi) || A->nrows != cut(n, pr, gi + 1) - cut(n, pr, gi) ||
+        A->col0 != cut(n, pc, gj) || A->ncols != cut(n, pc, gj + 1) - cut(n, pc, gj))
+        return fail(c, MCL_ERR_DIM, "block (%d,%d) does not match the %dx%d grid of n=%lld", gi, gj,
+                    pr, pc, (long long)n);
+    const int s = pr / gcd_i(pr, pc) * pc;  // lcm
+    const int64_t nj = A->ncols, mi = A->nrows;
+    const PruneParams pp = prune_params(pin);
+    CK(cudaEventRecord(c->ev[0], c->stream));
+
+    // ---- sizes of the panels this rank owns, all-gathered once (P:239-243 stage k)
+    int64_t *hdr, *first, *cnt;
+    RC(scratch_t(c, "summa_hdr", (size_t)2 * s * pr * pc, &hdr));
+    RC(scratch_t(c, "summa_first", (size_t)std::max<int64_t>(nj, 1), &first));
+    RC(scratch_t(c, "summa_cnt", (size_t)std::max<int64_t>(nj, 1), &cnt));
+    void *tmp;
+    RC(scratch(c, "scan_tmp", scan_tmp_bytes(nj + 1), &tmp));
+    int64_t *bcp_own;
+    RC(scratch_t(c, "summa_bcp_own", (size_t)s * (nj + 1), &bcp_own));
+    std::vector<int64_t> mine(2 * s, 0);
+    for (int q = 0; q < s; q++) {
+        const int64_t k0 = cut(n, s, q), k1 = cut(n, s, q + 1);
+        if ((int64_t)q * pc / s == gj) {  // A-panel owner: columns K_q of my block
+            int64_t ab[2];
+            RC(readback(c, A->col_ptr + (k0 - A->col0), sizeof(int64_t), &ab[0]));
+            RC(readback(c, A->col_ptr + (k1 - A->col0), sizeof(int64_t), &ab[1]));
+            mine[2 * q] = ab[1] - ab[0];
+        }
+        if ((int64_t)q * pr / s == gi) {  // B-panel owner: rows K_q of my block
+            CK(launch_rowslice_count(nj, A->col_ptr, A->row_idx, k0 - A->row0, k1 - A->row0, first,
+                                     cnt, c->stream));
+            CK(launch_scan_i64(cnt, bcp_own + (int64_t)q * (nj + 1), nj, tmp, c->stream));
+            RC(readback(c, bcp_own + (int64_t)q * (nj + 1) + nj, sizeof(int64_t), &mine[2 * q + 1]));
+        }
+    }
+    CK(cudaMemcpyAsync(hdr + (int64_t)2 * s * c->rank, mine.data(), sizeof(int64_t) * 2 * s,
+                       cudaMemcpyHostToDevice, c->stream));
+    NC(ncclAllGather(hdr + (int64_t)2 * s * c->rank, hdr, 2 * s, ncclInt64, c->world, c->stream));
+    std::vector<int64_t> table((size_t)2 * s * pr * pc);
+    CK(cudaMemcpyAsync(table.data(), hdr, sizeof(int64_t) * table.size(), cudaMemcpyDeviceToHost,
+                       c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+
+    // ---- stages: broadcast panels, local product, Alg. 2 binary merge
+    std::vector<mcl_csc_t> stack;
+    int64_t comm_bytes = 0, peak_partial = 0, live_partial = 0;
+    int rc = MCL_OK;
+    for (int q = 0; q < s && rc == MCL_OK; q++) {
+        const int64_t k0 = cut(n, s, q), k1 = cut(n, s, q + 1), kq = k1 - k0;
+        const int ca = (int)((int64_t)q * pc / s), rb = (int)((int64_t)q * pr / s);
+        const int64_t nnzA = table[(size_t)2 * s * (gi * pc + ca) + 2 * q];
+        const int64_t nnzB = table[(size_t)2 * s * (rb * pc + gj) + 2 * q + 1];
+        int64_t *pacp, *pbcp;
+        int32_t *parow, *pbrow;
+        float *paval, *pbval;
+        RC(scratch_t(c, "pa_cp", (size_t)kq + 1, &pacp));
+        RC(scratch_t(c, "pa_row", (size_t)std::max<int64_t>(nnzA, 1), &parow));
+        RC(scratch_t(c, "pa_val", (size_t)std::max<int64_t>(nnzA, 1), &paval));
+        RC(scratch_t(c, "pb_cp", (size_t)nj + 1, &pbcp));
+        RC(scratch_t(c, "pb_row", (size_t)std::max<int64_t>(nnzB, 1), &pbrow));
+        RC(scratch_t(c, "pb_val", (size_t)std::max<int64_t>(nnzB, 1), &pbval));
+        if (ca == gj) {
+            const int64_t *cps = A->col_ptr + (k0 - A->col0);
+            CK(launch_rebase_colptr(kq + 1, cps, pacp, c->stream));
+            int64_t a0 = 0;
+            RC(readback(c, cps, sizeof(int64_t), &a0));
+            if (nnzA) {
+                CK(cudaMemcpyAsync(parow, A->row_idx + a0, sizeof(int32_t) * nnzA,
+                                   cudaMemcpyDeviceToDevice, c->stream));
+                CK(cudaMemcpyAsync(paval, A->val + a0, sizeof(float) * nnzA, cudaMemcpyDeviceToDevice,
+                                   c->stream));
+            }
+        }
+        if (rb == gi) {
+            const int64_t *ocp = bcp_own + (int64_t)q * (nj + 1);
+            CK(launch_rowslice_count(nj, A->col_ptr, A->row_idx, k0 - A->row0, k1 - A->row0, first,
+                                     cnt, c->stream));
+            CK(cudaMemcpyAsync(pbcp, ocp, sizeof(int64_t) * (nj + 1), cudaMemcpyDeviceToDevice,
+                               c->stream));
+            CK(launch_rowslice_copy(nj, first, pbcp, A->row_idx, A->val, k0 - A->row0, pbrow, pbval,
+                                    c->stream));
+        }
+        NC(ncclGroupStart());
+        NC(ncclBroadcast(pacp, pacp, kq + 1, ncclInt64, ca, c->rowc, c->stream));
+        if (nnzA) {
+            NC(ncclBroadcast(parow, parow, nnzA, ncclInt32, ca, c->rowc, c->stream));
+            NC(ncclBroadcast(paval, paval, nnzA, ncclFloat32, ca, c->rowc, c->stream));
+        }
+        NC(ncclBroadcast(pbcp, pbcp, nj + 1, ncclInt64, rb, c->colc, c->stream));
+        if (nnzB) {
+            NC(ncclBroadcast(pbrow, pbrow, nnzB, ncclInt32, rb, c->colc, c->stream));
+            NC(ncclBroadcast(pbval, pbval, nnzB, ncclFloat32, rb, c->colc, c->stream));
+        }
+        NC(ncclGroupEnd());
+        if (ca != gj) comm_bytes += (kq + 1) * 8 + nnzA * 8;
+        if (rb != gi) comm_bytes += (nj + 1) * 8 + nnzB * 8;
+        mcl_csc_t Pa, Pb, Pq;
+        zero_csc(&Pa);
+        zero_csc(&Pb);
+        Pa.nrows = mi;
+        Pa.ncols = kq;
+        Pa.nnz = nnzA;
+        Pa.row0 = A->row0;
+        Pa.col0 = k0;
+        Pa.n_global = n;
+        Pa.col_ptr = pacp;
+        Pa.row_idx = parow;
+        Pa.val = paval;
+        Pb.nrows = kq;
+        Pb.ncols = nj;
+        Pb.nnz = nnzB;
+        Pb.row0 = k0;
+        Pb.col0 = A->col0;
+        Pb.n_global = n;
+        Pb.col_ptr = pbcp;
+        Pb.row_idx = pbrow;
+        Pb.val = pbval;
+        if ((rc = spgemm_impl(c, &Pa, &Pb, 0, nj, pin, &Pq, nullptr)) != MCL_OK) break;
+        Pq.row0 = A->row0;
+        Pq.col0 = A->col0;
+        Pq.n_global = n;
+        stack.push_back(Pq);
+        live_partial += Pq.nnz;
+        peak_partial = std::max(peak_partial, live_partial);
+        // Alg. 2 lines 5-14: merge nmerges+1 lists when the stage count is even
+        int jj = q + 1, nmerges = 0;
+        while (jj % 2 == 0 && jj != 0) {
+            nmerges++;
+            jj /= 2;
+        }
+        if (nmerges > 0) {
+            std::vector<mcl_csc_t> L(stack.end() - (nmerges + 1), stack.end());
+            mcl_csc_t merged;
+            if ((rc = merge_impl(c, (int32_t)L.size(), L.data(), &merged)) != MCL_OK) break;
+            for (auto &x : L) {
+                live_partial -= x.nnz;
+                free_csc(c, &x);
+            }
+            stack.resize(stack.size() - L.size());
+            stack.push_back(merged);
+            live_partial += merged.nnz;
+            peak_partial = std::max(peak_partial, live_partial);
+        }
+    }
+    if (rc == MCL_OK && stack.size() > 1) {  // Q16: stage counts that are not powers of two
+        mcl_csc_t merged;
+        rc = merge_impl(c, (int32_t)stack.size(), stack.data(), &merged);
+        if (rc == MCL_OK) {
+            for (auto &x : stack) free_csc(c, &x);
+            stack.assign(1, merged);
+        }
+    }
+    if (rc != MCL_OK) {
+        for (auto &x : stack) free_csc(c, &x);
+        return rc;
+    }
+    CK(cudaEventRecord(c->ev[1], c->stream));
+    mcl_csc_t Cb = stack[0];
+    float chaos = 0.f;
+    rc = dist_prune(c, &Cb, pr > 1 ? c->colc : nullptr, pp, A_next, &chaos);
+    const int64_t nnz_unpruned = Cb.nnz;
+    free_csc(c, &Cb);
+    if (rc != MCL_OK) return rc;
+    float *cm;
+    RC(scratch_t(c, "chaos_max", 4, &cm));
+    CK(cudaMemcpyAsync(cm, &chaos, sizeof(float), cudaMemcpyHostToDevice, c->stream));
+    NC(ncclAllReduce(cm, cm, 1, ncclFloat32, ncclMax, c->world, c->stream));
+    RC(readback(c, cm, sizeof(float), &chaos));
+    CK(cudaEventRecord(c->ev[2], c->stream));
+    if (st) {
+        st->nnz_in = A->nnz;
+        st->nnz_unpruned = nnz_unpruned;
+        st->nnz_out = A_next->nnz;
+        st->chaos = chaos;
+        st->phases = 1;
+        st->estimator_used = 1;
+        st->ms[3] = elapsed(c, 0, 1);
+        st->ms[4] = elapsed(c, 1, 2);
+        st->ms[6] = elapsed(c, 0, 2);
+        st->comm_bytes = comm_bytes;
+        st->peak_partial = peak_partial;
+        st->peak_bytes = (int64_t)c->peak;
+        st->launches = g_launches - launches0;
+    }
+    return MCL_OK;
 }
 
 }  // extern "C"

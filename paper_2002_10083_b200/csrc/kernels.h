@@ -103,6 +103,10 @@ cudaError_t launch_kcap(int64_t ncols, const int64_t *flops, int64_t m, int kmax
                         cudaStream_t s);
 cudaError_t launch_kcap_cp(int64_t ncols, const int64_t *cp, int kmax, int64_t *kcap,
                            cudaStream_t s);
+cudaError_t launch_offset_colptr(int64_t n1, const int64_t *cp, int64_t off, int64_t *out,
+                                 cudaStream_t s);
+cudaError_t launch_stack_identity(int64_t n, int L, int64_t *cp, int32_t *row, float *val,
+                                  cudaStream_t s);
 cudaError_t launch_copy_cols(int64_t ncols, const int64_t *cnt, const int64_t *soff,
                              const int32_t *srow, const float *sval, const int64_t *cp,
                              int32_t *orow, float *oval, cudaStream_t s);
@@ -122,5 +126,34 @@ cudaError_t launch_pre_fill(int64_t n, const int64_t *gcp, const int32_t *grow, 
 cudaError_t launch_cc(int64_t n, const int64_t *cp, const int32_t *row, int32_t *parent,
                       int64_t *flag, int64_t *rank, void *scan_tmp, int32_t *labels,
                       cudaStream_t s);
+
+// SUMMA kernels (kernels_summa.cu)
+cudaError_t launch_rebase_colptr(int64_t n1, const int64_t *cp, int64_t *out, cudaStream_t s);
+cudaError_t launch_rowslice_count(int64_t ncols, const int64_t *cp, const int32_t *rows, int64_t r0,
+                                  int64_t r1, int64_t *first, int64_t *cnt, cudaStream_t s);
+cudaError_t launch_rowslice_copy(int64_t ncols, const int64_t *first, const int64_t *ocp,
+                                 const int32_t *rows, const float *vals, int64_t r0, int32_t *orow,
+                                 float *oval, cudaStream_t s);
+cudaError_t launch_dp_stats(int64_t ncols, const int64_t *cp, const float *vals, double theta,
+                            int64_t *nnz, int64_t *m, double *sm, int grid, cudaStream_t s);
+cudaError_t launch_dp_branch(int64_t ncols, const int64_t *nnz, const int64_t *m, const double *sm,
+                             const PruneParams &pp, int64_t *K, int8_t *mode, int32_t *rem,
+                             uint32_t *prefix, int32_t *rowcut, cudaStream_t s);
+cudaError_t launch_dp_hist(int64_t ncols, const int64_t *cp, const int32_t *rows, const float *vals,
+                           int64_t row0, const int8_t *mode, const uint32_t *vprefix,
+                           const uint32_t *rprefix, const int32_t *done, int pass, unsigned *hist,
+                           int grid, cudaStream_t s);
+cudaError_t launch_dp_digit(int64_t ncols, const int8_t *mode, const unsigned *hist, int pass,
+                            uint32_t *vprefix, uint32_t *rprefix, int32_t *rem, int32_t *done,
+                            int32_t *rowcut, cudaStream_t s);
+cudaError_t launch_dp_keepstats(int64_t ncols, const int64_t *cp, const int32_t *rows,
+                                const float *vals, int64_t row0, const int8_t *mode,
+                                const uint32_t *vprefix, const int32_t *rowcut, const PruneParams &pp,
+                                int64_t *kcnt, double *sums, int grid, cudaStream_t s);
+cudaError_t launch_dp_write(int64_t ncols, const int64_t *cp, const int32_t *rows, const float *vals,
+                            int64_t row0, const int8_t *mode, const uint32_t *vprefix,
+                            const int32_t *rowcut, const PruneParams &pp, const double *gsums,
+                            const int64_t *gkcnt, const int64_t *soff, int32_t *srow, float *sval,
+                            int64_t *scnt, float *chaos, float *chaos_max, int grid, cudaStream_t s);
 
 }  // namespace mclx

@@ -267,6 +267,41 @@ cudaError_t launch_kcap_cp(int64_t ncols, const int64_t *cp, int kmax, int64_t *
     return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ merge helpers
+// col_ptr of list l inside the horizontal concatenation X = [P_0 | P_1 | ...]:
+// out[j] = cp[j] + off for j in [0, n] (out is X.col_ptr + l*n).
+__global__ void k_offset_colptr(int64_t n1, const int64_t *cp, int64_t off, int64_t *out) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n1;
+         j += (int64_t)gridDim.x * blockDim.x)
+        out[j] = cp[j] + off;
+}
+cudaError_t launch_offset_colptr(int64_t n1, const int64_t *cp, int64_t off, int64_t *out,
+                                 cudaStream_t s) {
+    if (n1 <= 0) return cudaSuccess;
+    ++g_launches;
+    k_offset_colptr<<<red_grid(n1) * 4, 256, 0, s>>>(n1, cp, off, out);
+    return cudaGetLastError();
+}
+// E = [I; I; ...; I] (L*n x n): column j holds rows j, n+j, ..., (L-1)n+j with value 1,
+// so that X * E = sum_l P_l (the merge of P:246 as a product).
+__global__ void k_stack_identity(int64_t n, int L, int64_t *cp, int32_t *row, float *val) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j <= n;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        cp[j] = (int64_t)L * j;
+        if (j < n)
+            for (int l = 0; l < L; l++) {
+                row[(int64_t)L * j + l] = (int32_t)((int64_t)l * n + j);
+                val[(int64_t)L * j + l] = 1.0f;
+            }
+    }
+}
+cudaError_t launch_stack_identity(int64_t n, int L, int64_t *cp, int32_t *row, float *val,
+                                  cudaStream_t s) {
+    ++g_launches;
+    k_stack_identity<<<red_grid(n + 1) * 4, 256, 0, s>>>(n, L, cp, row, val);
+    return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ assembly
 // Copy each column's cnt entries from its staging slot to the compact CSC.  Warp/column.
 __global__ void k_copy_cols(int64_t ncols, const int64_t *__restrict__ cnt,

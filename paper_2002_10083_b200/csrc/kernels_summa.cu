@@ -1,0 +1,400 @@
+// kernels_summa.cu -- device kernels of the 2D Sparse-SUMMA iteration (PAPER.md P:222-246
+// §II "Overview of Sparse SUMMA"; "selecting top-k entries in each process and then
+// exchanging").
+//
+//   panel extraction   A-panel = columns K_q of the local block (col_ptr rebased),
+//                      B-panel = rows K_q of the local block (row ids rebased to K_q);
+//   distributed prune  a column of C is split over the pr ranks of its column
+//                      communicator.  Every exchange is a fixed-size NCCL all-reduce:
+//                      per-column (nnz, m, s) sums decide the branch (Q5, Q7, Q8); the
+//                      exact top-K cut is found by a radix select whose 256-bin digit
+//                      histograms are all-reduced (4 passes on the fp32 bits of the value,
+//                      then 4 on the global row id for ties); the kept set's sums are
+//                      all-reduced for renormalisation, chaos and inflation.
+#include "kernels.h"
+
+namespace mclx {
+
+// ------------------------------------------------------------------ panels
+__global__ void k_rebase_colptr(int64_t n1, const int64_t *__restrict__ cp, int64_t *__restrict__ out) {
+    const int64_t base = cp[0];
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n1;
+         j += (int64_t)gridDim.x * blockDim.x)
+        out[j] = cp[j] - base;
+}
+cudaError_t launch_rebase_colptr(int64_t n1, const int64_t *cp, int64_t *out, cudaStream_t s) {
+    if (n1 <= 0) return cudaSuccess;
+    int64_t b = (n1 + 255) / 256;
+    if (b > 148 * 16) b = 148 * 16;
+    ++g_launches;
+    k_rebase_colptr<<<(int)b, 256, 0, s>>>(n1, cp, out);
+    return cudaGetLastError();
+}
+
+__device__ __forceinline__ int64_t lb_rows(const int32_t *rows, int64_t lo, int64_t hi, int64_t key) {
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if ((int64_t)rows[mid] < key) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+// per column: first position with row >= r0 and the count of rows in [r0, r1)
+__global__ void k_rowslice_count(int64_t ncols, const int64_t *__restrict__ cp,
+                                 const int32_t *__restrict__ rows, int64_t r0, int64_t r1,
+                                 int64_t *__restrict__ first, int64_t *__restrict__ cnt) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < ncols;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t a = lb_rows(rows, cp[j], cp[j + 1], r0);
+        const int64_t b = lb_rows(rows, a, cp[j + 1], r1);
+        first[j] = a;
+        cnt[j] = b - a;
+    }
+}
+cudaError_t launch_rowslice_count(int64_t ncols, const int64_t *cp, const int32_t *rows, int64_t r0,
+                                  int64_t r1, int64_t *first, int64_t *cnt, cudaStream_t s) {
+    if (ncols <= 0) return cudaSuccess;
+    int64_t b = (ncols + 255) / 256;
+    if (b > 148 * 16) b = 148 * 16;
+    ++g_launches;
+    k_rowslice_count<<<(int)b, 256, 0, s>>>(ncols, cp, rows, r0, r1, first, cnt);
+    return cudaGetLastError();
+}
+__global__ void k_rowslice_copy(int64_t ncols, const int64_t *__restrict__ first,
+                                const int64_t *__restrict__ ocp, const int32_t *__restrict__ rows,
+                                const float *__restrict__ vals, int64_t r0,
+                                int32_t *__restrict__ orow, float *__restrict__ oval) {
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = lane_id();
+    for (int64_t j = w; j < ncols; j += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t src = first[j], dst = ocp[j], n = ocp[j + 1] - dst;
+        for (int64_t i = lane; i < n; i += 32) {
+            orow[dst + i] = (int32_t)(rows[src + i] - r0);
+            oval[dst + i] = vals[src + i];
+        }
+    }
+}
+cudaError_t launch_rowslice_copy(int64_t ncols, const int64_t *first, const int64_t *ocp,
+                                 const int32_t *rows, const float *vals, int64_t r0, int32_t *orow,
+                                 float *oval, cudaStream_t s) {
+    if (ncols <= 0) return cudaSuccess;
+    int64_t b = (ncols * 32 + 255) / 256;
+    if (b > 148 * 32) b = 148 * 32;
+    ++g_launches;
+    k_rowslice_copy<<<(int)b, 256, 0, s>>>(ncols, first, ocp, rows, vals, r0, orow, oval);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ distributed prune
+constexpr int kDP = 256;
+
+// local threshold statistics per column: nnz, m = #{v >= theta}, s = sum{v >= theta}
+__global__ void __launch_bounds__(kDP) k_dp_stats(int64_t ncols, const int64_t *__restrict__ cp,
+                                                  const float *__restrict__ vals, double theta,
+                                                  int64_t *__restrict__ nnz, int64_t *__restrict__ m,
+                                                  double *__restrict__ sm) {
+    __shared__ double sred[kDP / 32];
+    __shared__ int64_t sred64[kDP / 32];
+    for (int64_t j = blockIdx.x; j < ncols; j += gridDim.x) {
+        const int64_t a = cp[j], b = cp[j + 1];
+        int64_t mloc = 0;
+        double sloc = 0.0;
+        for (int64_t t = a + threadIdx.x; t < b; t += kDP) {
+            const double v = (double)vals[t];
+            if (v >= theta) {
+                mloc++;
+                sloc += v;
+            }
+        }
+        mloc = block_sum<kDP, int64_t>(mloc, sred64);
+        sloc = block_sum<kDP, double>(sloc, sred);
+        if (threadIdx.x == 0) {
+            nnz[j] = b - a;
+            m[j] = mloc;
+            sm[j] = sloc;
+        }
+        __syncthreads();
+    }
+}
+cudaError_t launch_dp_stats(int64_t ncols, const int64_t *cp, const float *vals, double theta,
+                            int64_t *nnz, int64_t *m, double *sm, int grid, cudaStream_t s) {
+    if (ncols <= 0) return cudaSuccess;
+    ++g_launches;
+    k_dp_stats<<<grid, kDP, 0, s>>>(ncols, cp, vals, theta, nnz, m, sm);
+    return cudaGetLastError();
+}
+
+// Branch per column from the GLOBAL statistics (same on every rank of the column
+// communicator).  mode: 0 thresh, 1 top-K select, 2 keep all, 3 empty.  Columns that
+// need the select are appended to `sel` (order irrelevant; each rank builds the same
+// set, and the histograms are indexed by column, not by list position).
+__global__ void k_dp_branch(int64_t ncols, const int64_t *__restrict__ nnz,
+                            const int64_t *__restrict__ m, const double *__restrict__ sm,
+                            PruneParams pp, int64_t *__restrict__ K, int8_t *__restrict__ mode,
+                            int32_t *__restrict__ rem, uint32_t *__restrict__ prefix,
+                            int32_t *__restrict__ rowcut) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < ncols;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        int64_t k;
+        const int br = prune_branch(pp, nnz[j], m[j], sm[j], k);
+        int8_t md;
+        if (br == 4) md = 3;
+        else if (br == 0) md = 0;
+        else if (k >= nnz[j]) md = 2;
+        else md = 1;
+        K[j] = k;
+        mode[j] = md;
+        rem[j] = (int32_t)k;
+        prefix[j] = 0;
+        rowcut[j] = 0x7fffffff;
+    }
+}
+cudaError_t launch_dp_branch(int64_t ncols, const int64_t *nnz, const int64_t *m, const double *sm,
+                             const PruneParams &pp, int64_t *K, int8_t *mode, int32_t *rem,
+                             uint32_t *prefix, int32_t *rowcut, cudaStream_t s) {
+    if (ncols <= 0) return cudaSuccess;
+    int64_t b = (ncols + 255) / 256;
+    if (b > 148 * 16) b = 148 * 16;
+    ++g_launches;
+    k_dp_branch<<<(int)b, 256, 0, s>>>(ncols, nnz, m, sm, pp, K, mode, rem, prefix, rowcut);
+    return cudaGetLastError();
+}
+
+// Local 256-bin digit histogram of pass p for every select column j in [0, ncols)
+// (hist[j][256], zero for other columns).  Passes 0-3: value bits, digit (bits >> (24-8p))
+// among entries whose higher bits match prefix.  Passes 4-7: global row id bits among
+// entries whose value bits equal the cut t = vprefix.
+__global__ void __launch_bounds__(kDP) k_dp_hist(int64_t ncols, const int64_t *__restrict__ cp,
+                                                 const int32_t *__restrict__ rows,
+                                                 const float *__restrict__ vals, int64_t row0,
+                                                 const int8_t *__restrict__ mode,
+                                                 const uint32_t *__restrict__ vprefix,
+                                                 const uint32_t *__restrict__ rprefix,
+                                                 const int32_t *__restrict__ done, int pass,
+                                                 unsigned *__restrict__ hist) {
+    __shared__ unsigned h[256];
+    for (int64_t j = blockIdx.x; j < ncols; j += gridDim.x) {
+        if (mode[j] != 1 || done[j]) {
+            for (int i = threadIdx.x; i < 256; i += kDP) hist[j * 256 + i] = 0;
+            continue;
+        }
+        for (int i = threadIdx.x; i < 256; i += kDP) h[i] = 0;
+        __syncthreads();
+        const int64_t a = cp[j], b = cp[j + 1];
+        if (pass < 4) {
+            const int shift = 24 - 8 * pass;
+            const uint32_t mask = pass == 0 ? 0u : (0xFFFFFFFFu << (32 - 8 * pass));
+            const uint32_t pre = vprefix[j];
+            for (int64_t t = a + threadIdx.x; t < b; t += kDP) {
+                const uint32_t bits = __float_as_uint(vals[t]);
+                if ((bits & mask) == pre) atomicAdd(&h[(bits >> shift) & 255u], 1u);
+            }
+        } else {
+            const int q = pass - 4;
+            const int shift = 24 - 8 * q;
+            const uint32_t mask = q == 0 ? 0u : (0xFFFFFFFFu << (32 - 8 * q));
+            const uint32_t t0 = vprefix[j], pre = rprefix[j];
+            for (int64_t t = a + threadIdx.x; t < b; t += kDP) {
+                const uint32_t grow = (uint32_t)(row0 + rows[t]);
+                if (__float_as_uint(vals[t]) == t0 && (grow & mask) == pre)
+                    atomicAdd(&h[(grow >> shift) & 255u], 1u);
+            }
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < 256; i += kDP) hist[j * 256 + i] = h[i];
+        __syncthreads();
+    }
+}
+cudaError_t launch_dp_hist(int64_t ncols, const int64_t *cp, const int32_t *rows, const float *vals,
+                           int64_t row0, const int8_t *mode, const uint32_t *vprefix,
+                           const uint32_t *rprefix, const int32_t *done, int pass, unsigned *hist,
+                           int grid, cudaStream_t s) {
+    if (ncols <= 0) return cudaSuccess;
+    ++g_launches;
+    k_dp_hist<<<grid, kDP, 0, s>>>(ncols, cp, rows, vals, row0, mode, vprefix, rprefix, done, pass,
+                                   hist);
+    return cudaGetLastError();
+}
+
+// Digit step of pass p from the GLOBAL histogram: one warp per select column.
+__global__ void k_dp_digit(int64_t ncols, const int8_t *__restrict__ mode,
+                           const unsigned *__restrict__ hist, int pass, uint32_t *__restrict__ vprefix,
+                           uint32_t *__restrict__ rprefix, int32_t *__restrict__ rem,
+                           int32_t *__restrict__ done, int32_t *__restrict__ rowcut) {
+    __shared__ int sout[8][4];
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lw = threadIdx.x >> 5;
+    const int lane = lane_id();
+    for (int64_t j = w; j < ncols; j += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        if (mode[j] != 1 || done[j]) continue;
+        const int r = rem[j];
+        if (pass < 4) find_digit<true>(hist + j * 256, r, sout[lw]);
+        else find_digit<false>(hist + j * 256, r, sout[lw]);
+        __syncwarp();
+        if (lane == 0) {
+            const int d = sout[lw][0], before = sout[lw][1], eq = sout[lw][2];
+            const int nrem = r - before;
+            if (pass < 4) {
+                const int shift = 24 - 8 * pass;
+                vprefix[j] |= (uint32_t)d << shift;
+                rem[j] = nrem;
+                if (pass == 3 && nrem == eq) {  // every entry equal to the cut is kept
+                    done[j] = 1;
+                    rowcut[j] = 0x7fffffff;
+                }
+            } else {
+                const int shift = 24 - 8 * (pass - 4);
+                rprefix[j] |= (uint32_t)d << shift;
+                rem[j] = nrem;
+                if (pass == 7) {
+                    done[j] = 1;
+                    rowcut[j] = (int32_t)rprefix[j];
+                }
+            }
+        }
+        __syncwarp();
+    }
+}
+cudaError_t launch_dp_digit(int64_t ncols, const int8_t *mode, const unsigned *hist, int pass,
+                            uint32_t *vprefix, uint32_t *rprefix, int32_t *rem, int32_t *done,
+                            int32_t *rowcut, cudaStream_t s) {
+    if (ncols <= 0) return cudaSuccess;
+    int64_t b = (ncols * 32 + 255) / 256;
+    if (b > 148 * 32) b = 148 * 32;
+    ++g_launches;
+    k_dp_digit<<<(int)b, 256, 0, s>>>(ncols, mode, hist, pass, vprefix, rprefix, rem, done, rowcut);
+    return cudaGetLastError();
+}
+
+__device__ __forceinline__ bool dp_keep(int8_t md, float v, uint32_t grow, double theta, uint32_t t,
+                                        int32_t rowcut) {
+    if (md == 0) return (double)v >= theta;
+    if (md == 2) return true;
+    if (md == 1) {
+        const uint32_t b = __float_as_uint(v);
+        return b > t || (b == t && (int32_t)grow <= rowcut);
+    }
+    return false;
+}
+
+// local sums over the kept set: count, sum v, max v, sum v^2, sum v^r
+__global__ void __launch_bounds__(kDP) k_dp_keepstats(int64_t ncols, const int64_t *__restrict__ cp,
+                                                      const int32_t *__restrict__ rows,
+                                                      const float *__restrict__ vals, int64_t row0,
+                                                      const int8_t *__restrict__ mode,
+                                                      const uint32_t *__restrict__ vprefix,
+                                                      const int32_t *__restrict__ rowcut,
+                                                      PruneParams pp, int64_t *__restrict__ kcnt,
+                                                      double *__restrict__ sums /*[4][ncols]*/) {
+    __shared__ double sred[kDP / 32];
+    __shared__ int64_t sred64[kDP / 32];
+    for (int64_t j = blockIdx.x; j < ncols; j += gridDim.x) {
+        const int64_t a = cp[j], b = cp[j + 1];
+        const int8_t md = mode[j];
+        const uint32_t t = vprefix[j];
+        const int32_t rc = rowcut[j];
+        int64_t c = 0;
+        double sv = 0, mx = 0, sq = 0, sr = 0;
+        for (int64_t i = a + threadIdx.x; i < b; i += kDP) {
+            const float v = vals[i];
+            if (dp_keep(md, v, (uint32_t)(row0 + rows[i]), pp.theta, t, rc)) {
+                const double d = (double)v;
+                c++;
+                sv += d;
+                mx = d > mx ? d : mx;
+                sq += d * d;
+                sr += pow_r(d, pp);
+            }
+        }
+        c = block_sum<kDP, int64_t>(c, sred64);
+        sv = block_sum<kDP, double>(sv, sred);
+        mx = block_max<kDP, double>(mx, sred);
+        sq = block_sum<kDP, double>(sq, sred);
+        sr = block_sum<kDP, double>(sr, sred);
+        if (threadIdx.x == 0) {
+            kcnt[j] = c;
+            sums[j] = sv;
+            sums[ncols + j] = mx;
+            sums[2 * ncols + j] = sq;
+            sums[3 * ncols + j] = sr;
+        }
+        __syncthreads();
+    }
+}
+cudaError_t launch_dp_keepstats(int64_t ncols, const int64_t *cp, const int32_t *rows,
+                                const float *vals, int64_t row0, const int8_t *mode,
+                                const uint32_t *vprefix, const int32_t *rowcut, const PruneParams &pp,
+                                int64_t *kcnt, double *sums, int grid, cudaStream_t s) {
+    if (ncols <= 0) return cudaSuccess;
+    ++g_launches;
+    k_dp_keepstats<<<grid, kDP, 0, s>>>(ncols, cp, rows, vals, row0, mode, vprefix, rowcut, pp, kcnt,
+                                        sums);
+    return cudaGetLastError();
+}
+
+// Write the kept entries of every local column (row order preserved) with
+// a' = v^r / sum_global v^r; chaos_j = K (max w - sum w^2) from the global sums
+// (sums = [sv][mx][sq][sr], all-reduced; K = global kept count).
+__global__ void __launch_bounds__(kDP) k_dp_write(int64_t ncols, const int64_t *__restrict__ cp,
+                                                  const int32_t *__restrict__ rows,
+                                                  const float *__restrict__ vals, int64_t row0,
+                                                  const int8_t *__restrict__ mode,
+                                                  const uint32_t *__restrict__ vprefix,
+                                                  const int32_t *__restrict__ rowcut, PruneParams pp,
+                                                  const double *__restrict__ gsums,
+                                                  const int64_t *__restrict__ gkcnt,
+                                                  const int64_t *__restrict__ soff,
+                                                  int32_t *__restrict__ srow, float *__restrict__ sval,
+                                                  int64_t *__restrict__ scnt, float *__restrict__ chaos,
+                                                  float *chaos_max) {
+    __shared__ int sscan[kDP / 32];
+    for (int64_t j = blockIdx.x; j < ncols; j += gridDim.x) {
+        const int64_t a = cp[j];
+        const int nnz = (int)(cp[j + 1] - a);
+        const int8_t md = mode[j];
+        const uint32_t t = vprefix[j];
+        const int32_t rc = rowcut[j];
+        const double sr = gsums[3 * ncols + j];
+        const int64_t dst = soff[j];
+        int kept = 0;
+        for (int c = 0; c < nnz; c += kDP) {
+            const int i = c + threadIdx.x;
+            int f = 0, r = 0;
+            float v = 0.f;
+            if (i < nnz) {
+                r = rows[a + i];
+                v = vals[a + i];
+                f = dp_keep(md, v, (uint32_t)(row0 + r), pp.theta, t, rc) ? 1 : 0;
+            }
+            int tot;
+            const int pos = block_excl_scan<kDP>(f, sscan, tot);
+            if (f) {
+                srow[dst + kept + pos] = r;
+                sval[dst + kept + pos] = (float)(pow_r((double)v, pp) / sr);
+            }
+            kept += tot;
+        }
+        if (threadIdx.x == 0) {
+            scnt[j] = kept;
+            const double sv = gsums[j], mx = gsums[ncols + j], sq = gsums[2 * ncols + j];
+            const int64_t K = gkcnt[j];
+            const float ch = K > 0 ? (float)((double)K * (mx / sv - sq / (sv * sv))) : 0.0f;
+            if (chaos) chaos[j] = ch;
+            atomic_max_nonneg_float(chaos_max, ch);
+        }
+        __syncthreads();
+    }
+}
+cudaError_t launch_dp_write(int64_t ncols, const int64_t *cp, const int32_t *rows, const float *vals,
+                            int64_t row0, const int8_t *mode, const uint32_t *vprefix,
+                            const int32_t *rowcut, const PruneParams &pp, const double *gsums,
+                            const int64_t *gkcnt, const int64_t *soff, int32_t *srow, float *sval,
+                            int64_t *scnt, float *chaos, float *chaos_max, int grid, cudaStream_t s) {
+    if (ncols <= 0) return cudaSuccess;
+    ++g_launches;
+    k_dp_write<<<grid, kDP, 0, s>>>(ncols, cp, rows, vals, row0, mode, vprefix, rowcut, pp, gsums,
+                                    gkcnt, soff, srow, sval, scnt, chaos, chaos_max);
+    return cudaGetLastError();
+}
+
+}  // namespace mclx

@@ -174,6 +174,15 @@ def test_symbolic_and_flops():
     assert np.array_equal(f.cpu().numpy(), fl) and ftot == int(fl.sum())
 
 
+@pytest.mark.parametrize("L", [1, 2, 3, 5])
+def test_merge_partials(L):
+    """Device merge (Alg. 2's "merge all lists") equals the oracle's list merge."""
+    mats = [synth.random_sparse(3000, 2500, 0.004, seed=50 + s, empty_cols=0.2) for s in range(L)]
+    Mg = M.merge([dev(m) for m in mats])
+    Mo = O.merge(mats)
+    assert_unpruned_parity(host_mat(Mg), Mo, rtol=1e-6)
+
+
 # ---------------------------------------------------------------- Cohen (P5)
 @pytest.mark.parametrize("r,seed", [(3, 1), (10, 7), (16, 123456789)])
 def test_cohen_keys_and_estimates(r, seed):

@@ -1,0 +1,109 @@
+"""Multi-process (gloo, world size 2 and 4 on CPU) check of the Sparse-SUMMA schedule of
+paper_2002_10083_b200.grid: every rank holds only its block, owners broadcast the panels
+named by the grid arithmetic, each rank multiplies them (oracle spgemm) and merges the
+stage partials under Alg. 2; the result must equal the oracle's A.A restricted to the
+block (C_ij = sum_k A_ik B_kj)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle as O
+import synth
+from paper_2002_10083_b200.grid import Grid, binary_merge_schedule
+
+
+def _sub(M, r0, r1, c0, c1):
+    cp, rows, vals = [0], [], []
+    for j in range(c0, c1):
+        a, b = int(M.colptr[j]), int(M.colptr[j + 1])
+        rr = M.rows[a:b]
+        sel = (rr >= r0) & (rr < r1)
+        rows.append(rr[sel] - r0)
+        vals.append(M.vals[a:b][sel])
+        cp.append(cp[-1] + int(sel.sum()))
+    return O.Mat(r1 - r0, c1 - c0, np.array(cp, np.int64),
+                 np.concatenate(rows).astype(np.int32) if rows else np.zeros(0, np.int32),
+                 np.concatenate(vals) if vals else np.zeros(0))
+
+
+def _worker(rank, world, pr, pc, port, errq):
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        g = Grid(pr, pc, rank)
+        A = O.preprocess(synth.planted_partition())
+        n = A.ncols
+        r0, r1 = g.rows(n)
+        c0, c1 = g.cols(n)
+        mine = _sub(A, r0, r1, c0, c1)          # all this rank may read from now on
+        row_groups = [dist.new_group([i * pc + j for j in range(pc)]) for i in range(pr)]
+        col_groups = [dist.new_group([i * pc + j for i in range(pr)]) for j in range(pc)]
+        stack = []
+        sched = binary_merge_schedule(g.s)
+        for q in range(g.s):
+            k0, k1 = g.panel(n, q)
+            ca, rb = g.a_owner_col(q), g.b_owner_row(q)
+            pa = [_sub(mine, 0, r1 - r0, k0 - c0, k1 - c0) if ca == g.j else None]
+            pb = [_sub(mine, k0 - r0, k1 - r0, 0, c1 - c0) if rb == g.i else None]
+            dist.broadcast_object_list(pa, src=g.i * pc + ca, group=row_groups[g.i])
+            dist.broadcast_object_list(pb, src=rb * pc + g.j, group=col_groups[g.j])
+            P, _ = O.spgemm(pa[0], pb[0])
+            stack.append(P)
+            nm = sched[q][1]
+            if nm:
+                L = [stack.pop() for _ in range(nm + 1)][::-1]
+                stack.append(O.merge(L))
+        Cb = stack.pop() if len(stack) == 1 else O.merge(stack)
+        full, _ = O.expand(A)
+        ref = _sub(full, r0, r1, c0, c1)
+        assert np.array_equal(Cb.colptr, ref.colptr) and np.array_equal(Cb.rows, ref.rows)
+        np.testing.assert_allclose(Cb.vals, ref.vals, rtol=1e-12)
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover
+        errq.put(f"rank {rank}: {e!r}")
+        raise
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("pr,pc", [(1, 2), (2, 1), (2, 2)])
+def test_summa_schedule_gloo(pr, pc):
+    ctx = mp.get_context("spawn")
+    errq = ctx.Queue()
+    world = pr * pc
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, pr, pc, port, errq)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+    codes = [p.exitcode for p in procs]
+    msgs = []
+    while not errq.empty():
+        msgs.append(errq.get())
+    assert codes == [0] * world, (codes, msgs)
+
+
+def test_grid_arithmetic_matches_paper_square_case():
+    # square grid, s = sqrt(P): stage k uses A_ik from p_ik and B_kj from p_kj
+    for rank in range(4):
+        g = Grid(2, 2, rank)
+        assert g.s == 2
+        for q in range(2):
+            assert g.a_owner_col(q) == q and g.b_owner_row(q) == q
+    g = Grid(2, 4, 5)
+    assert g.s == 4 and (g.i, g.j) == (1, 1)
+    assert [g.a_owner_col(q) for q in range(4)] == [0, 1, 2, 3]
+    assert [g.b_owner_row(q) for q in range(4)] == [0, 0, 1, 1]
+    assert binary_merge_schedule(4) == [(1, 0), (2, 1), (3, 0), (4, 2)]
