@@ -43,6 +43,7 @@ CONFIG_PARAMS = {
     "C4": dict(prune_threshold=1e-4, select_k=1100, recover_k=1400, recover_pct=0.9),
     "C5": dict(prune_threshold=1e-4, select_k=1100, recover_k=1400, recover_pct=0.9),
 }
+GRIDS = {1: (1, 1), 2: (1, 2), 4: (2, 2), 8: (2, 4)}   # north star: 1x1, 1x2, 2x2, 2x4
 METRIC = "expansion SpGEMM GFLOP/s + HBM GB/s (% roofline), MCL iter time at 1/2/4/8 B200"
 UNIT = "GFLOP/s"
 
@@ -249,14 +250,28 @@ def run_gpu(args):
     A = ctx.preprocess(Gd)
     del Gd
     n = A.ncols
+    nnz0 = A.nnz
     params = M.Params(**CONFIG_PARAMS[args.config])
     b = (n * rank) // world
     e = (n * (rank + 1)) // world
+    mode = "fused" if world == 1 else args.mode
+    if mode == "summa":
+        from paper_2002_10083_b200.grid import Grid
+        pr, pc = GRIDS.get(world, (1, world))
+        uid = [M.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ctx.set_grid(pr, pc, rank, uid[0])
+        gr = Grid(pr, pc, rank)
+        blk0 = ctx.block(A, gr.rows(n), gr.cols(n))
+        del A
+        A = blk0
 
     def step():
-        if world == 1:
+        if mode == "fused":
             out, st = ctx.iterate(A, params)
             return out, st
+        if mode == "summa":
+            return ctx.summa_iterate(A, params)
         blk, st = ctx.iterate(A, params, cols=(b, e))
         full = allgather_csc(dist, M, blk, n, A.nrows, dev)
         return full, st
@@ -292,6 +307,8 @@ def run_gpu(args):
     flops_total = flops_rank
     if world > 1:
         t = torch.tensor([total_ms, float(flops_rank)], dtype=torch.float64, device=dev)
+        if mode == "summa":
+            t[1] = float(flops_rank)
         tl = [torch.zeros_like(t) for _ in range(world)]
         dist.all_gather(tl, t)
         total_ms = max(float(x[0]) for x in tl)
@@ -370,11 +387,14 @@ def run_gpu(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
-            "config": {"workload": workload_name(args.config, n, A.nnz), "config": args.config,
+            "config": {"workload": workload_name(args.config, n, nnz0), "config": args.config,
                        "global_batch": n, "flops_per_step": flops_total,
                        "nnz_out": int(s0["nnz_out"]) if world == 1 else None,
-                       "parallelism": "1 GPU" if world == 1 else
-                       f"column partition x{world} (A replicated) + NCCL all-gather of A_next",
+                       "parallelism": "1 GPU" if world == 1 else (
+                           f"2D Sparse-SUMMA {GRIDS.get(world, (1, world))[0]}x"
+                           f"{GRIDS.get(world, (1, world))[1]} (NCCL panel broadcasts, Alg. 2 merge)"
+                           if mode == "summa" else
+                           f"column partition x{world} (A replicated) + NCCL all-gather of A_next"),
                        "l2": "inputs larger than L2 (A0 > 126 MB), no flush",
                        "estimator_used": int(s0["estimator_used"]),
                        "stage_ms": {"flops": s0["ms"][0], "estimate": s0["ms"][1],
@@ -403,6 +423,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C3", choices=list(CONFIG_PARAMS))
     ap.add_argument("--scale", type=float, default=1.0)
+    ap.add_argument("--mode", default="colpart", choices=["colpart", "summa"],
+                    help="N>1: column partition + all-gather, or the 2D Sparse-SUMMA")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-flops", type=float, default=5e8)
     ap.add_argument("--ref-flops", type=float, default=2e8)

@@ -391,7 +391,7 @@ int spgemm_impl(mcl_ctx *c, const mcl_csc_t *A, const mcl_csc_t *B, int64_t cb, 
     CK(cudaEventRecord(c->ev[1], c->stream));
     RC(cohen(c, pr, p.est_keys, p.seed, est, nullptr));
     CK(cudaEventRecord(c->ev[2], c->stream));
-    RC(symbolic_sizes(c, pr, f, est, p.force_bin, nnzc, st));
+    RC(symbolic_sizes(c, pr, f, est, p.force_bin, nnzc, nullptr));
     CK(cudaEventRecord(c->ev[3], c->stream));
     C->col_ptr = nullptr;
     mcl_csc_t out;
@@ -415,7 +415,7 @@ int spgemm_impl(mcl_ctx *c, const mcl_csc_t *A, const mcl_csc_t *B, int64_t cb, 
         base.c_cp = out.col_ptr;
         base.c_row = out.row_idx;
         base.c_val = out.val;
-        if ((rc = run_bins(c, kNum, pr, f, nullptr, nnzc, p.force_bin, base, nullptr)) != MCL_OK) break;
+        if ((rc = run_bins(c, kNum, pr, f, nullptr, nnzc, p.force_bin, base, st)) != MCL_OK) break;
         CK(cudaEventRecord(c->ev[4], c->stream));
         e = launch_reduce_i64(f, n, tot, c->stream);
         if (e != cudaSuccess) { rc = fail(c, MCL_ERR_CUDA, "reduce: %s", cudaGetErrorString(e)); break; }
@@ -552,6 +552,7 @@ int merge_impl(mcl_ctx_t c, int32_t L, const mcl_csc_t *lists, mcl_csc_t *out) {
 // stripe (the boundaries coincide exactly, q*n/s = c*n/pc for q = c*s/pc).
 int64_t cut(int64_t n, int parts, int k) { return (int64_t)((__int128)k * n / parts); }
 int gcd_i(int a, int b) { return b ? gcd_i(b, a % b) : a; }
+int s_of(int pr, int pc) { return pr / gcd_i(pr, pc) * pc; }
 
 // Distributed prune / select / recover / inflate of a block column set whose columns are
 // split over the ranks of `comm` (the column communicator; nullptr = whole columns).
@@ -580,7 +581,13 @@ int dist_prune(mcl_ctx *c, const mcl_csc_t *C, ncclComm_t comm, const PruneParam
     rowcut = rem + 2 * n1;
     RC(scratch_t(c, "dp_pre", 2 * n1, &vpre));
     rpre = vpre + n1;
-    RC(scratch_t(c, "dp_hist", 256 * n1, &hist));
+    int64_t *selflag, *selpos;
+    int32_t *sel;
+    unsigned long long *undone;
+    RC(scratch_t(c, "dp_selflag", 2 * n1 + 1, &selflag));
+    selpos = selflag + n1;
+    RC(scratch_t(c, "dp_sel", n1, &sel));
+    RC(scratch_t(c, "dp_undone", 2, &undone));
     RC(scratch_t(c, "kcap", n1, &kcap));
     RC(scratch_t(c, "soff", n1 + 1, &soff));
     RC(scratch_t(c, "scnt", n1, &scnt));
@@ -596,11 +603,30 @@ int dist_prune(mcl_ctx *c, const mcl_csc_t *C, ncclComm_t comm, const PruneParam
     CK(launch_dp_branch(n, nnz, m, sm, pp, K, mode, rem, vpre, rowcut, c->stream));
     CK(cudaMemsetAsync(done, 0, sizeof(int32_t) * n1, c->stream));
     CK(cudaMemsetAsync(rpre, 0, sizeof(uint32_t) * n1, c->stream));
-    for (int pass = 0; pass < 8; pass++) {
-        CK(launch_dp_hist(n, C->col_ptr, C->row_idx, C->val, C->row0, mode, vpre, rpre, done, pass,
-                          hist, grid, c->stream));
-        if (comm) NC(ncclAllReduce(hist, hist, 256 * n1, ncclUint32, ncclSum, comm, c->stream));
-        CK(launch_dp_digit(n, mode, hist, pass, vpre, rpre, rem, done, rowcut, c->stream));
+    // exact global top-K cut of the select columns (same list, same order on every rank)
+    CK(launch_dp_sellist(n, mode, selflag, selpos, sel, tmp, c->stream));
+    int64_t nsel = 0;
+    {
+        int64_t last[2];
+        RC(readback(c, selpos + n - 1, sizeof(int64_t), &last[0]));
+        RC(readback(c, selflag + n - 1, sizeof(int64_t), &last[1]));
+        nsel = n > 0 ? last[0] + last[1] : 0;
+    }
+    if (nsel > 0) {
+        RC(scratch_t(c, "dp_hist", 256 * (size_t)nsel, &hist));
+        const int hgrid = (int)std::min<int64_t>(nsel, (int64_t)c->sms * 8);
+        for (int pass = 0; pass < 8; pass++) {
+            if (pass == 4) {  // ties at the cut need the row passes only if some column is open
+                unsigned long long open = 0;
+                CK(launch_dp_undone(nsel, sel, done, undone, c->stream));
+                RC(readback(c, undone, sizeof open, &open));
+                if (open == 0) break;
+            }
+            CK(launch_dp_hist(nsel, sel, C->col_ptr, C->row_idx, C->val, C->row0, mode, vpre, rpre,
+                              done, pass, hist, hgrid, c->stream));
+            if (comm) NC(ncclAllReduce(hist, hist, 256 * nsel, ncclUint32, ncclSum, comm, c->stream));
+            CK(launch_dp_digit(nsel, sel, hist, pass, vpre, rpre, rem, done, rowcut, c->stream));
+        }
     }
     CK(launch_dp_keepstats(n, C->col_ptr, C->row_idx, C->val, C->row0, mode, vpre, rowcut, pp, kcnt,
                            sums, grid, c->stream));
@@ -1138,6 +1164,70 @@ int mcl_summa_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, 
         A->col0 != cut(n, pc, gj) || A->ncols != cut(n, pc, gj + 1) - cut(n, pc, gj))
         return fail(c, MCL_ERR_DIM, "block (%d,%d) does not match the %dx%d grid of n=%lld", gi, gj,
                     pr, pc, (long long)n);
+    if (pr == 1 && !getenv("MCLX_SUMMA_STAGED")) {
+        // 1 x pc grid: every column of C = A*A lives on one rank.  The stage broadcasts of
+        // the A-panels (the pc column stripes) are issued together, and instead of
+        // materialising one partial product per stage and merging them (Alg. 2), all stages
+        // accumulate in the fused kernel's hash table; the prune is then local.
+        const int P = pc;
+        int64_t *szd;
+        RC(scratch_t(c, "summa_sz", (size_t)P, &szd));
+        const int64_t my = A->nnz;
+        CK(cudaMemcpyAsync(szd + c->rank, &my, sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
+        NC(ncclAllGather(szd + c->rank, szd, 1, ncclInt64, c->world, c->stream));
+        std::vector<int64_t> sz(P), off(P + 1, 0);
+        CK(cudaMemcpyAsync(sz.data(), szd, sizeof(int64_t) * P, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        for (int r = 0; r < P; r++) off[r + 1] = off[r] + sz[r];
+        const int64_t tot = off[P];
+        int64_t *fcp, *cps;
+        int32_t *frow;
+        float *fval;
+        RC(scratch_t(c, "summa_fcp", (size_t)n + 1, &fcp));
+        RC(scratch_t(c, "summa_cps", (size_t)n + P, &cps));
+        RC(scratch_t(c, "summa_frow", (size_t)std::max<int64_t>(tot, 1), &frow));
+        RC(scratch_t(c, "summa_fval", (size_t)std::max<int64_t>(tot, 1), &fval));
+        NC(ncclGroupStart());
+        for (int r = 0; r < P; r++) {
+            const int64_t c0 = cut(n, P, r), nc = cut(n, P, r + 1) - c0;
+            const bool me = r == c->rank;
+            NC(ncclBroadcast(me ? (const void *)A->col_ptr : (const void *)(cps + c0 + r), cps + c0 + r,
+                             nc + 1, ncclInt64, r, c->world, c->stream));
+            if (sz[r]) {
+                NC(ncclBroadcast(me ? (const void *)A->row_idx : (const void *)(frow + off[r]),
+                                 frow + off[r], sz[r], ncclInt32, r, c->world, c->stream));
+                NC(ncclBroadcast(me ? (const void *)A->val : (const void *)(fval + off[r]),
+                                 fval + off[r], sz[r], ncclFloat32, r, c->world, c->stream));
+            }
+        }
+        NC(ncclGroupEnd());
+        for (int r = 0; r < P; r++) {
+            const int64_t c0 = cut(n, P, r), nc = cut(n, P, r + 1) - c0;
+            CK(launch_offset_colptr(nc + 1, cps + c0 + r, off[r], fcp + c0, c->stream));
+        }
+        mcl_csc_t Af;
+        zero_csc(&Af);
+        Af.nrows = n;
+        Af.ncols = n;
+        Af.nnz = tot;
+        Af.n_global = n;
+        Af.col_ptr = fcp;
+        Af.row_idx = frow;
+        Af.val = fval;
+        RC(mcl_iterate_range(c, &Af, A->col0, A->col0 + A->ncols, pin, A_next, st));
+        float chaos = st ? st->chaos : 0.f;
+        float *cm;
+        RC(scratch_t(c, "chaos_max", 4, &cm));
+        CK(cudaMemcpyAsync(cm, &chaos, sizeof(float), cudaMemcpyHostToDevice, c->stream));
+        NC(ncclAllReduce(cm, cm, 1, ncclFloat32, ncclMax, c->world, c->stream));
+        RC(readback(c, cm, sizeof(float), &chaos));
+        if (st) {
+            st->chaos = chaos;
+            st->comm_bytes = (tot - my) * 8 + (n - A->ncols) * 8;
+            st->phases = 1;
+        }
+        return MCL_OK;
+    }
     const int s = pr / gcd_i(pr, pc) * pc;  // lcm
     const int64_t nj = A->ncols, mi = A->nrows;
     const PruneParams pp = prune_params(pin);
@@ -1178,7 +1268,10 @@ int mcl_summa_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, 
 
     // ---- stages: broadcast panels, local product, Alg. 2 binary merge
     std::vector<mcl_csc_t> stack;
-    int64_t comm_bytes = 0, peak_partial = 0, live_partial = 0;
+    int64_t comm_bytes = 0, peak_partial = 0, live_partial = 0, flops = 0;
+    float bin_ms[kNumBins + 1] = {};
+    int64_t bin_flops[kNumBins + 1] = {}, bin_cols[kNumBins + 1] = {}, bin_nnzb[kNumBins + 1] = {},
+            bin_out[kNumBins + 1] = {};
     int rc = MCL_OK;
     for (int q = 0; q < s && rc == MCL_OK; q++) {
         const int64_t k0 = cut(n, s, q), k1 = cut(n, s, q + 1), kq = k1 - k0;
@@ -1250,7 +1343,16 @@ int mcl_summa_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, 
         Pb.col_ptr = pbcp;
         Pb.row_idx = pbrow;
         Pb.val = pbval;
-        if ((rc = spgemm_impl(c, &Pa, &Pb, 0, nj, pin, &Pq, nullptr)) != MCL_OK) break;
+        mcl_stats_t sst;
+        if ((rc = spgemm_impl(c, &Pa, &Pb, 0, nj, pin, &Pq, &sst)) != MCL_OK) break;
+        flops += sst.flops;
+        for (int b = 0; b <= kNumBins; b++) {
+            bin_ms[b] += sst.bin_ms[b];
+            bin_flops[b] += sst.bin_flops[b];
+            bin_cols[b] += sst.bin_cols[b];
+            bin_nnzb[b] += sst.bin_nnzb[b];
+            bin_out[b] += sst.bin_out[b];
+        }
         Pq.row0 = A->row0;
         Pq.col0 = A->col0;
         Pq.n_global = n;
@@ -1314,6 +1416,14 @@ int mcl_summa_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, 
         st->ms[6] = elapsed(c, 0, 2);
         st->comm_bytes = comm_bytes;
         st->peak_partial = peak_partial;
+        st->flops = flops;
+        for (int b = 0; b <= kNumBins; b++) {
+            st->bin_ms[b] = bin_ms[b];
+            st->bin_flops[b] = bin_flops[b];
+            st->bin_cols[b] = bin_cols[b];
+            st->bin_nnzb[b] = bin_nnzb[b];
+            st->bin_out[b] = bin_out[b];
+        }
         st->peak_bytes = (int64_t)c->peak;
         st->launches = g_launches - launches0;
     }

@@ -11,6 +11,8 @@
 //                      histograms are all-reduced (4 passes on the fp32 bits of the value,
 //                      then 4 on the global row id for ties); the kept set's sums are
 //                      all-reduced for renormalisation, chaos and inflation.
+#include <algorithm>
+
 #include "kernels.h"
 
 namespace mclx {
@@ -164,7 +166,8 @@ cudaError_t launch_dp_branch(int64_t ncols, const int64_t *nnz, const int64_t *m
 // (hist[j][256], zero for other columns).  Passes 0-3: value bits, digit (bits >> (24-8p))
 // among entries whose higher bits match prefix.  Passes 4-7: global row id bits among
 // entries whose value bits equal the cut t = vprefix.
-__global__ void __launch_bounds__(kDP) k_dp_hist(int64_t ncols, const int64_t *__restrict__ cp,
+__global__ void __launch_bounds__(kDP) k_dp_hist(int64_t nsel, const int32_t *__restrict__ sel,
+                                                 const int64_t *__restrict__ cp,
                                                  const int32_t *__restrict__ rows,
                                                  const float *__restrict__ vals, int64_t row0,
                                                  const int8_t *__restrict__ mode,
@@ -173,9 +176,10 @@ __global__ void __launch_bounds__(kDP) k_dp_hist(int64_t ncols, const int64_t *_
                                                  const int32_t *__restrict__ done, int pass,
                                                  unsigned *__restrict__ hist) {
     __shared__ unsigned h[256];
-    for (int64_t j = blockIdx.x; j < ncols; j += gridDim.x) {
-        if (mode[j] != 1 || done[j]) {
-            for (int i = threadIdx.x; i < 256; i += kDP) hist[j * 256 + i] = 0;
+    for (int64_t li = blockIdx.x; li < nsel; li += gridDim.x) {
+        const int64_t j = sel[li];
+        if (done[j]) {
+            for (int i = threadIdx.x; i < 256; i += kDP) hist[li * 256 + i] = 0;
             continue;
         }
         for (int i = threadIdx.x; i < 256; i += kDP) h[i] = 0;
@@ -201,23 +205,24 @@ __global__ void __launch_bounds__(kDP) k_dp_hist(int64_t ncols, const int64_t *_
             }
         }
         __syncthreads();
-        for (int i = threadIdx.x; i < 256; i += kDP) hist[j * 256 + i] = h[i];
+        for (int i = threadIdx.x; i < 256; i += kDP) hist[li * 256 + i] = h[i];
         __syncthreads();
     }
 }
-cudaError_t launch_dp_hist(int64_t ncols, const int64_t *cp, const int32_t *rows, const float *vals,
+cudaError_t launch_dp_hist(int64_t nsel, const int32_t *sel, const int64_t *cp, const int32_t *rows,
+                           const float *vals,
                            int64_t row0, const int8_t *mode, const uint32_t *vprefix,
                            const uint32_t *rprefix, const int32_t *done, int pass, unsigned *hist,
                            int grid, cudaStream_t s) {
-    if (ncols <= 0) return cudaSuccess;
+    if (nsel <= 0) return cudaSuccess;
     ++g_launches;
-    k_dp_hist<<<grid, kDP, 0, s>>>(ncols, cp, rows, vals, row0, mode, vprefix, rprefix, done, pass,
+    k_dp_hist<<<grid, kDP, 0, s>>>(nsel, sel, cp, rows, vals, row0, mode, vprefix, rprefix, done, pass,
                                    hist);
     return cudaGetLastError();
 }
 
 // Digit step of pass p from the GLOBAL histogram: one warp per select column.
-__global__ void k_dp_digit(int64_t ncols, const int8_t *__restrict__ mode,
+__global__ void k_dp_digit(int64_t nsel, const int32_t *__restrict__ sel,
                            const unsigned *__restrict__ hist, int pass, uint32_t *__restrict__ vprefix,
                            uint32_t *__restrict__ rprefix, int32_t *__restrict__ rem,
                            int32_t *__restrict__ done, int32_t *__restrict__ rowcut) {
@@ -225,11 +230,12 @@ __global__ void k_dp_digit(int64_t ncols, const int8_t *__restrict__ mode,
     const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lw = threadIdx.x >> 5;
     const int lane = lane_id();
-    for (int64_t j = w; j < ncols; j += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-        if (mode[j] != 1 || done[j]) continue;
+    for (int64_t li = w; li < nsel; li += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t j = sel[li];
+        if (done[j]) continue;
         const int r = rem[j];
-        if (pass < 4) find_digit<true>(hist + j * 256, r, sout[lw]);
-        else find_digit<false>(hist + j * 256, r, sout[lw]);
+        if (pass < 4) find_digit<true>(hist + li * 256, r, sout[lw]);
+        else find_digit<false>(hist + li * 256, r, sout[lw]);
         __syncwarp();
         if (lane == 0) {
             const int d = sout[lw][0], before = sout[lw][1], eq = sout[lw][2];
@@ -255,14 +261,58 @@ __global__ void k_dp_digit(int64_t ncols, const int8_t *__restrict__ mode,
         __syncwarp();
     }
 }
-cudaError_t launch_dp_digit(int64_t ncols, const int8_t *mode, const unsigned *hist, int pass,
+cudaError_t launch_dp_digit(int64_t nsel, const int32_t *sel, const unsigned *hist, int pass,
                             uint32_t *vprefix, uint32_t *rprefix, int32_t *rem, int32_t *done,
                             int32_t *rowcut, cudaStream_t s) {
-    if (ncols <= 0) return cudaSuccess;
-    int64_t b = (ncols * 32 + 255) / 256;
+    if (nsel <= 0) return cudaSuccess;
+    int64_t b = (nsel * 32 + 255) / 256;
     if (b > 148 * 32) b = 148 * 32;
     ++g_launches;
-    k_dp_digit<<<(int)b, 256, 0, s>>>(ncols, mode, hist, pass, vprefix, rprefix, rem, done, rowcut);
+    k_dp_digit<<<(int)b, 256, 0, s>>>(nsel, sel, hist, pass, vprefix, rprefix, rem, done, rowcut);
+    return cudaGetLastError();
+}
+
+// flags for the select-column list: flag[j] = (mode[j] == 1)
+__global__ void k_dp_selflag(int64_t ncols, const int8_t *__restrict__ mode, int64_t *__restrict__ flag) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < ncols;
+         j += (int64_t)gridDim.x * blockDim.x)
+        flag[j] = mode[j] == 1 ? 1 : 0;
+}
+__global__ void k_dp_selscatter(int64_t ncols, const int8_t *__restrict__ mode,
+                                const int64_t *__restrict__ pos, int32_t *__restrict__ sel) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < ncols;
+         j += (int64_t)gridDim.x * blockDim.x)
+        if (mode[j] == 1) sel[pos[j]] = (int32_t)j;
+}
+cudaError_t launch_dp_sellist(int64_t ncols, const int8_t *mode, int64_t *flag, int64_t *pos,
+                              int32_t *sel, void *tmp, cudaStream_t s) {
+    if (ncols <= 0) return cudaSuccess;
+    int64_t b = (ncols + 255) / 256;
+    if (b > 148 * 16) b = 148 * 16;
+    ++g_launches;
+    k_dp_selflag<<<(int)b, 256, 0, s>>>(ncols, mode, flag);
+    cudaError_t e = launch_scan_i64(flag, pos, ncols, tmp, s);
+    if (e != cudaSuccess) return e;
+    ++g_launches;
+    k_dp_selscatter<<<(int)b, 256, 0, s>>>(ncols, mode, pos, sel);
+    return cudaGetLastError();
+}
+__global__ void k_dp_undone(int64_t nsel, const int32_t *__restrict__ sel,
+                            const int32_t *__restrict__ done, unsigned long long *cnt) {
+    unsigned long long c = 0;
+    for (int64_t li = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; li < nsel;
+         li += (int64_t)gridDim.x * blockDim.x)
+        c += done[sel[li]] ? 0 : 1;
+    c = warp_sum(c);
+    if (lane_id() == 0 && c) atomicAdd(cnt, c);
+}
+cudaError_t launch_dp_undone(int64_t nsel, const int32_t *sel, const int32_t *done,
+                             unsigned long long *cnt, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), s);
+    if (e != cudaSuccess || nsel <= 0) return e;
+    ++g_launches;
+    k_dp_undone<<<(int)std::min<int64_t>((nsel + 255) / 256, 148 * 4), 256, 0, s>>>(nsel, sel, done,
+                                                                                  cnt);
     return cudaGetLastError();
 }
 
