@@ -43,7 +43,6 @@ CONFIG_PARAMS = {
     "C4": dict(prune_threshold=1e-4, select_k=1100, recover_k=1400, recover_pct=0.9),
     "C5": dict(prune_threshold=1e-4, select_k=1100, recover_k=1400, recover_pct=0.9),
 }
-GRIDS = {1: (1, 1), 2: (1, 2), 4: (2, 2), 8: (2, 4)}   # north star: 1x1, 1x2, 2x2, 2x4
 METRIC = "expansion SpGEMM GFLOP/s + HBM GB/s (% roofline), MCL iter time at 1/2/4/8 B200"
 UNIT = "GFLOP/s"
 
@@ -255,9 +254,10 @@ def run_gpu(args):
     b = (n * rank) // world
     e = (n * (rank + 1)) // world
     mode = "fused" if world == 1 else args.mode
+    pr, pc = 1, world
     if mode == "summa":
         from paper_2002_10083_b200.grid import Grid
-        pr, pc = GRIDS.get(world, (1, world))
+        pr, pc = (int(x) for x in args.grid.split("x")) if args.grid else (1, world)
         uid = [M.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         ctx.set_grid(pr, pc, rank, uid[0])
@@ -391,8 +391,9 @@ def run_gpu(args):
                        "global_batch": n, "flops_per_step": flops_total,
                        "nnz_out": int(s0["nnz_out"]) if world == 1 else None,
                        "parallelism": "1 GPU" if world == 1 else (
-                           f"2D Sparse-SUMMA {GRIDS.get(world, (1, world))[0]}x"
-                           f"{GRIDS.get(world, (1, world))[1]} (NCCL panel broadcasts, Alg. 2 merge)"
+                           (f"2D Sparse-SUMMA {pr}x{pc}: NCCL panel broadcasts, "
+                            + ("stages accumulated in the fused kernel, local prune" if pr == 1 else
+                               "stage products + Alg. 2 device merge, distributed prune"))
                            if mode == "summa" else
                            f"column partition x{world} (A replicated) + NCCL all-gather of A_next"),
                        "l2": "inputs larger than L2 (A0 > 126 MB), no flush",
@@ -423,8 +424,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C3", choices=list(CONFIG_PARAMS))
     ap.add_argument("--scale", type=float, default=1.0)
-    ap.add_argument("--mode", default="colpart", choices=["colpart", "summa"],
-                    help="N>1: column partition + all-gather, or the 2D Sparse-SUMMA")
+    ap.add_argument("--mode", default="summa", choices=["colpart", "summa"],
+                    help="N>1: the 2D Sparse-SUMMA (default) or column partition + all-gather")
+    ap.add_argument("--grid", default=None, help="pr x pc for --mode summa, e.g. 2x2 (default "
+                    "1xN: whole columns per rank, stages accumulated in the fused kernel)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-flops", type=float, default=5e8)
     ap.add_argument("--ref-flops", type=float, default=2e8)
