@@ -401,6 +401,7 @@ def run_gpu(args):
                        "stage_ms": {"flops": s0["ms"][0], "estimate": s0["ms"][1],
                                     "symbolic": s0["ms"][2], "fused_numeric": s0["ms"][3],
                                     "assemble": s0["ms"][5]},
+                       "ms_raw": s0["ms"],
                        "bin_cols": s0["bin_cols"], "bin_ms": bin_ms,
                        "bin_flops": s0["bin_flops"], "retries": int(s0["retries"]),
                        "step_ms_min": min(step_ms), "step_ms_max": max(step_ms)},

@@ -37,6 +37,8 @@ struct mcl_ctx {
     void *pin = nullptr;  // pinned host staging for small read-backs
     cudaEvent_t ev[8] = {};
     cudaEvent_t bev[2 * (kNumBins + 1)] = {};
+    cudaEvent_t pev[6] = {};  // phases of the distributed prune
+    cudaEvent_t sev[3] = {};  // SUMMA iteration (ev[] is reused by the stage products)
     // 2D Sparse-SUMMA grid (mcl_ctx_set_grid): world / row / column communicators
     int pr = 1, pc = 1, rank = 0;
     ncclComm_t world = nullptr, rowc = nullptr, colc = nullptr;
@@ -593,6 +595,7 @@ int dist_prune(mcl_ctx *c, const mcl_csc_t *C, ncclComm_t comm, const PruneParam
     RC(scratch_t(c, "scnt", n1, &scnt));
     RC(scratch_t(c, "chaos_max", 4, &cmax));
     RC(scratch(c, "scan_tmp", scan_tmp_bytes(n + 1), &tmp));
+    CK(cudaEventRecord(c->pev[0], c->stream));
     CK(launch_dp_stats(n, C->col_ptr, C->val, pp.theta, nnz, m, sm, grid, c->stream));
     if (comm) {
         NC(ncclGroupStart());
@@ -600,6 +603,7 @@ int dist_prune(mcl_ctx *c, const mcl_csc_t *C, ncclComm_t comm, const PruneParam
         NC(ncclAllReduce(sm, sm, n1, ncclFloat64, ncclSum, comm, c->stream));
         NC(ncclGroupEnd());
     }
+    CK(cudaEventRecord(c->pev[1], c->stream));
     CK(launch_dp_branch(n, nnz, m, sm, pp, K, mode, rem, vpre, rowcut, c->stream));
     CK(cudaMemsetAsync(done, 0, sizeof(int32_t) * n1, c->stream));
     CK(cudaMemsetAsync(rpre, 0, sizeof(uint32_t) * n1, c->stream));
@@ -628,6 +632,7 @@ int dist_prune(mcl_ctx *c, const mcl_csc_t *C, ncclComm_t comm, const PruneParam
             CK(launch_dp_digit(nsel, sel, hist, pass, vpre, rpre, rem, done, rowcut, c->stream));
         }
     }
+    CK(cudaEventRecord(c->pev[2], c->stream));
     CK(launch_dp_keepstats(n, C->col_ptr, C->row_idx, C->val, C->row0, mode, vpre, rowcut, pp, kcnt,
                            sums, grid, c->stream));
     // staging capacity per local column: the local nnz (kept <= local nnz)
@@ -642,6 +647,7 @@ int dist_prune(mcl_ctx *c, const mcl_csc_t *C, ncclComm_t comm, const PruneParam
         NC(ncclGroupEnd());
     }
     CK(launch_scan_i64(kcap, soff, n, tmp, c->stream));
+    CK(cudaEventRecord(c->pev[3], c->stream));
     int64_t stot = 0;
     RC(readback(c, soff + n, sizeof(int64_t), &stot));
     RC(scratch_t(c, "s_row", (size_t)std::max<int64_t>(stot, 1), &srow));
@@ -654,6 +660,7 @@ int dist_prune(mcl_ctx *c, const mcl_csc_t *C, ncclComm_t comm, const PruneParam
     out->row0 = C->row0;
     out->col0 = C->col0;
     out->n_global = C->n_global;
+    CK(cudaEventRecord(c->pev[4], c->stream));
     float h = 0.f;
     RC(readback(c, cmax, sizeof(float), &h));
     *chaos_out = h;
@@ -718,6 +725,8 @@ int mcl_ctx_create(mcl_ctx_t *out, int device, void *stream, mcl_alloc_fn alloc,
     }
     for (int i = 0; i < 8; i++) cudaEventCreate(&c->ev[i]);
     for (int i = 0; i < 2 * (kNumBins + 1); i++) cudaEventCreate(&c->bev[i]);
+    for (int i = 0; i < 6; i++) cudaEventCreate(&c->pev[i]);
+    for (int i = 0; i < 3; i++) cudaEventCreate(&c->sev[i]);
     for (int m = 0; m < 3; m++)
         for (int b = 0; b <= kNumBins; b++) c->occ[m][b] = bin_occupancy(m, b);
     if (cudaGetLastError() != cudaSuccess) {
@@ -748,6 +757,10 @@ int mcl_ctx_destroy(mcl_ctx_t c) {
         if (c->ev[i]) cudaEventDestroy(c->ev[i]);
     for (int i = 0; i < 2 * (kNumBins + 1); i++)
         if (c->bev[i]) cudaEventDestroy(c->bev[i]);
+    for (int i = 0; i < 6; i++)
+        if (c->pev[i]) cudaEventDestroy(c->pev[i]);
+    for (int i = 0; i < 3; i++)
+        if (c->sev[i]) cudaEventDestroy(c->sev[i]);
     if (c->pin) cudaFreeHost(c->pin);
     delete c;
     return MCL_OK;
@@ -1231,7 +1244,7 @@ int mcl_summa_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, 
     const int s = pr / gcd_i(pr, pc) * pc;  // lcm
     const int64_t nj = A->ncols, mi = A->nrows;
     const PruneParams pp = prune_params(pin);
-    CK(cudaEventRecord(c->ev[0], c->stream));
+    CK(cudaEventRecord(c->sev[0], c->stream));
 
     // ---- sizes of the panels this rank owns, all-gathered once (P:239-243 stage k)
     int64_t *hdr, *first, *cnt;
@@ -1391,7 +1404,7 @@ int mcl_summa_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, 
         for (auto &x : stack) free_csc(c, &x);
         return rc;
     }
-    CK(cudaEventRecord(c->ev[1], c->stream));
+    CK(cudaEventRecord(c->sev[1], c->stream));
     mcl_csc_t Cb = stack[0];
     float chaos = 0.f;
     rc = dist_prune(c, &Cb, pr > 1 ? c->colc : nullptr, pp, A_next, &chaos);
@@ -1403,7 +1416,7 @@ int mcl_summa_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, 
     CK(cudaMemcpyAsync(cm, &chaos, sizeof(float), cudaMemcpyHostToDevice, c->stream));
     NC(ncclAllReduce(cm, cm, 1, ncclFloat32, ncclMax, c->world, c->stream));
     RC(readback(c, cm, sizeof(float), &chaos));
-    CK(cudaEventRecord(c->ev[2], c->stream));
+    CK(cudaEventRecord(c->sev[2], c->stream));
     if (st) {
         st->nnz_in = A->nnz;
         st->nnz_unpruned = nnz_unpruned;
@@ -1411,9 +1424,25 @@ int mcl_summa_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, 
         st->chaos = chaos;
         st->phases = 1;
         st->estimator_used = 1;
-        st->ms[3] = elapsed(c, 0, 1);
-        st->ms[4] = elapsed(c, 1, 2);
-        st->ms[6] = elapsed(c, 0, 2);
+        float sm3 = -1.f, sm4 = -1.f;
+        cudaEventElapsedTime(&sm3, c->sev[0], c->sev[1]);
+        cudaEventElapsedTime(&sm4, c->sev[1], c->sev[2]);
+        cudaGetLastError();
+        st->ms[3] = sm3;  // stages: broadcasts + products + Alg. 2 merges
+        st->ms[4] = sm4;  // distributed prune + inflate
+        st->ms[6] = sm3 + sm4;
+        float pm[4];
+        for (int q = 0; q < 4; q++) {
+            pm[q] = 0.f;
+            if (cudaEventElapsedTime(&pm[q], c->pev[q], c->pev[q + 1]) != cudaSuccess) {
+                cudaGetLastError();
+                pm[q] = -1.f;
+            }
+        }
+        st->ms[0] = pm[0];  // prune: local stats + all-reduce
+        st->ms[1] = pm[1];  // prune: top-k cut (radix histograms + all-reduces)
+        st->ms[2] = pm[2];  // prune: kept sums + all-reduce
+        st->ms[5] = pm[3];  // prune: write + assemble
         st->comm_bytes = comm_bytes;
         st->peak_partial = peak_partial;
         st->flops = flops;

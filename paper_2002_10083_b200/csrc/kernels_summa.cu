@@ -90,39 +90,50 @@ cudaError_t launch_rowslice_copy(int64_t ncols, const int64_t *first, const int6
 // ------------------------------------------------------------------ distributed prune
 constexpr int kDP = 256;
 
+// One warp per column in every kernel below: block columns hold a few hundred entries,
+// so warp shuffles / ballots replace block barriers.
+__device__ __forceinline__ int64_t dp_warp0() {
+    return ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+}
+__device__ __forceinline__ int64_t dp_wstride() { return ((int64_t)gridDim.x * blockDim.x) >> 5; }
+static int dp_grid(int64_t ncols) {
+    int64_t b = (ncols * 32 + kDP - 1) / kDP;
+    if (b > 148 * 32) b = 148 * 32;
+    return b < 1 ? 1 : (int)b;
+}
+
 // local threshold statistics per column: nnz, m = #{v >= theta}, s = sum{v >= theta}
 __global__ void __launch_bounds__(kDP) k_dp_stats(int64_t ncols, const int64_t *__restrict__ cp,
                                                   const float *__restrict__ vals, double theta,
                                                   int64_t *__restrict__ nnz, int64_t *__restrict__ m,
                                                   double *__restrict__ sm) {
-    __shared__ double sred[kDP / 32];
-    __shared__ int64_t sred64[kDP / 32];
-    for (int64_t j = blockIdx.x; j < ncols; j += gridDim.x) {
+    const int lane = lane_id();
+    for (int64_t j = dp_warp0(); j < ncols; j += dp_wstride()) {
         const int64_t a = cp[j], b = cp[j + 1];
         int64_t mloc = 0;
         double sloc = 0.0;
-        for (int64_t t = a + threadIdx.x; t < b; t += kDP) {
+        for (int64_t t = a + lane; t < b; t += 32) {
             const double v = (double)vals[t];
             if (v >= theta) {
                 mloc++;
                 sloc += v;
             }
         }
-        mloc = block_sum<kDP, int64_t>(mloc, sred64);
-        sloc = block_sum<kDP, double>(sloc, sred);
-        if (threadIdx.x == 0) {
+        mloc = warp_sum(mloc);
+        sloc = warp_sum(sloc);
+        if (lane == 0) {
             nnz[j] = b - a;
             m[j] = mloc;
             sm[j] = sloc;
         }
-        __syncthreads();
     }
 }
 cudaError_t launch_dp_stats(int64_t ncols, const int64_t *cp, const float *vals, double theta,
                             int64_t *nnz, int64_t *m, double *sm, int grid, cudaStream_t s) {
     if (ncols <= 0) return cudaSuccess;
+    (void)grid;
     ++g_launches;
-    k_dp_stats<<<grid, kDP, 0, s>>>(ncols, cp, vals, theta, nnz, m, sm);
+    k_dp_stats<<<dp_grid(ncols), kDP, 0, s>>>(ncols, cp, vals, theta, nnz, m, sm);
     return cudaGetLastError();
 }
 
@@ -162,10 +173,10 @@ cudaError_t launch_dp_branch(int64_t ncols, const int64_t *nnz, const int64_t *m
     return cudaGetLastError();
 }
 
-// Local 256-bin digit histogram of pass p for every select column j in [0, ncols)
-// (hist[j][256], zero for other columns).  Passes 0-3: value bits, digit (bits >> (24-8p))
-// among entries whose higher bits match prefix.  Passes 4-7: global row id bits among
-// entries whose value bits equal the cut t = vprefix.
+// Local 256-bin digit histogram of pass p for every select column (hist[li][256] for list
+// index li).  Passes 0-3: value bits, digit (bits >> (24-8p)) among entries whose higher
+// bits match the prefix.  Passes 4-7: global row id bits among entries whose value bits
+// equal the cut t = vprefix.  One warp per column with a warp-private smem histogram.
 __global__ void __launch_bounds__(kDP) k_dp_hist(int64_t nsel, const int32_t *__restrict__ sel,
                                                  const int64_t *__restrict__ cp,
                                                  const int32_t *__restrict__ rows,
@@ -175,49 +186,49 @@ __global__ void __launch_bounds__(kDP) k_dp_hist(int64_t nsel, const int32_t *__
                                                  const uint32_t *__restrict__ rprefix,
                                                  const int32_t *__restrict__ done, int pass,
                                                  unsigned *__restrict__ hist) {
-    __shared__ unsigned h[256];
-    for (int64_t li = blockIdx.x; li < nsel; li += gridDim.x) {
+    __shared__ unsigned hs[kDP / 32][256];
+    unsigned *h = hs[threadIdx.x >> 5];
+    const int lane = lane_id();
+    for (int64_t li = dp_warp0(); li < nsel; li += dp_wstride()) {
         const int64_t j = sel[li];
-        if (done[j]) {
-            for (int i = threadIdx.x; i < 256; i += kDP) hist[li * 256 + i] = 0;
-            continue;
-        }
-        for (int i = threadIdx.x; i < 256; i += kDP) h[i] = 0;
-        __syncthreads();
-        const int64_t a = cp[j], b = cp[j + 1];
-        if (pass < 4) {
-            const int shift = 24 - 8 * pass;
-            const uint32_t mask = pass == 0 ? 0u : (0xFFFFFFFFu << (32 - 8 * pass));
-            const uint32_t pre = vprefix[j];
-            for (int64_t t = a + threadIdx.x; t < b; t += kDP) {
-                const uint32_t bits = __float_as_uint(vals[t]);
-                if ((bits & mask) == pre) atomicAdd(&h[(bits >> shift) & 255u], 1u);
-            }
-        } else {
-            const int q = pass - 4;
-            const int shift = 24 - 8 * q;
-            const uint32_t mask = q == 0 ? 0u : (0xFFFFFFFFu << (32 - 8 * q));
-            const uint32_t t0 = vprefix[j], pre = rprefix[j];
-            for (int64_t t = a + threadIdx.x; t < b; t += kDP) {
-                const uint32_t grow = (uint32_t)(row0 + rows[t]);
-                if (__float_as_uint(vals[t]) == t0 && (grow & mask) == pre)
-                    atomicAdd(&h[(grow >> shift) & 255u], 1u);
+        for (int i = lane; i < 256; i += 32) h[i] = 0;
+        __syncwarp();
+        if (!done[j]) {
+            const int64_t a = cp[j], b = cp[j + 1];
+            if (pass < 4) {
+                const int shift = 24 - 8 * pass;
+                const uint32_t mask = pass == 0 ? 0u : (0xFFFFFFFFu << (32 - 8 * pass));
+                const uint32_t pre = vprefix[j];
+                for (int64_t t = a + lane; t < b; t += 32) {
+                    const uint32_t bits = __float_as_uint(vals[t]);
+                    if ((bits & mask) == pre) atomicAdd(&h[(bits >> shift) & 255u], 1u);
+                }
+            } else {
+                const int q = pass - 4;
+                const int shift = 24 - 8 * q;
+                const uint32_t mask = q == 0 ? 0u : (0xFFFFFFFFu << (32 - 8 * q));
+                const uint32_t t0 = vprefix[j], pre = rprefix[j];
+                for (int64_t t = a + lane; t < b; t += 32) {
+                    const uint32_t grow = (uint32_t)(row0 + rows[t]);
+                    if (__float_as_uint(vals[t]) == t0 && (grow & mask) == pre)
+                        atomicAdd(&h[(grow >> shift) & 255u], 1u);
+                }
             }
         }
-        __syncthreads();
-        for (int i = threadIdx.x; i < 256; i += kDP) hist[li * 256 + i] = h[i];
-        __syncthreads();
+        __syncwarp();
+        for (int i = lane; i < 256; i += 32) hist[li * 256 + i] = h[i];
+        __syncwarp();
     }
 }
 cudaError_t launch_dp_hist(int64_t nsel, const int32_t *sel, const int64_t *cp, const int32_t *rows,
-                           const float *vals,
-                           int64_t row0, const int8_t *mode, const uint32_t *vprefix,
-                           const uint32_t *rprefix, const int32_t *done, int pass, unsigned *hist,
-                           int grid, cudaStream_t s) {
+                           const float *vals, int64_t row0, const int8_t *mode,
+                           const uint32_t *vprefix, const uint32_t *rprefix, const int32_t *done,
+                           int pass, unsigned *hist, int grid, cudaStream_t s) {
     if (nsel <= 0) return cudaSuccess;
+    (void)grid;
     ++g_launches;
-    k_dp_hist<<<grid, kDP, 0, s>>>(nsel, sel, cp, rows, vals, row0, mode, vprefix, rprefix, done, pass,
-                                   hist);
+    k_dp_hist<<<dp_grid(nsel), kDP, 0, s>>>(nsel, sel, cp, rows, vals, row0, mode, vprefix, rprefix,
+                                             done, pass, hist);
     return cudaGetLastError();
 }
 
@@ -336,16 +347,15 @@ __global__ void __launch_bounds__(kDP) k_dp_keepstats(int64_t ncols, const int64
                                                       const int32_t *__restrict__ rowcut,
                                                       PruneParams pp, int64_t *__restrict__ kcnt,
                                                       double *__restrict__ sums /*[4][ncols]*/) {
-    __shared__ double sred[kDP / 32];
-    __shared__ int64_t sred64[kDP / 32];
-    for (int64_t j = blockIdx.x; j < ncols; j += gridDim.x) {
+    const int lane = lane_id();
+    for (int64_t j = dp_warp0(); j < ncols; j += dp_wstride()) {
         const int64_t a = cp[j], b = cp[j + 1];
         const int8_t md = mode[j];
         const uint32_t t = vprefix[j];
         const int32_t rc = rowcut[j];
         int64_t c = 0;
         double sv = 0, mx = 0, sq = 0, sr = 0;
-        for (int64_t i = a + threadIdx.x; i < b; i += kDP) {
+        for (int64_t i = a + lane; i < b; i += 32) {
             const float v = vals[i];
             if (dp_keep(md, v, (uint32_t)(row0 + rows[i]), pp.theta, t, rc)) {
                 const double d = (double)v;
@@ -356,19 +366,18 @@ __global__ void __launch_bounds__(kDP) k_dp_keepstats(int64_t ncols, const int64
                 sr += pow_r(d, pp);
             }
         }
-        c = block_sum<kDP, int64_t>(c, sred64);
-        sv = block_sum<kDP, double>(sv, sred);
-        mx = block_max<kDP, double>(mx, sred);
-        sq = block_sum<kDP, double>(sq, sred);
-        sr = block_sum<kDP, double>(sr, sred);
-        if (threadIdx.x == 0) {
+        c = warp_sum(c);
+        sv = warp_sum(sv);
+        mx = warp_max(mx);
+        sq = warp_sum(sq);
+        sr = warp_sum(sr);
+        if (lane == 0) {
             kcnt[j] = c;
             sums[j] = sv;
             sums[ncols + j] = mx;
             sums[2 * ncols + j] = sq;
             sums[3 * ncols + j] = sr;
         }
-        __syncthreads();
     }
 }
 cudaError_t launch_dp_keepstats(int64_t ncols, const int64_t *cp, const int32_t *rows,
@@ -376,14 +385,15 @@ cudaError_t launch_dp_keepstats(int64_t ncols, const int64_t *cp, const int32_t 
                                 const uint32_t *vprefix, const int32_t *rowcut, const PruneParams &pp,
                                 int64_t *kcnt, double *sums, int grid, cudaStream_t s) {
     if (ncols <= 0) return cudaSuccess;
+    (void)grid;
     ++g_launches;
-    k_dp_keepstats<<<grid, kDP, 0, s>>>(ncols, cp, rows, vals, row0, mode, vprefix, rowcut, pp, kcnt,
-                                        sums);
+    k_dp_keepstats<<<dp_grid(ncols), kDP, 0, s>>>(ncols, cp, rows, vals, row0, mode, vprefix, rowcut,
+                                                   pp, kcnt, sums);
     return cudaGetLastError();
 }
 
-// Write the kept entries of every local column (row order preserved) with
-// a' = v^r / sum_global v^r; chaos_j = K (max w - sum w^2) from the global sums
+// Write the kept entries of every local column (row order preserved, ballot compaction)
+// with a' = v^r / sum_global v^r; chaos_j = K (max w - sum w^2) from the global sums
 // (sums = [sv][mx][sq][sr], all-reduced; K = global kept count).
 __global__ void __launch_bounds__(kDP) k_dp_write(int64_t ncols, const int64_t *__restrict__ cp,
                                                   const int32_t *__restrict__ rows,
@@ -397,34 +407,35 @@ __global__ void __launch_bounds__(kDP) k_dp_write(int64_t ncols, const int64_t *
                                                   int32_t *__restrict__ srow, float *__restrict__ sval,
                                                   int64_t *__restrict__ scnt, float *__restrict__ chaos,
                                                   float *chaos_max) {
-    __shared__ int sscan[kDP / 32];
-    for (int64_t j = blockIdx.x; j < ncols; j += gridDim.x) {
-        const int64_t a = cp[j];
-        const int nnz = (int)(cp[j + 1] - a);
+    const int lane = lane_id();
+    const unsigned lt = (1u << lane) - 1u;
+    for (int64_t j = dp_warp0(); j < ncols; j += dp_wstride()) {
+        const int64_t a = cp[j], b = cp[j + 1];
         const int8_t md = mode[j];
         const uint32_t t = vprefix[j];
         const int32_t rc = rowcut[j];
         const double sr = gsums[3 * ncols + j];
         const int64_t dst = soff[j];
-        int kept = 0;
-        for (int c = 0; c < nnz; c += kDP) {
-            const int i = c + threadIdx.x;
-            int f = 0, r = 0;
+        int64_t kept = 0;
+        for (int64_t c0 = a; c0 < b; c0 += 32) {
+            const int64_t i = c0 + lane;
+            bool f = false;
+            int r = 0;
             float v = 0.f;
-            if (i < nnz) {
-                r = rows[a + i];
-                v = vals[a + i];
-                f = dp_keep(md, v, (uint32_t)(row0 + r), pp.theta, t, rc) ? 1 : 0;
+            if (i < b) {
+                r = rows[i];
+                v = vals[i];
+                f = dp_keep(md, v, (uint32_t)(row0 + r), pp.theta, t, rc);
             }
-            int tot;
-            const int pos = block_excl_scan<kDP>(f, sscan, tot);
+            const unsigned bal = __ballot_sync(0xffffffffu, f);
             if (f) {
-                srow[dst + kept + pos] = r;
-                sval[dst + kept + pos] = (float)(pow_r((double)v, pp) / sr);
+                const int64_t pos = dst + kept + __popc(bal & lt);
+                srow[pos] = r;
+                sval[pos] = (float)(pow_r((double)v, pp) / sr);
             }
-            kept += tot;
+            kept += __popc(bal);
         }
-        if (threadIdx.x == 0) {
+        if (lane == 0) {
             scnt[j] = kept;
             const double sv = gsums[j], mx = gsums[ncols + j], sq = gsums[2 * ncols + j];
             const int64_t K = gkcnt[j];
@@ -432,7 +443,6 @@ __global__ void __launch_bounds__(kDP) k_dp_write(int64_t ncols, const int64_t *
             if (chaos) chaos[j] = ch;
             atomic_max_nonneg_float(chaos_max, ch);
         }
-        __syncthreads();
     }
 }
 cudaError_t launch_dp_write(int64_t ncols, const int64_t *cp, const int32_t *rows, const float *vals,
@@ -441,9 +451,10 @@ cudaError_t launch_dp_write(int64_t ncols, const int64_t *cp, const int32_t *row
                             const int64_t *gkcnt, const int64_t *soff, int32_t *srow, float *sval,
                             int64_t *scnt, float *chaos, float *chaos_max, int grid, cudaStream_t s) {
     if (ncols <= 0) return cudaSuccess;
+    (void)grid;
     ++g_launches;
-    k_dp_write<<<grid, kDP, 0, s>>>(ncols, cp, rows, vals, row0, mode, vprefix, rowcut, pp, gsums,
-                                    gkcnt, soff, srow, sval, scnt, chaos, chaos_max);
+    k_dp_write<<<dp_grid(ncols), kDP, 0, s>>>(ncols, cp, rows, vals, row0, mode, vprefix, rowcut, pp,
+                                               gsums, gkcnt, soff, srow, sval, scnt, chaos, chaos_max);
     return cudaGetLastError();
 }
 
