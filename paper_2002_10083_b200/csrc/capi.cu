@@ -227,6 +227,10 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
     RC(scratch_t(c, "retry_list", (size_t)std::max<int64_t>(n, 1), &retry_list));
     RC(scratch_t(c, "retry_in", (size_t)std::max<int64_t>(n, 1), &retry_in));
     CK(cudaMemsetAsync(err, 0, sizeof(int), c->stream));
+    int *rowpart;
+    RC(scratch_t(c, "rowpart", (size_t)std::max<int64_t>(pr.A->ncols, 1) * 33, &rowpart));
+    CK(launch_rowpart(pr.A->ncols, pr.A->col_ptr, pr.A->row_idx, pr.A->nrows, rowpart, c->stream));
+    base.rowpart = rowpart;
 
 
     // Rounds: 0 sizes by the caller's estimate / exact sizes; 1 re-runs overflowed
@@ -554,7 +558,6 @@ int merge_impl(mcl_ctx_t c, int32_t L, const mcl_csc_t *lists, mcl_csc_t *out) {
 // stripe (the boundaries coincide exactly, q*n/s = c*n/pc for q = c*s/pc).
 int64_t cut(int64_t n, int parts, int k) { return (int64_t)((__int128)k * n / parts); }
 int gcd_i(int a, int b) { return b ? gcd_i(b, a % b) : a; }
-int s_of(int pr, int pc) { return pr / gcd_i(pr, pc) * pc; }
 
 // Distributed prune / select / recover / inflate of a block column set whose columns are
 // split over the ranks of `comm` (the column communicator; nullptr = whole columns).

@@ -12,7 +12,7 @@ namespace mclx {
 // its size bound at load factor <= 1/2 (kLoadNum/kLoadDen).
 constexpr int kNumBins = 6;
 constexpr int kBinCap[kNumBins] = {512, 1024, 2048, 4096, 8192, 16384};
-constexpr int kBinThreads[kNumBins] = {64, 64, 128, 256, 512, 1024};
+constexpr int kBinThreads[kNumBins] = {32, 32, 64, 128, 256, 512};
 constexpr int kGlobalThreads = 512;
 __host__ __device__ constexpr int bin_cap(int b) {
     return b == 0 ? 512 : b == 1 ? 1024 : b == 2 ? 2048 : b == 3 ? 4096 : b == 4 ? 8192 : 16384;
@@ -36,6 +36,7 @@ struct BinArgs {
     const float *bval;
     int64_t cb;
     const int64_t *flops;  // [ncols_out]
+    const int *rowpart;    // [A.ncols][33] row-range index of A (see kernels_spgemm.cu)
     // work list of this bin
     const int32_t *list;
     const int *count;
@@ -68,6 +69,10 @@ cudaError_t launch_bin(int mode, int bin, const BinArgs &a, int grid, cudaStream
 // Max resident CTAs per SM for (mode, bin); also sets the dynamic smem attribute.
 int bin_occupancy(int mode, int bin);
 size_t bin_smem_bytes(int mode, int bin);
+
+// rowpart[k][i] = first position in A_*k whose row >= ceil(i*m/32), i = 0..32
+cudaError_t launch_rowpart(int64_t ncols, const int64_t *cp, const int32_t *row, int64_t m,
+                           int *rowpart, cudaStream_t s);
 
 // misc kernels (kernels_misc.cu)
 cudaError_t launch_flops(int64_t ncols, const int64_t *acp, const int64_t *bcp,

@@ -38,6 +38,36 @@ cudaError_t launch_flops(int64_t ncols, const int64_t *acp, const int64_t *bcp,
     return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ row-range index of A
+// rowpart[k][i] = lower_bound(rows of A_*k, ceil(i*m/32)) - col_ptr[k], i = 0..32.  One
+// warp per column; lane i binary-searches boundary i (independent searches).
+__global__ void k_rowpart(int64_t ncols, const int64_t *__restrict__ cp,
+                          const int32_t *__restrict__ row, int64_t m, int *__restrict__ P) {
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = lane_id();
+    for (int64_t k = w; k < ncols; k += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t a = cp[k], b = cp[k + 1];
+        const int64_t bound = ((int64_t)lane * m + 31) / 32;
+        int64_t lo = a, hi = b;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if ((int64_t)__ldg(row + mid) < bound) lo = mid + 1;
+            else hi = mid;
+        }
+        P[k * 33 + lane] = (int)(lo - a);
+        if (lane == 0) P[k * 33 + 32] = (int)(b - a);
+    }
+}
+cudaError_t launch_rowpart(int64_t ncols, const int64_t *cp, const int32_t *row, int64_t m,
+                           int *rowpart, cudaStream_t s) {
+    if (ncols <= 0) return cudaSuccess;
+    int64_t blocks = (ncols * 32 + 255) / 256;
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    ++g_launches;
+    k_rowpart<<<(int)blocks, 256, 0, s>>>(ncols, cp, row, m, rowpart);
+    return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ reductions
 __global__ void k_reduce_i64(const int64_t *__restrict__ x, int64_t n, unsigned long long *out) {
     __shared__ int64_t sh[8];
@@ -204,7 +234,7 @@ __global__ void k_classify(ClassifyArgs c) {
         atomicAdd(&c.bin_flops[b], (unsigned long long)f);
         atomicAdd(&c.bin_nnzb[b], (unsigned long long)nb);
         if (b == kNumBins) {
-            int64_t cap = 64;
+            int64_t cap = 64 * (kGlobalThreads / 32);
             while ((double)need > c.max_load * cap) cap <<= 1;
             c.gcap_col[col] = (int32_t)cap;
         }

@@ -11,99 +11,78 @@
 // C_*j = sum_{k in inds(B_*j)} b_kj A_*k (Gustavson in CSC).  One CTA owns
 // one output column at a time (persistent CTAs pull columns from the bin's work list).
 //
-// ACCUMULATION.  One CTA owns one output column.  Its lanes are split into groups of
-// g in {4,8,16,32} lanes (g from the average segment length flops_j / nnz(B_*j)); each
-// group gathers one operand segment A_*k at a time with kUnroll independent (row, val)
-// loads per lane in flight, then inserts a_ik * b_kj into an open-addressing table
-// keyed by row (shared memory in bins 0..5; global memory + fp64 in bin 6).  Slots are
-// claimed with an integer CAS and values added with atomicAdd.  Measured on B200
-// (tools/ubench.cu): a shared-memory float atomicAdd -- a CAS loop (ATOMS.CAST.SPIN) on
-// sm_100 -- sustains ~2.5 lane-ops/cycle/SM, plain LDS/FADD/STS ~4.5 and MATCH.ANY only
-// ~0.5, so atomics are kept and warp-synchronous conflict resolution is not used.  What
-// matters is convergence: every batch loop is warp-uniform (the trip count is the warp
-// max over its groups) and each insert ends with __syncwarp(), otherwise independent
-// thread scheduling fragments the warp after the first divergent probe (profiled at
-// 3-8 active lanes per instruction before this).
+// ACCUMULATION (atomic-free values).  The CTA of a bin has W = NT/32 warps; each warp
+// owns a private slice (cap/W slots) of the column's table and 1/W of the row space: the
+// 32-way row-partition index of A (rowpart[k][i] = first position in A_*k with row >=
+// ceil(i m/32), built once per call) gives every warp its sub-segment of each A_*k.  A warp
+// walks the column's segments on its own (32 segment descriptors loaded by its lanes, one
+// per lane, and broadcast with shuffles -- no CTA barrier), gathers one sub-segment per
+// instruction so the 32 rows of an insert are distinct, claims empty slots with an
+// integer CAS (only new keys) and adds values with a plain LDS/FADD/STS.  Measured on
+// B200 (tools/ubench.cu): shared float atomicAdd is a CAS loop (ATOMS.CAST.SPIN) at
+// ~2.5 lane-ops/cycle/SM, MATCH.ANY ~0.5, plain RMW ~4.5, so neither value atomics nor
+// warp-synchronous matching is used.  Slices are ordered by row range, so the compacted
+// table is grouped by row range for the epilogue.
 #include <type_traits>
 
 #include "kernels.h"
 
 namespace mclx {
 
-// Open addressing with linear probing, four keys per lane at a time.  Phase 1 finds
-// the slot of every (row) -- the first probe of all four is issued back to back, and
-// lanes that collide or insert a new key resolve in a warp-uniform loop (claims by
-// integer CAS; `fill` counts occupied slots and an insert that would push the load
-// past `limit` = 7/8 cap reports overflow, so an under-estimated column fails fast
-// and is re-run in a bigger bin).  Phase 2, after the warp reconverges, adds all
-// values together, so the float atomicAdd (a CAS loop on sm_100) runs with full warps.
-// Returns false (warp-uniform) on overflow.  `fresh` counts keys this lane created.
+constexpr int kParts = 32;  // row ranges of the rowpart index
+constexpr int kItems = 4;   // sub-segment chunks whose gathers a warp keeps in flight
+
+// Insert one (row, v) per valid lane into this warp's private slice (keys, vals)[0, scap).
+// The valid lanes hold distinct rows (one sub-segment), so after the slots are found the
+// value update is a plain read-modify-write.  Open addressing with linear probing; empty
+// slots are claimed with atomicCAS (lanes of the warp may race for one slot).  `fill`
+// (warp-uniform) counts claimed slots; passing `limit` (7/8 of the slice) reports
+// overflow so the column is re-run in a bigger bin.  All 32 lanes must call.
 template <int MODE, typename V>
-__device__ __forceinline__ bool insert4(int *keys, V *vals, uint32_t cap, const int (&row)[4],
-                                        const V (&v)[4], const bool (&valid)[4], int *fill,
-                                        int limit, int &fresh) {
+__device__ __forceinline__ bool warp_insert(int *keys, V *vals, uint32_t scap, bool valid, int row,
+                                            V v, int &fill, int limit) {
+    const unsigned FULL = 0xffffffffu;
+    uint32_t s = hash_slot(row, scap);
     volatile int *vk = keys;
-    uint32_t s[4];
-    int k[4];
-    bool need[4];
-#pragma unroll
-    for (int j = 0; j < 4; j++) {
-        s[j] = hash_slot(row[j], cap);
-        k[j] = valid[j] ? vk[s[j]] : row[j];
-        need[j] = k[j] != row[j];
-    }
-    bool ok = true;
-    while (__any_sync(0xffffffffu, need[0] | need[1] | need[2] | need[3])) {
-#pragma unroll
-        for (int j = 0; j < 4; j++) {
-            if (!need[j]) continue;
-            if (k[j] == kEmptyKey) {
-                if (atomicAdd(fill, 1) >= limit) {
-                    ok = false;
-                    need[j] = false;
-                    continue;
-                }
-                const int old = atomicCAS(&keys[s[j]], kEmptyKey, row[j]);
+    int k = valid ? vk[s] : row;
+    bool need = k != row;
+    while (__any_sync(FULL, need)) {
+        bool claimed = false;
+        if (need) {
+            if (k == kEmptyKey) {
+                const int old = atomicCAS(&keys[s], kEmptyKey, row);
                 if (old == kEmptyKey) {
-                    fresh++;
-                    need[j] = false;
+                    claimed = true;
+                    need = false;
                 } else {
-                    atomicSub(fill, 1);
-                    k[j] = old;  // another lane claimed the slot: re-examine it
-                    need[j] = old != row[j];
+                    k = old;  // another lane took the slot: re-examine it
+                    need = old != row;
                 }
             } else {
-                s[j] = (s[j] + 1 == cap) ? 0u : s[j] + 1;
-                k[j] = vk[s[j]];
-                need[j] = k[j] != row[j];
+                s = (s + 1 == scap) ? 0u : s + 1;
+                k = vk[s];
+                need = k != row;
             }
         }
+        fill += __popc(__ballot_sync(FULL, claimed));
+        if (fill > limit) return false;
     }
-    ok = __all_sync(0xffffffffu, ok);
-    if (MODE != kSym && ok) {
-#pragma unroll
-        for (int j = 0; j < 4; j++)
-            if (valid[j]) atomicAdd(&vals[s[j]], v[j]);
-    }
-    return ok;
-}
-
-__device__ __forceinline__ int group_size_for(int64_t avg) {
-    return avg >= 24 ? 32 : avg >= 12 ? 16 : avg >= 6 ? 8 : 4;
+    if (MODE != kSym && valid) vals[s] += v;
+    __syncwarp();
+    return true;
 }
 
 template <int CAP, int NT, int MODE, bool GLOBAL>
-__global__ void __launch_bounds__(NT, 1024 / NT) k_bin(BinArgs a) {
+__global__ void __launch_bounds__(NT, (1024 / NT > 32 ? 32 : 1024 / NT)) k_bin(BinArgs a) {
     using V = typename std::conditional<GLOBAL, double, float>::type;
     extern __shared__ __align__(16) unsigned char dsm[];
     __shared__ unsigned hist[256];
     __shared__ int sint[4];
     __shared__ double sred[NT / 32];
     __shared__ int sscan[NT / 32];
-    __shared__ int s_col, s_idx, s_ovf, s_fill;
-    __shared__ int64_t st_start[NT];
-    __shared__ int st_k[NT];
-    __shared__ float st_b[NT];
+    __shared__ int s_col, s_idx, s_ovf;
+    constexpr int W = NT / 32;         // warps = row-range owners
+    constexpr int PSTEP = kParts / W;  // rowpart boundaries per warp
 
     const int tid = threadIdx.x;
     const int lane = lane_id();
@@ -115,7 +94,6 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_bin(BinArgs a) {
             s_idx = idx;
             s_col = idx < count ? a.list[idx] : -1;
             s_ovf = 0;
-            s_fill = 0;
         }
         __syncthreads();
         const int col = s_col;
@@ -140,79 +118,76 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_bin(BinArgs a) {
         }
         __syncthreads();
 
-        // ---- accumulate C_*j = sum_k b_kj A_*k.  Each lane gathers 4 consecutive
-        // (row, val) pairs of a segment with one 16-byte load each (segment starts are
-        // aligned down to 4 elements and the head / tail masked).
-        const int limit = (int)(cap - (cap >> 3));
+        // ---- accumulate C_*j = sum_k b_kj A_*k: warp `warp` handles rows of its range
+        const uint32_t scap = cap / W;
+        int *wkeys = keys + (size_t)warp * scap;
+        V *wvals = vals + (size_t)warp * scap;
+        const int limit = (int)(scap - (scap >> 3));
         const int64_t bj = a.cb + col;
         const int64_t q0 = a.bcp[bj], q1 = a.bcp[bj + 1];
-        const int64_t nb = q1 - q0;
-        const int g = group_size_for(nb > 0 ? a.flops[col] / (4 * nb) : 0);
-        const int lane_g = lane & (g - 1);
-        const int grp = tid / g;        // group index in the CTA
-        const int ngrp = NT / g;
-        int fresh = 0;
+        int fill = 0;
         bool ok = true;
-        volatile int *vovf = &s_ovf;
-        for (int64_t c0 = q0; c0 < q1; c0 += NT) {
-            const int cnt = (int)((q1 - c0) < NT ? (q1 - c0) : NT);
-            if (tid < cnt) {
-                const int k = __ldg(a.brow + c0 + tid);
-                const int64_t st = __ldg(a.acp + k);
-                st_start[tid] = st;
-                st_k[tid] = (int)(__ldg(a.acp + k + 1) - st);  // segment length
-                st_b[tid] = __ldg(a.bval + c0 + tid);
+        for (int64_t e0 = q0; e0 < q1 && ok; e0 += 32) {
+            // lane l holds the descriptor of segment e0 + l (this warp's sub-segment)
+            int64_t dlo = 0;
+            int dlen = 0;
+            float db = 0.f;
+            if (e0 + lane < q1) {
+                const int k = __ldg(a.brow + e0 + lane);
+                const int64_t base = __ldg(a.acp + k);
+                if (W == 1) {
+                    dlo = base;
+                    dlen = (int)(__ldg(a.acp + k + 1) - base);
+                } else {
+                    const int *pk = a.rowpart + (int64_t)k * (kParts + 1) + warp * PSTEP;
+                    const int p0 = __ldg(pk), p1 = __ldg(pk + PSTEP);
+                    dlo = base + p0;
+                    dlen = p1 - p0;
+                }
+                db = __ldg(a.bval + e0 + lane);
             }
-            __syncthreads();
-            const int wgrp0 = warp * (32 / g);
-            for (int e0 = 0; e0 < cnt && ok; e0 += ngrp) {
-                if (e0 + wgrp0 >= cnt) break;  // warp-uniform: no work for this warp's groups
-                if (*vovf) {
-                    ok = false;
-                    break;
-                }
-                const int e = e0 + grp;
-                int lo = 0, hi = 0;     // valid element window relative to the aligned base
-                float bkj = 0.f;
-                const int *rp = a.arow;
-                const float *vp = a.aval;
-                if (e < cnt) {
-                    const int64_t t0 = st_start[e];
-                    const int64_t ab = t0 & ~(int64_t)3;
-                    rp = a.arow + ab;
-                    vp = a.aval + ab;
-                    lo = (int)(t0 - ab);
-                    hi = lo + st_k[e];
-                    bkj = st_b[e];
-                }
-                const unsigned nstep = (unsigned)((hi + 4 * g - 1) / (4 * g));
-                const unsigned maxs = __reduce_max_sync(0xffffffffu, nstep);
-                for (unsigned si = 0; si < maxs; si++) {
-                    const int i0 = 4 * ((int)si * g + lane_g);
-                    int4 r4 = make_int4(-1, -1, -1, -1);
-                    float4 v4 = make_float4(0.f, 0.f, 0.f, 0.f);
-                    if (i0 < hi) {
-                        r4 = __ldg(reinterpret_cast<const int4 *>(rp + i0));
-                        if (MODE != kSym) v4 = __ldg(reinterpret_cast<const float4 *>(vp + i0));
-                    }
-                    const int rr[4] = {r4.x, r4.y, r4.z, r4.w};
-                    V pv[4];
-                    bool vld[4];
+            const int ncnt = (int)((q1 - e0) < 32 ? (q1 - e0) : 32);
+            int e = 0, o = 0;  // warp-uniform cursor: segment, offset
+            while (e < ncnt && ok) {
+                int rr[kItems];
+                V vv[kItems];
+                bool vl[kItems];
 #pragma unroll
-                    for (int j = 0; j < 4; j++) {
-                        vld[j] = i0 + j >= lo && i0 + j < hi;
-                        pv[j] = GLOBAL ? (V)(&v4.x)[j] * (V)bkj : (V)((&v4.x)[j] * bkj);
+                for (int u = 0; u < kItems; u++) {
+                    int len_e = __shfl_sync(0xffffffffu, dlen, e & 31);
+                    while (e < ncnt && o >= len_e) {
+                        e++;
+                        o = 0;
+                        len_e = __shfl_sync(0xffffffffu, dlen, e & 31);
                     }
-                    if (!insert4<MODE, V>(keys, vals, cap, rr, pv, vld, &s_fill, limit, fresh)) {
-                        ok = false;
-                        *vovf = 1;
+                    vl[u] = false;
+                    rr[u] = -1;
+                    vv[u] = V(0);
+                    if (e < ncnt) {
+                        const int64_t lo_e = __shfl_sync(0xffffffffu, dlo, e);
+                        const float b_e = __shfl_sync(0xffffffffu, db, e);
+                        const int t = o + lane;
+                        if (t < len_e) {
+                            vl[u] = true;
+                            rr[u] = __ldg(a.arow + lo_e + t);
+                            if (MODE != kSym) {
+                                const float av = __ldg(a.aval + lo_e + t);
+                                vv[u] = GLOBAL ? (V)av * (V)b_e : (V)(av * b_e);
+                            }
+                        }
+                        o += 32;
                     }
-                    if (!__all_sync(0xffffffffu, ok)) break;
                 }
-                ok = __all_sync(0xffffffffu, ok);
+#pragma unroll
+                for (int u = 0; u < kItems; u++) {
+                    if (!warp_insert<MODE, V>(wkeys, wvals, scap, vl[u], rr[u], vv[u], fill, limit)) {
+                        ok = false;
+                        break;
+                    }
+                }
             }
-            __syncthreads();
         }
+        const int fresh = lane == 0 ? fill : 0;
         if (!ok && lane == 0) s_ovf = 1;
         __syncthreads();
         if (s_ovf) {
@@ -330,12 +305,12 @@ static cudaError_t launch_of(const BinArgs &a, int grid, cudaStream_t s) {
 
 #define MCLX_BIN_SWITCH(MODE, WHAT, ...)                                          \
     switch (bin) {                                                                \
-        case 0: return WHAT<512, 64, MODE, false>(__VA_ARGS__);                   \
-        case 1: return WHAT<1024, 64, MODE, false>(__VA_ARGS__);                  \
-        case 2: return WHAT<2048, 128, MODE, false>(__VA_ARGS__);                 \
-        case 3: return WHAT<4096, 256, MODE, false>(__VA_ARGS__);                 \
-        case 4: return WHAT<8192, 512, MODE, false>(__VA_ARGS__);                 \
-        case 5: return WHAT<16384, 1024, MODE, false>(__VA_ARGS__);               \
+        case 0: return WHAT<512, 32, MODE, false>(__VA_ARGS__);                   \
+        case 1: return WHAT<1024, 32, MODE, false>(__VA_ARGS__);                  \
+        case 2: return WHAT<2048, 64, MODE, false>(__VA_ARGS__);                  \
+        case 3: return WHAT<4096, 128, MODE, false>(__VA_ARGS__);                 \
+        case 4: return WHAT<8192, 256, MODE, false>(__VA_ARGS__);                 \
+        case 5: return WHAT<16384, 512, MODE, false>(__VA_ARGS__);                \
         default: return WHAT<0, kGlobalThreads, MODE, true>(__VA_ARGS__);         \
     }
 
