@@ -147,42 +147,42 @@ __global__ void __launch_bounds__(NT, (1024 / NT > 32 ? 32 : 1024 / NT)) k_bin(B
                 db = __ldg(a.bval + e0 + lane);
             }
             const int ncnt = (int)((q1 - e0) < 32 ? (q1 - e0) : 32);
-            int e = 0, o = 0;  // warp-uniform cursor: segment, offset
-            while (e < ncnt && ok) {
-                int rr[kItems];
-                V vv[kItems];
-                bool vl[kItems];
+            // kItems segments side by side; chunks of 32 rows of each per step
+            for (int eb = 0; eb < ncnt && ok; eb += kItems) {
+                int64_t lo_u[kItems];
+                int len_u[kItems];
+                float b_u[kItems];
+                int maxlen = 0;
 #pragma unroll
                 for (int u = 0; u < kItems; u++) {
-                    int len_e = __shfl_sync(0xffffffffu, dlen, e & 31);
-                    while (e < ncnt && o >= len_e) {
-                        e++;
-                        o = 0;
-                        len_e = __shfl_sync(0xffffffffu, dlen, e & 31);
-                    }
-                    vl[u] = false;
-                    rr[u] = -1;
-                    vv[u] = V(0);
-                    if (e < ncnt) {
-                        const int64_t lo_e = __shfl_sync(0xffffffffu, dlo, e);
-                        const float b_e = __shfl_sync(0xffffffffu, db, e);
-                        const int t = o + lane;
-                        if (t < len_e) {
-                            vl[u] = true;
-                            rr[u] = __ldg(a.arow + lo_e + t);
-                            if (MODE != kSym) {
-                                const float av = __ldg(a.aval + lo_e + t);
-                                vv[u] = GLOBAL ? (V)av * (V)b_e : (V)(av * b_e);
-                            }
-                        }
-                        o += 32;
-                    }
+                    const int e = eb + u;
+                    lo_u[u] = __shfl_sync(0xffffffffu, dlo, e & 31);
+                    len_u[u] = __shfl_sync(0xffffffffu, dlen, e & 31);
+                    b_u[u] = __shfl_sync(0xffffffffu, db, e & 31);
+                    if (e >= ncnt) len_u[u] = 0;
+                    maxlen = len_u[u] > maxlen ? len_u[u] : maxlen;
                 }
+                for (int c = 0; c < maxlen && ok; c += 32) {
+                    int rr[kItems];
+                    V vv[kItems];
+                    bool vl[kItems];
+                    const int t = c + lane;
 #pragma unroll
-                for (int u = 0; u < kItems; u++) {
-                    if (!warp_insert<MODE, V>(wkeys, wvals, scap, vl[u], rr[u], vv[u], fill, limit)) {
-                        ok = false;
-                        break;
+                    for (int u = 0; u < kItems; u++) {
+                        vl[u] = t < len_u[u];
+                        rr[u] = vl[u] ? __ldg(a.arow + lo_u[u] + t) : -1;
+                        vv[u] = V(0);
+                        if (MODE != kSym && vl[u]) {
+                            const float av = __ldg(a.aval + lo_u[u] + t);
+                            vv[u] = GLOBAL ? (V)av * (V)b_u[u] : (V)(av * b_u[u]);
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < kItems; u++) {
+                        if (!warp_insert<MODE, V>(wkeys, wvals, scap, vl[u], rr[u], vv[u], fill, limit)) {
+                            ok = false;
+                            break;
+                        }
                     }
                 }
             }
