@@ -42,6 +42,7 @@ struct mcl_ctx {
     // 2D Sparse-SUMMA grid (mcl_ctx_set_grid): world / row / column communicators
     int pr = 1, pc = 1, rank = 0;
     ncclComm_t world = nullptr, rowc = nullptr, colc = nullptr;
+    int64_t gbin_budget = (int64_t)8 << 30;  // bytes of fp64 global-bin tables live at once
     float alpha = 1.2f;     // table sizing: need = alpha * Cohen estimate + 16
     float max_load = 0.5f;  // bin when need <= max_load * cap
 };
@@ -293,28 +294,56 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
             a.retry_count = retry_count;
             a.err_flag = err;
             a.bin_out = bout + b;
+            const int occ = std::max(1, c->occ[mode][b]);
             if (b == kNumBins) {
+                // fp64 global-memory tables, allocated per chunk of the bin's list so that
+                // the live tables stay within c->gbin_budget bytes (R-MAT hubs: C4)
                 int32_t *gcap;
                 int64_t *gcap64, *goff;
+                int *gcount;
                 void *tmp;
                 RC(scratch_t(c, "gcap", (size_t)hc[b], &gcap));
                 RC(scratch_t(c, "gcap64", (size_t)hc[b], &gcap64));
                 RC(scratch_t(c, "goff", (size_t)hc[b] + 1, &goff));
+                RC(scratch_t(c, "gcount", 2, &gcount));
                 RC(scratch(c, "scan_tmp", scan_tmp_bytes(hc[b]), &tmp));
                 CK(launch_global_layout(hc[b], a.list, gcap_col, gcap, gcap64, c->stream));
                 CK(launch_scan_i64(gcap64, goff, hc[b], tmp, c->stream));
-                int64_t gtot = 0;
-                RC(readback(c, goff + hc[b], sizeof(int64_t), &gtot));
-                int *gkeys;
-                double *gvals;
-                RC(scratch_t(c, "gkeys", (size_t)gtot, &gkeys));
-                RC(scratch_t(c, "gvals", (size_t)gtot, &gvals));
-                a.goff = goff;
-                a.gcap = gcap;
-                a.gkeys = gkeys;
-                a.gvals = gvals;
+                std::vector<int64_t> hoff((size_t)hc[b] + 1);
+                CK(cudaMemcpyAsync(hoff.data(), goff, sizeof(int64_t) * (hc[b] + 1),
+                                   cudaMemcpyDeviceToHost, c->stream));
+                CK(cudaStreamSynchronize(c->stream));
+                const int64_t slots_budget = std::max<int64_t>(c->gbin_budget / 12, 1 << 20);
+                CK(cudaEventRecord(c->bev[2 * b], c->stream));
+                for (int i0 = 0; i0 < hc[b];) {
+                    int i1 = i0 + 1;
+                    while (i1 < hc[b] && hoff[i1 + 1] - hoff[i0] <= slots_budget) i1++;
+                    const int64_t chunk = hoff[i1] - hoff[i0];
+                    int *gkeys;
+                    double *gvals;
+                    RC(scratch_t(c, "gkeys", (size_t)chunk, &gkeys));
+                    RC(scratch_t(c, "gvals", (size_t)chunk, &gvals));
+                    const int cnt_chunk = i1 - i0;
+                    CK(cudaMemcpyAsync(gcount, &cnt_chunk, sizeof(int), cudaMemcpyHostToDevice,
+                                       c->stream));
+                    CK(cudaMemsetAsync(gcount + 1, 0, sizeof(int), c->stream));
+                    BinArgs ag = a;
+                    ag.list = a.list + i0;
+                    ag.count = gcount;
+                    ag.counter = gcount + 1;
+                    ag.goff = goff + i0;
+                    ag.gcap = gcap + i0;
+                    ag.gkeys = gkeys - hoff[i0];   // goff[idx] - hoff[i0] indexes the chunk
+                    ag.gvals = gvals - hoff[i0];
+                    const int grid = (int)std::min<int64_t>(cnt_chunk, (int64_t)occ * c->sms);
+                    CK(launch_bin(mode, b, ag, grid, c->stream));
+                    if (i1 < hc[b]) CK(cudaStreamSynchronize(c->stream));  // scratch reuse
+                    i0 = i1;
+                }
+                CK(cudaEventRecord(c->bev[2 * b + 1], c->stream));
+                launched[b] = true;
+                continue;
             }
-            const int occ = std::max(1, c->occ[mode][b]);
             const int grid = (int)std::min<int64_t>(hc[b], (int64_t)occ * c->sms);
             CK(cudaEventRecord(c->bev[2 * b], c->stream));
             CK(launch_bin(mode, b, a, grid, c->stream));
@@ -722,6 +751,7 @@ int mcl_ctx_create(mcl_ctx_t *out, int device, void *stream, mcl_alloc_fn alloc,
     c->sms = prop.multiProcessorCount;
     if (const char *e = getenv("MCLX_ALPHA")) c->alpha = (float)atof(e);
     if (const char *e = getenv("MCLX_MAX_LOAD")) c->max_load = (float)atof(e);
+    if (const char *e = getenv("MCLX_GBIN_BUDGET_MB")) c->gbin_budget = (int64_t)atoll(e) << 20;
     if (cudaMallocHost(&c->pin, 4096) != cudaSuccess) {
         delete c;
         return MCL_ERR_CUDA;

@@ -277,6 +277,35 @@ def test_iterate_c1_second_iteration_all_bins():
         kept_parity(host_mat(Ag), Cr1, info, (1e-4, 1100, 1400, 0.9))
 
 
+@pytest.mark.parametrize("scale", [12, 14])
+def test_rmat_iterate_parity(scale):
+    """R-MAT (C4 shape: skewed degrees, hub columns) -- one fused iteration vs the oracle."""
+    A = f32(O.preprocess(synth.rmat(scale=scale, seed=4)))
+    Ag, st = M.iterate(dev(A), M.Params())
+    Cr, fl = O.expand(A)
+    _, info = O.prune_inflate(Cr, 1e-4, 1100, 1400, 0.9, 2.0)
+    kept_parity(host_mat(Ag), Cr, info, (1e-4, 1100, 1400, 0.9))
+    assert st["flops"] == int(fl.sum())
+
+
+def test_global_bin_chunked(monkeypatch):
+    """fp64 global-memory bin processed in memory-bounded chunks (R-MAT hubs)."""
+    monkeypatch.setenv("MCLX_GBIN_BUDGET_MB", "1")
+    ctx = M.Context()
+    A0 = O.preprocess(synth.planted_partition())
+    Cr, _ = O.expand(A0)
+    A1, _ = O.prune_inflate(Cr, 1e-4, 1100, 1400, 0.9, 2.0)
+    A1 = f32(A1)
+    Cg, st = ctx.expand(dev(A1), params=M.Params(force_bin=6))
+    Cr1, _ = O.expand(A1)
+    assert_unpruned_parity(host_mat(Cg), Cr1)
+    assert st["bin_cols"][6] == A1.ncols
+    Ag, st = ctx.iterate(dev(A1), M.Params(force_bin=6))
+    _, info = O.prune_inflate(Cr1, 1e-4, 1100, 1400, 0.9, 2.0)
+    kept_parity(host_mat(Ag), Cr1, info, (1e-4, 1100, 1400, 0.9))
+    ctx.close()
+
+
 # ---------------------------------------------------------------- clusters (P4)
 @pytest.mark.parametrize("seed", range(4))
 def test_clusters_random(seed):
