@@ -81,8 +81,10 @@ typedef struct {
     double mem_safety;       /* [0.9] fraction of free HBM the phase planner may use (Q15)     */
     int32_t estimator;       /* [0] 0 = policy of P:1076-1077, 1 = always exact symbolic,
                                 2 = always Cohen (with overflow retry)                        */
-    int32_t force_bin;       /* [-1] >= 0 forces every non-empty column into that smem bin (or
-                                the global bin, MCL_NUM_BINS) -- for bin-invariance tests      */
+    int32_t force_bin;       /* [-1] >= 0 forces every non-empty column into bin (force_bin % 7)
+                                or a bigger one (6 = the fp64 global-memory bin), of kernel
+                                family force_bin / 7 (0 private row-range slices, 1 CTA-shared
+                                atomic table) -- for bin-invariance tests                      */
 } mcl_params_t;
 
 #define MCL_NUM_BINS 6 /* shared-memory bins; bin index MCL_NUM_BINS is the global-memory bin */

@@ -33,16 +33,16 @@ struct mcl_ctx {
     int sms = 148;
     std::unordered_map<std::string, Buf> scratch;
     size_t cur = 0, peak = 0;
-    int occ[3][kNumBins + 1] = {};
+    int occ[3][kAllBins] = {};
     void *pin = nullptr;  // pinned host staging for small read-backs
     cudaEvent_t ev[8] = {};
-    cudaEvent_t bev[2 * (kNumBins + 1)] = {};
+    cudaEvent_t bev[2 * kAllBins] = {};
     cudaEvent_t pev[6] = {};  // phases of the distributed prune
     cudaEvent_t sev[3] = {};  // SUMMA iteration (ev[] is reused by the stage products)
     // 2D Sparse-SUMMA grid (mcl_ctx_set_grid): world / row / column communicators
     int pr = 1, pc = 1, rank = 0;
     ncclComm_t world = nullptr, rowc = nullptr, colc = nullptr;
-    int64_t gbin_budget = (int64_t)8 << 30;  // bytes of fp64 global-bin tables live at once
+    int64_t gbin_budget = (int64_t)32 << 30;  // bytes of fp64 global-bin tables live at once
     float alpha = 1.2f;     // table sizing: need = alpha * Cohen estimate + 16
     float max_load = 0.5f;  // bin when need <= max_load * cap
 };
@@ -213,7 +213,7 @@ int cohen(mcl_ctx *c, const Prod &pr, int r, uint64_t seed, float *est, float *k
 int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float *est,
              const int64_t *exact, int force_bin, BinArgs base, mcl_stats_t *st) {
     const int64_t n = pr.n;
-    const int NB1 = kNumBins + 1;
+    const int NB1 = kAllBins;  // both kernel families
     int *counts, *counters, *retry_count, *err;
     unsigned long long *bflops;
     int32_t *lists, *gcap_col, *retry_list, *retry_in;
@@ -255,7 +255,8 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
         ca.m = pr.A->nrows;
         ca.alpha = round == 0 ? c->alpha : 4.0f * c->alpha;
         ca.max_load = round == 2 ? 0.5f : c->max_load;
-        ca.force_bin = force_bin;
+        ca.force_bin = force_bin < 0 ? -1 : force_bin % kFamily;
+        ca.force_family = force_bin < 0 ? -1 : force_bin / kFamily;
         ca.list_stride = std::max<int64_t>(n, 1);
         ca.bin_count = counts;
         ca.lists = lists;
@@ -263,19 +264,21 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
         ca.bin_flops = bflops;
         ca.bin_nnzb = bnnzb;
         CK(launch_classify(ca, c->stream));
-        int hc[2 * 8 + 1];
-        unsigned long long hf[3 * 8];
+        int hc[2 * kAllBins + 1];
+        unsigned long long hf[3 * kAllBins];
         RC(readback(c, counts, sizeof(int) * NB1, hc));
         RC(readback(c, bflops, sizeof(unsigned long long) * 2 * NB1, hf));
         if (st && round == 0) {
             for (int b = 0; b < NB1; b++) {
-                st->bin_cols[b] += hc[b];
-                st->bin_flops[b] += (int64_t)hf[b];
-                st->bin_nnzb[b] += (int64_t)hf[NB1 + b];
+                st->bin_cols[b % kFamily] += hc[b];
+                st->bin_flops[b % kFamily] += (int64_t)hf[b];
+                st->bin_nnzb[b % kFamily] += (int64_t)hf[NB1 + b];
             }
         }
-        bool launched[8] = {};
-        for (int b = kNumBins; b >= 0; b--) {
+        bool launched[kAllBins] = {};
+        for (int bi = kAllBins - 1; bi >= 0; bi--) {
+            // heaviest bins first: global, then big shared-memory tables, both families
+            const int b = (bi % 2 == 0) ? bi / 2 : kFamily + bi / 2;
             if (hc[b] == 0) continue;
             BinArgs a = base;
             a.acp = pr.A->col_ptr;
@@ -295,7 +298,7 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
             a.err_flag = err;
             a.bin_out = bout + b;
             const int occ = std::max(1, c->occ[mode][b]);
-            if (b == kNumBins) {
+            if (b % kFamily == kNumBins) {
                 // fp64 global-memory tables, allocated per chunk of the bin's list so that
                 // the live tables stay within c->gbin_budget bytes (R-MAT hubs: C4)
                 int32_t *gcap;
@@ -307,6 +310,20 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
                 RC(scratch_t(c, "goff", (size_t)hc[b] + 1, &goff));
                 RC(scratch_t(c, "gcount", 2, &gcount));
                 RC(scratch(c, "scan_tmp", scan_tmp_bytes(hc[b]), &tmp));
+                {   // largest columns first (LPT): homogeneous chunks, hubs start first
+                    std::vector<int32_t> hl((size_t)hc[b]);
+                    std::vector<int64_t> hfl((size_t)pr.n);
+                    CK(cudaMemcpyAsync(hl.data(), a.list, sizeof(int32_t) * hc[b],
+                                       cudaMemcpyDeviceToHost, c->stream));
+                    CK(cudaMemcpyAsync(hfl.data(), f, sizeof(int64_t) * pr.n, cudaMemcpyDeviceToHost,
+                                       c->stream));
+                    CK(cudaStreamSynchronize(c->stream));
+                    std::stable_sort(hl.begin(), hl.end(),
+                                     [&](int32_t x, int32_t y) { return hfl[x] > hfl[y]; });
+                    CK(cudaMemcpyAsync(const_cast<int32_t *>(a.list), hl.data(),
+                                       sizeof(int32_t) * hc[b], cudaMemcpyHostToDevice, c->stream));
+                    CK(cudaStreamSynchronize(c->stream));
+                }
                 CK(launch_global_layout(hc[b], a.list, gcap_col, gcap, gcap64, c->stream));
                 CK(launch_scan_i64(gcap64, goff, hc[b], tmp, c->stream));
                 std::vector<int64_t> hoff((size_t)hc[b] + 1);
@@ -357,7 +374,7 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
                 if (!launched[b]) continue;
                 float ms = 0.f;
                 CK(cudaEventElapsedTime(&ms, c->bev[2 * b], c->bev[2 * b + 1]));
-                st->bin_ms[b] += ms;
+                st->bin_ms[b % kFamily] += ms;
             }
         }
         if (nretry == 0) break;
@@ -370,9 +387,9 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
         cls_list = retry_in;
     }
     if (st) {
-        unsigned long long ho[8];
+        unsigned long long ho[kAllBins];
         RC(readback(c, bout, sizeof(unsigned long long) * NB1, ho));
-        for (int b = 0; b < NB1; b++) st->bin_out[b] += (int64_t)ho[b];
+        for (int b = 0; b < NB1; b++) st->bin_out[b % kFamily] += (int64_t)ho[b];
     }
     int herr = 0;
     RC(readback(c, err, sizeof(int), &herr));
@@ -757,11 +774,11 @@ int mcl_ctx_create(mcl_ctx_t *out, int device, void *stream, mcl_alloc_fn alloc,
         return MCL_ERR_CUDA;
     }
     for (int i = 0; i < 8; i++) cudaEventCreate(&c->ev[i]);
-    for (int i = 0; i < 2 * (kNumBins + 1); i++) cudaEventCreate(&c->bev[i]);
+    for (int i = 0; i < 2 * kAllBins; i++) cudaEventCreate(&c->bev[i]);
     for (int i = 0; i < 6; i++) cudaEventCreate(&c->pev[i]);
     for (int i = 0; i < 3; i++) cudaEventCreate(&c->sev[i]);
     for (int m = 0; m < 3; m++)
-        for (int b = 0; b <= kNumBins; b++) c->occ[m][b] = bin_occupancy(m, b);
+        for (int b = 0; b < kAllBins; b++) c->occ[m][b] = bin_occupancy(m, b);
     if (cudaGetLastError() != cudaSuccess) {
         mcl_ctx_destroy(c);
         return MCL_ERR_CUDA;
@@ -788,7 +805,7 @@ int mcl_ctx_destroy(mcl_ctx_t c) {
     cudaStreamSynchronize(c->stream);
     for (int i = 0; i < 8; i++)
         if (c->ev[i]) cudaEventDestroy(c->ev[i]);
-    for (int i = 0; i < 2 * (kNumBins + 1); i++)
+    for (int i = 0; i < 2 * kAllBins; i++)
         if (c->bev[i]) cudaEventDestroy(c->bev[i]);
     for (int i = 0; i < 6; i++)
         if (c->pev[i]) cudaEventDestroy(c->pev[i]);

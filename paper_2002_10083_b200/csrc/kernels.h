@@ -64,7 +64,14 @@ struct BinArgs {
     PruneParams pp;
 };
 
-// One launch of bin `bin` (0..kNumBins) in mode `mode`; grid chosen from occupancy.
+// Two kernel families share the bins: private row-range slices (bin b = 0..kNumBins) for
+// columns whose average gathered segment is long, and a CTA-shared atomic table
+// (bin kFamily + b) for short-segment (R-MAT-like) columns.
+constexpr int kFamily = kNumBins + 1;
+constexpr int kAllBins = 2 * kFamily;
+constexpr int kShortSegment = 16;  // flops_j / nnz(B_*j) below this -> atomic family
+
+// One launch of bin `bin` (0..kAllBins-1) in mode `mode`; grid chosen from occupancy.
 cudaError_t launch_bin(int mode, int bin, const BinArgs &a, int grid, cudaStream_t s);
 // Max resident CTAs per SM for (mode, bin); also sets the dynamic smem attribute.
 int bin_occupancy(int mode, int bin);
@@ -94,9 +101,10 @@ struct ClassifyArgs {
     float alpha;
     float max_load;          // table load factor bound used for binning (<= 0.5 default)
     int force_bin;
+    int force_family;        // -1 auto, 0 private slices, 1 atomic shared table
     int64_t list_stride;     // columns per bin list
-    int *bin_count;          // [kNumBins + 1]
-    int32_t *lists;          // [(kNumBins + 1) * list_stride]
+    int *bin_count;          // [kAllBins]
+    int32_t *lists;          // [kAllBins * list_stride]
     int32_t *gcap_col;       // [ncols_out]
     unsigned long long *bin_flops;  // [kNumBins + 1]
     unsigned long long *bin_nnzb;   // [kNumBins + 1] sum of nnz(B_*j)

@@ -229,10 +229,14 @@ __global__ void k_classify(ClassifyArgs c) {
         while (b < kNumBins && (double)need > c.max_load * bin_cap(b)) b++;
         if (nb > kFp64Terms) b = kNumBins;
         if (c.force_bin > b && c.force_bin <= kNumBins) b = c.force_bin;
-        const int pos = atomicAdd(&c.bin_count[b], 1);
-        c.lists[(int64_t)b * c.list_stride + pos] = (int32_t)col;
-        atomicAdd(&c.bin_flops[b], (unsigned long long)f);
-        atomicAdd(&c.bin_nnzb[b], (unsigned long long)nb);
+        // family: short average segments go to the CTA-shared atomic table
+        const bool shortseg = f < (int64_t)kShortSegment * nb;
+        const int fam = c.force_family >= 0 ? c.force_family : (shortseg ? 1 : 0);
+        const int bb = fam * kFamily + b;
+        const int pos = atomicAdd(&c.bin_count[bb], 1);
+        c.lists[(int64_t)bb * c.list_stride + pos] = (int32_t)col;
+        atomicAdd(&c.bin_flops[bb], (unsigned long long)f);
+        atomicAdd(&c.bin_nnzb[bb], (unsigned long long)nb);
         if (b == kNumBins) {
             int64_t cap = 64 * (kGlobalThreads / 32);
             while ((double)need > c.max_load * cap) cap <<= 1;

@@ -32,6 +32,68 @@ namespace mclx {
 constexpr int kParts = 32;  // row ranges of the rowpart index
 constexpr int kItems = 4;   // sub-segment chunks whose gathers a warp keeps in flight
 
+// Open addressing with linear probing, four keys per lane at a time.  Phase 1 finds
+// the slot of every (row) -- the first probe of all four is issued back to back, and
+// lanes that collide or insert a new key resolve in a warp-uniform loop (claims by
+// integer CAS; `fill` counts occupied slots and an insert that would push the load
+// past `limit` = 7/8 cap reports overflow, so an under-estimated column fails fast
+// and is re-run in a bigger bin).  Phase 2, after the warp reconverges, adds all
+// values together, so the float atomicAdd (a CAS loop on sm_100) runs with full warps.
+// Returns false (warp-uniform) on overflow.  `fresh` counts keys this lane created.
+template <int MODE, typename V>
+__device__ __forceinline__ bool insert4(int *keys, V *vals, uint32_t cap, const int (&row)[4],
+                                        const V (&v)[4], const bool (&valid)[4], int *fill,
+                                        int limit, int &fresh) {
+    volatile int *vk = keys;
+    uint32_t s[4];
+    int k[4];
+    bool need[4];
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+        s[j] = hash_slot(row[j], cap);
+        k[j] = valid[j] ? vk[s[j]] : row[j];
+        need[j] = k[j] != row[j];
+    }
+    bool ok = true;
+    while (__any_sync(0xffffffffu, need[0] | need[1] | need[2] | need[3])) {
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            if (!need[j]) continue;
+            if (k[j] == kEmptyKey) {
+                if (atomicAdd(fill, 1) >= limit) {
+                    ok = false;
+                    need[j] = false;
+                    continue;
+                }
+                const int old = atomicCAS(&keys[s[j]], kEmptyKey, row[j]);
+                if (old == kEmptyKey) {
+                    fresh++;
+                    need[j] = false;
+                } else {
+                    atomicSub(fill, 1);
+                    k[j] = old;  // another lane claimed the slot: re-examine it
+                    need[j] = old != row[j];
+                }
+            } else {
+                s[j] = (s[j] + 1 == cap) ? 0u : s[j] + 1;
+                k[j] = vk[s[j]];
+                need[j] = k[j] != row[j];
+            }
+        }
+    }
+    ok = __all_sync(0xffffffffu, ok);
+    if (MODE != kSym && ok) {
+#pragma unroll
+        for (int j = 0; j < 4; j++)
+            if (valid[j]) atomicAdd(&vals[s[j]], v[j]);
+    }
+    return ok;
+}
+
+__device__ __forceinline__ int group_size_for(int64_t avg) {
+    return avg >= 24 ? 32 : avg >= 12 ? 16 : avg >= 6 ? 8 : 4;
+}
+
 // Insert one (row, v) per valid lane into this warp's private slice (keys, vals)[0, scap).
 // The valid lanes hold distinct rows (one sub-segment), so after the slots are found the
 // value update is a plain read-modify-write.  Open addressing with linear probing; empty
@@ -72,7 +134,7 @@ __device__ __forceinline__ bool warp_insert(int *keys, V *vals, uint32_t scap, b
     return true;
 }
 
-template <int CAP, int NT, int MODE, bool GLOBAL>
+template <int CAP, int NT, int MODE, bool GLOBAL, bool ATOMIC>
 __global__ void __launch_bounds__(NT, (1024 / NT > 32 ? 32 : 1024 / NT)) k_bin(BinArgs a) {
     using V = typename std::conditional<GLOBAL, double, float>::type;
     extern __shared__ __align__(16) unsigned char dsm[];
@@ -118,76 +180,161 @@ __global__ void __launch_bounds__(NT, (1024 / NT > 32 ? 32 : 1024 / NT)) k_bin(B
         }
         __syncthreads();
 
-        // ---- accumulate C_*j = sum_k b_kj A_*k: warp `warp` handles rows of its range
-        const uint32_t scap = cap / W;
-        int *wkeys = keys + (size_t)warp * scap;
-        V *wvals = vals + (size_t)warp * scap;
-        const int limit = (int)(scap - (scap >> 3));
-        const int64_t bj = a.cb + col;
-        const int64_t q0 = a.bcp[bj], q1 = a.bcp[bj + 1];
-        int fill = 0;
+        int fresh = 0;
         bool ok = true;
-        for (int64_t e0 = q0; e0 < q1 && ok; e0 += 32) {
-            // lane l holds the descriptor of segment e0 + l (this warp's sub-segment)
-            int64_t dlo = 0;
-            int dlen = 0;
-            float db = 0.f;
-            if (e0 + lane < q1) {
-                const int k = __ldg(a.brow + e0 + lane);
-                const int64_t base = __ldg(a.acp + k);
-                if (W == 1) {
-                    dlo = base;
-                    dlen = (int)(__ldg(a.acp + k + 1) - base);
-                } else {
-                    const int *pk = a.rowpart + (int64_t)k * (kParts + 1) + warp * PSTEP;
-                    const int p0 = __ldg(pk), p1 = __ldg(pk + PSTEP);
-                    dlo = base + p0;
-                    dlen = p1 - p0;
+        if constexpr (ATOMIC) {
+            // ---- short segments (R-MAT-like): CTA-shared table, groups of g lanes per
+            // segment, integer-CAS claims and float atomicAdd values (insert4)
+            __shared__ int64_t st_start[NT];
+            __shared__ int st_k[NT];
+            __shared__ float st_b[NT];
+            __shared__ int s_fill[1];
+            if (tid == 0) s_fill[0] = 0;
+            __syncthreads();
+            // ---- accumulate C_*j = sum_k b_kj A_*k.  Each lane gathers 4 consecutive
+            // (row, val) pairs of a segment with one 16-byte load each (segment starts are
+            // aligned down to 4 elements and the head / tail masked).
+            const int limit = (int)(cap - (cap >> 3));
+            const int64_t bj = a.cb + col;
+            const int64_t q0 = a.bcp[bj], q1 = a.bcp[bj + 1];
+            const int64_t nb = q1 - q0;
+            const int g = group_size_for(nb > 0 ? a.flops[col] / (4 * nb) : 0);
+            const int lane_g = lane & (g - 1);
+            const int grp = tid / g;        // group index in the CTA
+            const int ngrp = NT / g;
+            volatile int *vovf = &s_ovf;
+            for (int64_t c0 = q0; c0 < q1; c0 += NT) {
+                const int cnt = (int)((q1 - c0) < NT ? (q1 - c0) : NT);
+                if (tid < cnt) {
+                    const int k = __ldg(a.brow + c0 + tid);
+                    const int64_t st = __ldg(a.acp + k);
+                    st_start[tid] = st;
+                    st_k[tid] = (int)(__ldg(a.acp + k + 1) - st);  // segment length
+                    st_b[tid] = __ldg(a.bval + c0 + tid);
                 }
-                db = __ldg(a.bval + e0 + lane);
-            }
-            const int ncnt = (int)((q1 - e0) < 32 ? (q1 - e0) : 32);
-            // kItems segments side by side; chunks of 32 rows of each per step
-            for (int eb = 0; eb < ncnt && ok; eb += kItems) {
-                int64_t lo_u[kItems];
-                int len_u[kItems];
-                float b_u[kItems];
-                int maxlen = 0;
-#pragma unroll
-                for (int u = 0; u < kItems; u++) {
-                    const int e = eb + u;
-                    lo_u[u] = __shfl_sync(0xffffffffu, dlo, e & 31);
-                    len_u[u] = __shfl_sync(0xffffffffu, dlen, e & 31);
-                    b_u[u] = __shfl_sync(0xffffffffu, db, e & 31);
-                    if (e >= ncnt) len_u[u] = 0;
-                    maxlen = len_u[u] > maxlen ? len_u[u] : maxlen;
-                }
-                for (int c = 0; c < maxlen && ok; c += 32) {
-                    int rr[kItems];
-                    V vv[kItems];
-                    bool vl[kItems];
-                    const int t = c + lane;
-#pragma unroll
-                    for (int u = 0; u < kItems; u++) {
-                        vl[u] = t < len_u[u];
-                        rr[u] = vl[u] ? __ldg(a.arow + lo_u[u] + t) : -1;
-                        vv[u] = V(0);
-                        if (MODE != kSym && vl[u]) {
-                            const float av = __ldg(a.aval + lo_u[u] + t);
-                            vv[u] = GLOBAL ? (V)av * (V)b_u[u] : (V)(av * b_u[u]);
-                        }
+                __syncthreads();
+                const int wgrp0 = warp * (32 / g);
+                for (int e0 = 0; e0 < cnt && ok; e0 += ngrp) {
+                    if (e0 + wgrp0 >= cnt) break;  // warp-uniform: no work for this warp's groups
+                    if (*vovf) {
+                        ok = false;
+                        break;
                     }
-#pragma unroll
-                    for (int u = 0; u < kItems; u++) {
-                        if (!warp_insert<MODE, V>(wkeys, wvals, scap, vl[u], rr[u], vv[u], fill, limit)) {
+                    const int e = e0 + grp;
+                    int lo = 0, hi = 0;     // valid element window relative to the aligned base
+                    float bkj = 0.f;
+                    const int *rp = a.arow;
+                    const float *vp = a.aval;
+                    if (e < cnt) {
+                        const int64_t t0 = st_start[e];
+                        const int64_t ab = t0 & ~(int64_t)3;
+                        rp = a.arow + ab;
+                        vp = a.aval + ab;
+                        lo = (int)(t0 - ab);
+                        hi = lo + st_k[e];
+                        bkj = st_b[e];
+                    }
+                    const unsigned nstep = (unsigned)((hi + 4 * g - 1) / (4 * g));
+                    const unsigned maxs = __reduce_max_sync(0xffffffffu, nstep);
+                    for (unsigned si = 0; si < maxs; si++) {
+                        const int i0 = 4 * ((int)si * g + lane_g);
+                        int4 r4 = make_int4(-1, -1, -1, -1);
+                        float4 v4 = make_float4(0.f, 0.f, 0.f, 0.f);
+                        if (i0 < hi) {
+                            r4 = __ldg(reinterpret_cast<const int4 *>(rp + i0));
+                            if (MODE != kSym) v4 = __ldg(reinterpret_cast<const float4 *>(vp + i0));
+                        }
+                        const int rr[4] = {r4.x, r4.y, r4.z, r4.w};
+                        V pv[4];
+                        bool vld[4];
+    #pragma unroll
+                        for (int j = 0; j < 4; j++) {
+                            vld[j] = i0 + j >= lo && i0 + j < hi;
+                            pv[j] = GLOBAL ? (V)(&v4.x)[j] * (V)bkj : (V)((&v4.x)[j] * bkj);
+                        }
+                        if (!insert4<MODE, V>(keys, vals, cap, rr, pv, vld, &s_fill[0], limit, fresh)) {
                             ok = false;
-                            break;
+                            *vovf = 1;
+                        }
+                        if (!__all_sync(0xffffffffu, ok)) break;
+                    }
+                    ok = __all_sync(0xffffffffu, ok);
+                }
+                __syncthreads();
+            }
+
+        } else {
+            // ---- accumulate C_*j = sum_k b_kj A_*k: warp `warp` handles rows of its range
+            const uint32_t scap = cap / W;
+            int *wkeys = keys + (size_t)warp * scap;
+            V *wvals = vals + (size_t)warp * scap;
+            const int limit = (int)(scap - (scap >> 3));
+            const int64_t bj = a.cb + col;
+            const int64_t q0 = a.bcp[bj], q1 = a.bcp[bj + 1];
+            int fill = 0;
+            for (int64_t e0 = q0; e0 < q1 && ok; e0 += 32) {
+                // lane l holds the descriptor of segment e0 + l (this warp's sub-segment)
+                int64_t dlo = 0;
+                int dlen = 0;
+                float db = 0.f;
+                if (e0 + lane < q1) {
+                    const int k = __ldg(a.brow + e0 + lane);
+                    const int64_t base = __ldg(a.acp + k);
+                    if (W == 1) {
+                        dlo = base;
+                        dlen = (int)(__ldg(a.acp + k + 1) - base);
+                    } else {
+                        const int *pk = a.rowpart + (int64_t)k * (kParts + 1) + warp * PSTEP;
+                        const int p0 = __ldg(pk), p1 = __ldg(pk + PSTEP);
+                        dlo = base + p0;
+                        dlen = p1 - p0;
+                    }
+                    db = __ldg(a.bval + e0 + lane);
+                }
+                const int ncnt = (int)((q1 - e0) < 32 ? (q1 - e0) : 32);
+                // kItems segments side by side; chunks of 32 rows of each per step
+                for (int eb = 0; eb < ncnt && ok; eb += kItems) {
+                    int64_t lo_u[kItems];
+                    int len_u[kItems];
+                    float b_u[kItems];
+                    int maxlen = 0;
+    #pragma unroll
+                    for (int u = 0; u < kItems; u++) {
+                        const int e = eb + u;
+                        lo_u[u] = __shfl_sync(0xffffffffu, dlo, e & 31);
+                        len_u[u] = __shfl_sync(0xffffffffu, dlen, e & 31);
+                        b_u[u] = __shfl_sync(0xffffffffu, db, e & 31);
+                        if (e >= ncnt) len_u[u] = 0;
+                        maxlen = len_u[u] > maxlen ? len_u[u] : maxlen;
+                    }
+                    for (int c = 0; c < maxlen && ok; c += 32) {
+                        int rr[kItems];
+                        V vv[kItems];
+                        bool vl[kItems];
+                        const int t = c + lane;
+    #pragma unroll
+                        for (int u = 0; u < kItems; u++) {
+                            vl[u] = t < len_u[u];
+                            rr[u] = vl[u] ? __ldg(a.arow + lo_u[u] + t) : -1;
+                            vv[u] = V(0);
+                            if (MODE != kSym && vl[u]) {
+                                const float av = __ldg(a.aval + lo_u[u] + t);
+                                vv[u] = GLOBAL ? (V)av * (V)b_u[u] : (V)(av * b_u[u]);
+                            }
+                        }
+    #pragma unroll
+                        for (int u = 0; u < kItems; u++) {
+                            if (!warp_insert<MODE, V>(wkeys, wvals, scap, vl[u], rr[u], vv[u], fill, limit)) {
+                                ok = false;
+                                break;
+                            }
                         }
                     }
                 }
             }
+            fresh = lane == 0 ? fill : 0;
+
         }
-        const int fresh = lane == 0 ? fill : 0;
         if (!ok && lane == 0) s_ovf = 1;
         __syncthreads();
         if (s_ovf) {
@@ -280,38 +427,45 @@ __global__ void __launch_bounds__(NT, (1024 / NT > 32 ? 32 : 1024 / NT)) k_bin(B
     }
 }
 
-template <int CAP, int NT, int MODE, bool GLOBAL>
+template <int CAP, int NT, int MODE, bool GLOBAL, bool ATOMIC>
 static size_t smem_of() {
     if (GLOBAL) return 0;
     return (size_t)CAP * (MODE == kSym ? 4 : 8);
 }
 
-template <int CAP, int NT, int MODE, bool GLOBAL>
+template <int CAP, int NT, int MODE, bool GLOBAL, bool ATOMIC>
 static int occ_of() {
-    auto fn = k_bin<CAP, NT, MODE, GLOBAL>;
-    size_t sm = smem_of<CAP, NT, MODE, GLOBAL>();
+    auto fn = k_bin<CAP, NT, MODE, GLOBAL, ATOMIC>;
+    size_t sm = smem_of<CAP, NT, MODE, GLOBAL, ATOMIC>();
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     int nb = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, NT, sm);
     return nb;
 }
 
-template <int CAP, int NT, int MODE, bool GLOBAL>
+template <int CAP, int NT, int MODE, bool GLOBAL, bool ATOMIC>
 static cudaError_t launch_of(const BinArgs &a, int grid, cudaStream_t s) {
     ++g_launches;
-    k_bin<CAP, NT, MODE, GLOBAL><<<grid, NT, smem_of<CAP, NT, MODE, GLOBAL>(), s>>>(a);
+    k_bin<CAP, NT, MODE, GLOBAL, ATOMIC><<<grid, NT, smem_of<CAP, NT, MODE, GLOBAL, ATOMIC>(), s>>>(a);
     return cudaGetLastError();
 }
 
 #define MCLX_BIN_SWITCH(MODE, WHAT, ...)                                          \
     switch (bin) {                                                                \
-        case 0: return WHAT<512, 32, MODE, false>(__VA_ARGS__);                   \
-        case 1: return WHAT<1024, 32, MODE, false>(__VA_ARGS__);                  \
-        case 2: return WHAT<2048, 64, MODE, false>(__VA_ARGS__);                  \
-        case 3: return WHAT<4096, 128, MODE, false>(__VA_ARGS__);                 \
-        case 4: return WHAT<8192, 256, MODE, false>(__VA_ARGS__);                 \
-        case 5: return WHAT<16384, 512, MODE, false>(__VA_ARGS__);                \
-        default: return WHAT<0, kGlobalThreads, MODE, true>(__VA_ARGS__);         \
+        case 0: return WHAT<512, 32, MODE, false, false>(__VA_ARGS__);            \
+        case 1: return WHAT<1024, 32, MODE, false, false>(__VA_ARGS__);           \
+        case 2: return WHAT<2048, 64, MODE, false, false>(__VA_ARGS__);           \
+        case 3: return WHAT<4096, 128, MODE, false, false>(__VA_ARGS__);          \
+        case 4: return WHAT<8192, 256, MODE, false, false>(__VA_ARGS__);          \
+        case 5: return WHAT<16384, 512, MODE, false, false>(__VA_ARGS__);         \
+        case 6: return WHAT<0, kGlobalThreads, MODE, true, false>(__VA_ARGS__);   \
+        case 7: return WHAT<512, 64, MODE, false, true>(__VA_ARGS__);             \
+        case 8: return WHAT<1024, 64, MODE, false, true>(__VA_ARGS__);            \
+        case 9: return WHAT<2048, 128, MODE, false, true>(__VA_ARGS__);           \
+        case 10: return WHAT<4096, 256, MODE, false, true>(__VA_ARGS__);          \
+        case 11: return WHAT<8192, 512, MODE, false, true>(__VA_ARGS__);          \
+        case 12: return WHAT<16384, 1024, MODE, false, true>(__VA_ARGS__);        \
+        default: return WHAT<0, kGlobalThreads, MODE, true, true>(__VA_ARGS__);   \
     }
 
 cudaError_t launch_bin(int mode, int bin, const BinArgs &a, int grid, cudaStream_t s) {

@@ -109,15 +109,16 @@ def test_expand_random(seed):
     assert st["nnz_unpruned"] == Cr.nnz
 
 
-@pytest.mark.parametrize("bin_", list(range(7)))
+@pytest.mark.parametrize("bin_", list(range(14)))
 def test_expand_forced_bins(bin_):
-    """Bin invariance (T2): every column forced into bin >= b gives the same product."""
+    """Bin invariance (T2): every column forced into bin >= b (0-6: private row-range
+    slices, 7-13: CTA-shared atomic table) gives the same product."""
     A = synth.random_sparse(700, 700, 0.02, seed=11, empty_cols=0.1)
     p = M.Params(force_bin=bin_)
     Cg, st = M.expand(dev(A), params=p)
     Cr, _ = O.expand(A)
     assert_unpruned_parity(host_mat(Cg), Cr)
-    assert sum(st["bin_cols"][:bin_]) == 0
+    assert sum(st["bin_cols"][:bin_ % 7]) == 0
 
 
 @pytest.mark.parametrize("seed", range(4))
@@ -272,7 +273,7 @@ def test_iterate_c1_second_iteration_all_bins():
     A1 = f32(A1)
     Cr1, _ = O.expand(A1)
     _, info = O.prune_inflate(Cr1, 1e-4, 1100, 1400, 0.9, 2.0)
-    for b in (-1, 3, 5, 6):
+    for b in (-1, 3, 5, 6, 8, 10, 12, 13):
         Ag, st = M.iterate(dev(A1), M.Params(force_bin=b, estimator=2))
         kept_parity(host_mat(Ag), Cr1, info, (1e-4, 1100, 1400, 0.9))
 
