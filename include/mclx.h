@@ -220,6 +220,10 @@ int mcl_merge(mcl_ctx_t ctx, int32_t L, const mcl_csc_t *lists, mcl_csc_t *out);
  * advanced by r0 / c0, n_global kept.  Used to distribute an iterate over the grid. */
 int mcl_block(mcl_ctx_t ctx, const mcl_csc_t *A, int64_t r0, int64_t r1, int64_t c0, int64_t c1,
               mcl_csc_t *out);
+/* Development counters of the SpGEMM kernel (all zero unless libmclx was built with
+ * -DMCLX_PROF): [0] warp insert calls, [1] probe-loop passes, [2] products, [3] accumulate
+ * cycles summed over warps, [4] epilogue cycles summed over CTAs, [5] columns. */
+int mcl_prof_read(uint64_t out[8], int reset);
 /* rank 0 creates the id and shares it (e.g. through torch.distributed) */
 int mcl_nccl_unique_id(unsigned char out[128]);
 /* collective over the pr*pc ranks: creates the world, row and column communicators */

@@ -29,6 +29,16 @@
 
 namespace mclx {
 
+// Development counters (compiled in with -DMCLX_PROF; read with mcl_prof_read):
+// [0] insert calls (warp) [1] probe-loop passes (warp) [2] valid lanes (products)
+// [3] accumulate cycles (per warp, summed) [4] epilogue cycles (per CTA) [5] columns
+__device__ unsigned long long g_prof[8];
+#ifdef MCLX_PROF
+#define PROF_ADD(i, v) atomicAdd(&g_prof[i], (unsigned long long)(v))
+#else
+#define PROF_ADD(i, v) ((void)0)
+#endif
+
 constexpr int kParts = 32;  // row ranges of the rowpart index
 constexpr int kItems = 4;   // sub-segment chunks whose gathers a warp keeps in flight
 
@@ -102,13 +112,14 @@ __device__ __forceinline__ int group_size_for(int64_t avg) {
 // overflow so the column is re-run in a bigger bin.  All 32 lanes must call.
 template <int MODE, typename V>
 __device__ __forceinline__ bool warp_insert(int *keys, V *vals, uint32_t scap, bool valid, int row,
-                                            V v, int &fill, int limit) {
+                                            V v, int &fill, int limit, unsigned &passes) {
     const unsigned FULL = 0xffffffffu;
     uint32_t s = hash_slot(row, scap);
     volatile int *vk = keys;
     int k = valid ? vk[s] : row;
     bool need = k != row;
     while (__any_sync(FULL, need)) {
+        passes++;
         bool claimed = false;
         if (need) {
             if (k == kEmptyKey) {
@@ -265,6 +276,10 @@ __global__ void __launch_bounds__(NT, (1024 / NT > 32 ? 32 : 1024 / NT)) k_bin(B
 
         } else {
             // ---- accumulate C_*j = sum_k b_kj A_*k: warp `warp` handles rows of its range
+            unsigned prof_passes = 0, prof_calls = 0, prof_valid = 0;
+#ifdef MCLX_PROF
+            const long long prof_t0 = clock64();
+#endif
             const uint32_t scap = cap / W;
             int *wkeys = keys + (size_t)warp * scap;
             V *wvals = vals + (size_t)warp * scap;
@@ -324,7 +339,12 @@ __global__ void __launch_bounds__(NT, (1024 / NT > 32 ? 32 : 1024 / NT)) k_bin(B
                         }
     #pragma unroll
                         for (int u = 0; u < kItems; u++) {
-                            if (!warp_insert<MODE, V>(wkeys, wvals, scap, vl[u], rr[u], vv[u], fill, limit)) {
+    #ifdef MCLX_PROF
+                        prof_calls++;
+                        prof_valid += __popc(__ballot_sync(0xffffffffu, vl[u]));
+#endif
+                        if (!warp_insert<MODE, V>(wkeys, wvals, scap, vl[u], rr[u], vv[u], fill, limit,
+                                                  prof_passes)) {
                                 ok = false;
                                 break;
                             }
@@ -333,6 +353,18 @@ __global__ void __launch_bounds__(NT, (1024 / NT > 32 ? 32 : 1024 / NT)) k_bin(B
                 }
             }
             fresh = lane == 0 ? fill : 0;
+#ifdef MCLX_PROF
+            if (lane == 0) {
+                PROF_ADD(0, prof_calls);
+                PROF_ADD(1, prof_passes);
+                PROF_ADD(2, prof_valid);
+                PROF_ADD(3, clock64() - prof_t0);
+            }
+#else
+            (void)prof_passes;
+            (void)prof_calls;
+            (void)prof_valid;
+#endif
 
         }
         if (!ok && lane == 0) s_ovf = 1;
@@ -349,6 +381,10 @@ __global__ void __launch_bounds__(NT, (1024 / NT > 32 ? 32 : 1024 / NT)) k_bin(B
             continue;
         }
 
+#ifdef MCLX_PROF
+        const long long prof_e0 = clock64();
+        if (tid == 0) PROF_ADD(5, 1);
+#endif
         // ---- compact occupied slots to the front of the table
         const int nnz = compact_inplace<NT, V>(
             keys, vals, (int)cap, [](int k, V) { return k != kEmptyKey; }, sscan);
@@ -422,8 +458,19 @@ __global__ void __launch_bounds__(NT, (1024 / NT > 32 ? 32 : 1024 / NT)) k_bin(B
             a.chaos[col] = chaos;
             atomicAdd(a.bin_out, (unsigned long long)kept);
             atomic_max_nonneg_float(a.chaos_max, chaos);
+#ifdef MCLX_PROF
+            PROF_ADD(4, clock64() - prof_e0);
+#endif
         }
         __syncthreads();
+    }
+}
+
+void prof_read(unsigned long long out[8], int reset) {
+    cudaMemcpyFromSymbol(out, g_prof, sizeof(unsigned long long) * 8);
+    if (reset) {
+        unsigned long long z[8] = {};
+        cudaMemcpyToSymbol(g_prof, z, sizeof z);
     }
 }
 
