@@ -178,6 +178,72 @@ __device__ void sort_write(int *keys, V *vals, int K, int cap, int32_t *out_row,
     }
     lo = -block_max<NT, int>(-lo, sh);
     hi = block_max<NT, int>(hi, sh);
+    {
+        // Fast path: build the sorted column in the table's free space -- keys[K, 2K) and
+        // vals[K, 2K) (as float) for the output, counters at keys[2K, 2K + nbk) -- with
+        // insertion sorts inside the (tiny) buckets, then one coalesced copy out.
+        int nbk = 1;
+        while (nbk * 4 <= K) nbk *= 2;
+        if (2 * K + nbk <= cap) {
+            int *okey = keys + K;
+            float *oval = reinterpret_cast<float *>(vals + K);
+            int *cnt = keys + 2 * K;
+            for (int i = threadIdx.x; i < nbk; i += NT) cnt[i] = 0;
+            __syncthreads();
+            const uint64_t range = (uint64_t)(hi - lo) + 1;
+            for (int i = threadIdx.x; i < K; i += NT)
+                atomicAdd(&cnt[(int)(((uint64_t)(keys[i] - lo) * nbk) / range)], 1);
+            __syncthreads();
+            const int per = (nbk + NT - 1) / NT;
+            const int b0 = threadIdx.x * per;
+            int loc = 0, mx = 0;
+            for (int b = b0; b < b0 + per && b < nbk; b++) {
+                loc += cnt[b];
+                mx = cnt[b] > mx ? cnt[b] : mx;
+            }
+            int tot;
+            int off = block_excl_scan<NT>(loc, sh, tot);
+            mx = block_max<NT, int>(mx, sh);
+            if (mx <= 48) {
+                for (int b = b0; b < b0 + per && b < nbk; b++) {
+                    const int c = cnt[b];
+                    cnt[b] = off;
+                    off += c;
+                }
+                __syncthreads();
+                for (int i = threadIdx.x; i < K; i += NT) {
+                    const int r = keys[i];
+                    const int pos = atomicAdd(&cnt[(int)(((uint64_t)(r - lo) * nbk) / range)], 1);
+                    okey[pos] = r;
+                    oval[pos] = xf(vals[i]);
+                }
+                __syncthreads();
+                for (int b = threadIdx.x; b < nbk; b += NT) {
+                    const int start = b ? cnt[b - 1] : 0, end = cnt[b];
+                    for (int i = start + 1; i < end; i++) {
+                        const int r = okey[i];
+                        const float v = oval[i];
+                        int j = i - 1;
+                        while (j >= start && okey[j] > r) {
+                            okey[j + 1] = okey[j];
+                            oval[j + 1] = oval[j];
+                            j--;
+                        }
+                        okey[j + 1] = r;
+                        oval[j + 1] = v;
+                    }
+                }
+                __syncthreads();
+                for (int i = threadIdx.x; i < K; i += NT) {
+                    out_row[i] = okey[i];
+                    out_val[i] = oval[i];
+                }
+                __syncthreads();
+                return;
+            }
+            __syncthreads();
+        }
+    }
     int free_slots = cap - K;
     int nbk = 1;
     while (nbk * 2 <= free_slots && nbk * 4 <= K) nbk *= 2;
