@@ -222,8 +222,10 @@ int mcl_block(mcl_ctx_t ctx, const mcl_csc_t *A, int64_t r0, int64_t r1, int64_t
               mcl_csc_t *out);
 /* Development counters of the SpGEMM kernel (all zero unless libmclx was built with
  * -DMCLX_PROF): [0] warp insert calls, [1] probe-loop passes, [2] products, [3] accumulate
- * cycles summed over warps, [4] epilogue cycles summed over CTAs, [5] columns. */
-int mcl_prof_read(uint64_t out[8], int reset);
+ * cycles summed over warps, [4] epilogue cycles summed over CTAs, [5] columns, epilogue
+ * phases: [6] table compaction, [7] stats + select + kept compaction, [8] sums, [9] sort
+ * and write; [10], [11] reserved. */
+int mcl_prof_read(uint64_t out[12], int reset);
 /* rank 0 creates the id and shares it (e.g. through torch.distributed) */
 int mcl_nccl_unique_id(unsigned char out[128]);
 /* collective over the pr*pc ranks: creates the world, row and column communicators */

@@ -109,7 +109,7 @@ _sig = {
     "mcl_clusters": ([_P, C.POINTER(CscT), _P, C.POINTER(_i64)], C.c_int),
     "mcl_merge": ([_P, C.c_int32, C.POINTER(CscT), C.POINTER(CscT)], C.c_int),
     "mcl_block": ([_P, C.POINTER(CscT), _i64, _i64, _i64, _i64, C.POINTER(CscT)], C.c_int),
-    "mcl_prof_read": ([C.POINTER(C.c_uint64 * 8), C.c_int], C.c_int),
+    "mcl_prof_read": ([C.POINTER(C.c_uint64 * 12), C.c_int], C.c_int),
     "mcl_nccl_unique_id": ([C.c_char * 128], C.c_int),
     "mcl_ctx_set_grid": ([_P, C.c_int, C.c_int, C.c_int, C.c_char * 128], C.c_int),
     "mcl_summa_iterate": ([_P, C.POINTER(CscT), C.POINTER(ParamsT), C.POINTER(CscT),
@@ -449,7 +449,7 @@ def merge(lists):
 
 def prof_read(reset: bool = True):
     """Development counters of the SpGEMM kernel (zeros unless built with -DMCLX_PROF)."""
-    v = (C.c_uint64 * 8)()
+    v = (C.c_uint64 * 12)()
     _lib.mcl_prof_read(C.byref(v), int(reset))
     return list(v)
 

@@ -1179,11 +1179,11 @@ int mcl_block(mcl_ctx_t c, const mcl_csc_t *A, int64_t r0, int64_t r1, int64_t c
     return MCL_OK;
 }
 
-int mcl_prof_read(uint64_t out[8], int reset) {
+int mcl_prof_read(uint64_t out[12], int reset) {
     if (!out) return MCL_ERR_INVALID_ARG;
-    unsigned long long v[8];
+    unsigned long long v[12];
     prof_read(v, reset);
-    for (int i = 0; i < 8; i++) out[i] = v[i];
+    for (int i = 0; i < 12; i++) out[i] = v[i];
     return MCL_OK;
 }
 

@@ -75,7 +75,7 @@ constexpr int kShortSegment = 16;  // flops_j / nnz(B_*j) below this -> atomic f
 cudaError_t launch_bin(int mode, int bin, const BinArgs &a, int grid, cudaStream_t s);
 // Max resident CTAs per SM for (mode, bin); also sets the dynamic smem attribute.
 int bin_occupancy(int mode, int bin);
-void prof_read(unsigned long long out[8], int reset);  // development counters (-DMCLX_PROF)
+void prof_read(unsigned long long out[12], int reset);  // development counters (-DMCLX_PROF)
 size_t bin_smem_bytes(int mode, int bin);
 
 // rowpart[k][i] = first position in A_*k whose row >= ceil(i*m/32), i = 0..32

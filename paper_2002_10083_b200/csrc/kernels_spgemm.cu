@@ -32,7 +32,7 @@ namespace mclx {
 // Development counters (compiled in with -DMCLX_PROF; read with mcl_prof_read):
 // [0] insert calls (warp) [1] probe-loop passes (warp) [2] valid lanes (products)
 // [3] accumulate cycles (per warp, summed) [4] epilogue cycles (per CTA) [5] columns
-__device__ unsigned long long g_prof[8];
+__device__ unsigned long long g_prof[12];
 #ifdef MCLX_PROF
 #define PROF_ADD(i, v) atomicAdd(&g_prof[i], (unsigned long long)(v))
 #else
@@ -154,6 +154,8 @@ __global__ void __launch_bounds__(NT, (1024 / NT > 32 ? 32 : 1024 / NT)) k_bin(B
     __shared__ double sred[NT / 32];
     __shared__ int sscan[NT / 32];
     __shared__ int s_col, s_idx, s_ovf;
+    __shared__ int swi[2][NT / 32];
+    __shared__ double swd[4][NT / 32];
     constexpr int W = NT / 32;         // warps = row-range owners
     constexpr int PSTEP = kParts / W;  // rowpart boundaries per warp
 
@@ -385,91 +387,239 @@ __global__ void __launch_bounds__(NT, (1024 / NT > 32 ? 32 : 1024 / NT)) k_bin(B
         const long long prof_e0 = clock64();
         if (tid == 0) PROF_ADD(5, 1);
 #endif
-        // ---- compact occupied slots to the front of the table
-        const int nnz = compact_inplace<NT, V>(
-            keys, vals, (int)cap, [](int k, V) { return k != kEmptyKey; }, sscan);
-
-        if (MODE == kNum) {
-            const int64_t dst = a.c_cp[col];
-            if (tid == 0 && a.c_cp[col + 1] - dst != nnz) atomicExch(a.err_flag, 1);
-            sort_write<NT, V>(keys, vals, nnz, (int)cap, a.c_row + dst, a.c_val + dst,
-                              [](V v) { return (float)v; }, sscan);
-            continue;
-        }
-
-        // ---- kFused: threshold statistics (Q3, Q4)
-        const PruneParams &pp = a.pp;
-        int mloc = 0;
-        double sloc = 0.0;
-        for (int i = tid; i < nnz; i += NT) {
-            double v = (double)vals[i];
-            if (v >= pp.theta) {
-                mloc++;
-                sloc += v;
+        if constexpr (!ATOMIC) {
+            // ---- warp-local epilogue: warp `warp` owns slice [warp*scap, +scap) and an
+            // ordered row range, so it compacts, selects its part of the kept set, sorts it
+            // and writes it at its offset; only the branch decision, the radix-select
+            // histograms and the sums are CTA-wide.
+            const uint32_t scap = cap / W;
+            int *wk = keys + (size_t)warp * scap;
+            V *wv = vals + (size_t)warp * scap;
+            const int cnt_w = warp_compact<V>(wk, wv, (int)scap,
+                                              [](int k, V) { return k != kEmptyKey; });
+#ifdef MCLX_PROF
+            if (tid == 0) PROF_ADD(6, clock64() - prof_e0);  // compaction of the slices
+            const long long prof_e1 = clock64();
+#endif
+            if (MODE == kNum) {
+                if (lane == 0) swi[0][warp] = cnt_w;
+                __syncthreads();
+                int off = 0, tot = 0;
+                for (int w2 = 0; w2 < W; w2++) {
+                    off += w2 < warp ? swi[0][w2] : 0;
+                    tot += swi[0][w2];
+                }
+                const int64_t dst = a.c_cp[col];
+                if (tid == 0 && a.c_cp[col + 1] - dst != tot) atomicExch(a.err_flag, 1);
+                warp_sort_write<V>(wk, wv, cnt_w, (int)scap, a.c_row + dst + off,
+                                   a.c_val + dst + off, [](V v) { return (float)v; });
+                __syncthreads();
+                continue;
             }
-        }
-        const int m = block_sum<NT, int>(mloc, sscan);
-        const double s = block_sum<NT, double>(sloc, sred);
-        int64_t K;
-        const int br = prune_branch(pp, nnz, m, s, K);
-        uint32_t t = 0;
-        int rowcut = 0;
-        int sel = 0;  // 0: v >= theta, 1: top-K, 2: all
-        if (br == 0) {
-            sel = 0;
-        } else if (K >= nnz) {
-            sel = 2;
-        } else {
-            radix_select_topk<NT, V>(keys, vals, nnz, (int)K, t, rowcut, hist, sint);
-            sel = 1;
-        }
-        const double theta = pp.theta;
-        const int kept = compact_inplace<NT, V>(
-            keys, vals, nnz,
-            [=](int k, V v) {
+            const PruneParams &pp = a.pp;
+            int mloc = 0;
+            double sloc = 0.0;
+            for (int i = lane; i < cnt_w; i += 32) {
+                const double v = (double)wv[i];
+                if (v >= pp.theta) {
+                    mloc++;
+                    sloc += v;
+                }
+            }
+            mloc = warp_sum(mloc);
+            sloc = warp_sum(sloc);
+            if (lane == 0) {
+                swi[0][warp] = cnt_w;
+                swi[1][warp] = mloc;
+                swd[0][warp] = sloc;
+            }
+            __syncthreads();
+            int nnz = 0, m = 0;
+            double sm = 0.0;
+            for (int w2 = 0; w2 < W; w2++) {
+                nnz += swi[0][w2];
+                m += swi[1][w2];
+                sm += swd[0][w2];
+            }
+            int64_t K;
+            const int br = prune_branch(pp, nnz, m, sm, K);
+            uint32_t t = 0;
+            int rowcut = 0;
+            int sel = 0;  // 0: v >= theta, 1: top-K, 2: all
+            if (br == 0) {
+                sel = 0;
+            } else if (K >= nnz) {
+                sel = 2;
+            } else {
+                radix_select_topk_seg<NT, V>(wk, wv, cnt_w, (int)K, t, rowcut, hist, sint);
+                sel = 1;
+            }
+            const double theta = pp.theta;
+            const int kept_w = warp_compact<V>(wk, wv, cnt_w, [=](int k, V v) {
                 if (sel == 0) return (double)v >= theta;
                 if (sel == 2) return true;
-                uint32_t b = val_bits(v);
-                return b > t || (b == t && k <= rowcut);
-            },
-            sscan);
-        if (tid == 0 && kept != (int)K) atomicExch(a.err_flag, 2);
-
-        // ---- renormalise, chaos (Q9), inflate, renormalise (Q1)
-        double sv = 0.0, mx = 0.0, sq = 0.0, sr = 0.0;
-        for (int i = tid; i < kept; i += NT) {
-            double v = (double)vals[i];
-            sv += v;
-            mx = v > mx ? v : mx;
-            sq += v * v;
-            sr += pow_r(v, pp);
-        }
-        sv = block_sum<NT, double>(sv, sred);
-        mx = block_max<NT, double>(mx, sred);
-        sq = block_sum<NT, double>(sq, sred);
-        sr = block_sum<NT, double>(sr, sred);
-        const float chaos = kept > 0 ? (float)((double)kept * (mx / sv - sq / (sv * sv))) : 0.0f;
-
-        const int64_t dst = a.soff[col];
-        sort_write<NT, V>(keys, vals, kept, (int)cap, a.s_row + dst, a.s_val + dst,
-                          [&](V v) { return (float)(pow_r((double)v, pp) / sr); }, sscan);
-        if (tid == 0) {
-            a.s_cnt[col] = kept;
-            a.chaos[col] = chaos;
-            atomicAdd(a.bin_out, (unsigned long long)kept);
-            atomic_max_nonneg_float(a.chaos_max, chaos);
+                const uint32_t bb = val_bits(v);
+                return bb > t || (bb == t && k <= rowcut);
+            });
 #ifdef MCLX_PROF
-            PROF_ADD(4, clock64() - prof_e0);
+            if (tid == 0) PROF_ADD(7, clock64() - prof_e1);  // stats + select + kept
+            const long long prof_e2 = clock64();
 #endif
+            double sv = 0.0, mx = 0.0, sq = 0.0, sr = 0.0;
+            for (int i = lane; i < kept_w; i += 32) {
+                const double v = (double)wv[i];
+                sv += v;
+                mx = v > mx ? v : mx;
+                sq += v * v;
+                sr += pow_r(v, pp);
+            }
+            sv = warp_sum(sv);
+            mx = warp_max(mx);
+            sq = warp_sum(sq);
+            sr = warp_sum(sr);
+            __syncthreads();  // swi / swd reuse
+            if (lane == 0) {
+                swi[0][warp] = kept_w;
+                swd[0][warp] = sv;
+                swd[1][warp] = mx;
+                swd[2][warp] = sq;
+                swd[3][warp] = sr;
+            }
+            __syncthreads();
+            int off = 0, kept = 0;
+            sv = 0.0;
+            mx = 0.0;
+            sq = 0.0;
+            sr = 0.0;
+            for (int w2 = 0; w2 < W; w2++) {
+                off += w2 < warp ? swi[0][w2] : 0;
+                kept += swi[0][w2];
+                sv += swd[0][w2];
+                mx = swd[1][w2] > mx ? swd[1][w2] : mx;
+                sq += swd[2][w2];
+                sr += swd[3][w2];
+            }
+            if (tid == 0 && kept != (int)K) atomicExch(a.err_flag, 2);
+            const float chaos =
+                kept > 0 ? (float)((double)kept * (mx / sv - sq / (sv * sv))) : 0.0f;
+            const int64_t dst = a.soff[col] + off;
+#ifdef MCLX_PROF
+            if (tid == 0) PROF_ADD(8, clock64() - prof_e2);  // sums
+            const long long prof_e3 = clock64();
+#endif
+            warp_sort_write<V>(wk, wv, kept_w, (int)scap, a.s_row + dst, a.s_val + dst,
+                               [&](V v) { return (float)(pow_r((double)v, pp) / sr); });
+            if (tid == 0) {
+                a.s_cnt[col] = kept;
+                a.chaos[col] = chaos;
+                atomicAdd(a.bin_out, (unsigned long long)kept);
+                atomic_max_nonneg_float(a.chaos_max, chaos);
+#ifdef MCLX_PROF
+                PROF_ADD(4, clock64() - prof_e0);
+                PROF_ADD(9, clock64() - prof_e3);  // sort + write
+#endif
+            }
+            __syncthreads();
+        } else {
+            // ---- compact occupied slots to the front of the table
+            const int nnz = compact_inplace<NT, V>(
+                keys, vals, (int)cap, [](int k, V) { return k != kEmptyKey; }, sscan);
+
+            if (MODE == kNum) {
+                const int64_t dst = a.c_cp[col];
+                if (tid == 0 && a.c_cp[col + 1] - dst != nnz) atomicExch(a.err_flag, 1);
+                sort_write<NT, V>(keys, vals, nnz, (int)cap, a.c_row + dst, a.c_val + dst,
+                                  [](V v) { return (float)v; }, sscan);
+                continue;
+            }
+
+    #ifdef MCLX_PROF
+            if (tid == 0) PROF_ADD(6, clock64() - prof_e0);  // compaction of the table
+            const long long prof_e1 = clock64();
+    #endif
+            // ---- kFused: threshold statistics (Q3, Q4)
+            const PruneParams &pp = a.pp;
+            int mloc = 0;
+            double sloc = 0.0;
+            for (int i = tid; i < nnz; i += NT) {
+                double v = (double)vals[i];
+                if (v >= pp.theta) {
+                    mloc++;
+                    sloc += v;
+                }
+            }
+            const int m = block_sum<NT, int>(mloc, sscan);
+            const double s = block_sum<NT, double>(sloc, sred);
+            int64_t K;
+            const int br = prune_branch(pp, nnz, m, s, K);
+            uint32_t t = 0;
+            int rowcut = 0;
+            int sel = 0;  // 0: v >= theta, 1: top-K, 2: all
+            if (br == 0) {
+                sel = 0;
+            } else if (K >= nnz) {
+                sel = 2;
+            } else {
+                radix_select_topk<NT, V>(keys, vals, nnz, (int)K, t, rowcut, hist, sint);
+                sel = 1;
+            }
+            const double theta = pp.theta;
+            const int kept = compact_inplace<NT, V>(
+                keys, vals, nnz,
+                [=](int k, V v) {
+                    if (sel == 0) return (double)v >= theta;
+                    if (sel == 2) return true;
+                    uint32_t b = val_bits(v);
+                    return b > t || (b == t && k <= rowcut);
+                },
+                sscan);
+            if (tid == 0 && kept != (int)K) atomicExch(a.err_flag, 2);
+
+    #ifdef MCLX_PROF
+            if (tid == 0) PROF_ADD(7, clock64() - prof_e1);  // stats + select + kept compaction
+            const long long prof_e2 = clock64();
+    #endif
+            // ---- renormalise, chaos (Q9), inflate, renormalise (Q1)
+            double sv = 0.0, mx = 0.0, sq = 0.0, sr = 0.0;
+            for (int i = tid; i < kept; i += NT) {
+                double v = (double)vals[i];
+                sv += v;
+                mx = v > mx ? v : mx;
+                sq += v * v;
+                sr += pow_r(v, pp);
+            }
+            sv = block_sum<NT, double>(sv, sred);
+            mx = block_max<NT, double>(mx, sred);
+            sq = block_sum<NT, double>(sq, sred);
+            sr = block_sum<NT, double>(sr, sred);
+            const float chaos = kept > 0 ? (float)((double)kept * (mx / sv - sq / (sv * sv))) : 0.0f;
+
+            const int64_t dst = a.soff[col];
+    #ifdef MCLX_PROF
+            if (tid == 0) PROF_ADD(8, clock64() - prof_e2);  // sums
+            const long long prof_e3 = clock64();
+    #endif
+            sort_write<NT, V>(keys, vals, kept, (int)cap, a.s_row + dst, a.s_val + dst,
+                              [&](V v) { return (float)(pow_r((double)v, pp) / sr); }, sscan);
+            if (tid == 0) {
+                a.s_cnt[col] = kept;
+                a.chaos[col] = chaos;
+                atomicAdd(a.bin_out, (unsigned long long)kept);
+                atomic_max_nonneg_float(a.chaos_max, chaos);
+    #ifdef MCLX_PROF
+                PROF_ADD(4, clock64() - prof_e0);
+                PROF_ADD(9, clock64() - prof_e3);  // sort + write
+    #endif
+            }
+            __syncthreads();
         }
-        __syncthreads();
     }
 }
 
-void prof_read(unsigned long long out[8], int reset) {
-    cudaMemcpyFromSymbol(out, g_prof, sizeof(unsigned long long) * 8);
+void prof_read(unsigned long long out[12], int reset) {
+    cudaMemcpyFromSymbol(out, g_prof, sizeof(unsigned long long) * 12);
     if (reset) {
-        unsigned long long z[8] = {};
+        unsigned long long z[12] = {};
         cudaMemcpyToSymbol(g_prof, z, sizeof z);
     }
 }

@@ -313,6 +313,158 @@ __device__ void sort_write(int *keys, V *vals, int K, int cap, int32_t *out_row,
     __syncthreads();
 }
 
+// ------------------------------------------------------------------ warp-scoped helpers
+// (the private-slice kernel family: each warp owns a slice of the table and an ordered
+// row range, so the epilogue works slice by slice with warp ballots instead of CTA scans)
+
+// In-place, order-preserving compaction of (keys, vals)[0, len) by keep(key, val) within
+// one warp (chunks of 32 read before written; writes land at or below the chunk).
+template <typename V, class Pred>
+__device__ __forceinline__ int warp_compact(int *keys, V *vals, int len, Pred keep) {
+    const int lane = lane_id();
+    const unsigned lt = (1u << lane) - 1u;
+    int base = 0;
+    for (int c = 0; c < len; c += 32) {
+        const int i = c + lane;
+        int k = 0;
+        V v = V(0);
+        bool f = false;
+        if (i < len) {
+            k = keys[i];
+            v = vals[i];
+            f = keep(k, v);
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, f);
+        __syncwarp();
+        if (f) {
+            keys[base + __popc(bal & lt)] = k;
+            vals[base + __popc(bal & lt)] = v;
+        }
+        base += __popc(bal);
+        __syncwarp();
+    }
+    return base;
+}
+
+// Warp-level bitonic sort of (keys, vals)[0, P), P a power of two, padded by the caller.
+template <typename V>
+__device__ void warp_bitonic_sort(int *keys, V *vals, int P) {
+    for (int k = 2; k <= P; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = lane_id(); i < P; i += 32) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const int a = keys[i], b = keys[ixj];
+                    if ((a > b) == ((i & k) == 0)) {
+                        keys[i] = b;
+                        keys[ixj] = a;
+                        const V t = vals[i];
+                        vals[i] = vals[ixj];
+                        vals[ixj] = t;
+                    }
+                }
+            }
+            __syncwarp();
+        }
+    }
+}
+
+// Sort the K entries of one warp's slice (keys, vals)[0, K) by row and write them, mapped
+// by xf, to out_row / out_val[0, K): interpolation bucket sort in the slice's free space
+// (keys/vals[K, 2K) for the output, counters at keys[2K, 2K + nbk)), else an in-place
+// bitonic sort (slice length scap a power of two >= K).
+template <typename V, class XF>
+__device__ void warp_sort_write(int *keys, V *vals, int K, int scap, int32_t *out_row,
+                                float *out_val, XF xf) {
+    if (K <= 0) return;
+    const int lane = lane_id();
+    int lo = 0x7fffffff, hi = 0;
+    for (int i = lane; i < K; i += 32) {
+        const int r = keys[i];
+        lo = r < lo ? r : lo;
+        hi = r > hi ? r : hi;
+    }
+    lo = warp_min(lo);
+    hi = warp_max(hi);
+    int nbk = 1;
+    while (nbk * 4 <= K) nbk *= 2;
+    if (2 * K + nbk <= scap) {
+        int *okey = keys + K;
+        float *oval = reinterpret_cast<float *>(vals + K);
+        int *cnt = keys + 2 * K;
+        for (int i = lane; i < nbk; i += 32) cnt[i] = 0;
+        __syncwarp();
+        const uint64_t range = (uint64_t)(hi - lo) + 1;
+        for (int i = lane; i < K; i += 32)
+            atomicAdd(&cnt[(int)(((uint64_t)(keys[i] - lo) * nbk) / range)], 1);
+        __syncwarp();
+        // exclusive scan of the counters, 32 contiguous chunks
+        const int per = (nbk + 31) / 32;
+        const int b0 = lane * per;
+        int loc = 0, mx = 0;
+        for (int b = b0; b < b0 + per && b < nbk; b++) {
+            loc += cnt[b];
+            mx = cnt[b] > mx ? cnt[b] : mx;
+        }
+        int inc = loc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        mx = warp_max(mx);
+        if (mx <= 48) {
+            int off = inc - loc;
+            for (int b = b0; b < b0 + per && b < nbk; b++) {
+                const int c = cnt[b];
+                cnt[b] = off;
+                off += c;
+            }
+            __syncwarp();
+            for (int i = lane; i < K; i += 32) {
+                const int r = keys[i];
+                const int pos = atomicAdd(&cnt[(int)(((uint64_t)(r - lo) * nbk) / range)], 1);
+                okey[pos] = r;
+                oval[pos] = xf(vals[i]);
+            }
+            __syncwarp();
+            for (int b = lane; b < nbk; b += 32) {
+                const int start = b ? cnt[b - 1] : 0, end = cnt[b];
+                for (int i = start + 1; i < end; i++) {
+                    const int r = okey[i];
+                    const float v = oval[i];
+                    int j = i - 1;
+                    while (j >= start && okey[j] > r) {
+                        okey[j + 1] = okey[j];
+                        oval[j + 1] = oval[j];
+                        j--;
+                    }
+                    okey[j + 1] = r;
+                    oval[j + 1] = v;
+                }
+            }
+            __syncwarp();
+            for (int i = lane; i < K; i += 32) {
+                out_row[i] = okey[i];
+                out_val[i] = oval[i];
+            }
+            __syncwarp();
+            return;
+        }
+        __syncwarp();
+    }
+    int P = 1;
+    while (P < K) P <<= 1;
+    for (int i = K + lane; i < P; i += 32) keys[i] = kPadKey;
+    __syncwarp();
+    warp_bitonic_sort<V>(keys, vals, P);
+    for (int i = lane; i < K; i += 32) {
+        out_row[i] = keys[i];
+        out_val[i] = xf(vals[i]);
+    }
+    __syncwarp();
+}
+
 // Warp 0 only: find the digit d of a 256-bin histogram at which the running count
 // (from the top digit when DESC, from digit 0 otherwise) first reaches `rem`.
 // out[0] = d, out[1] = count strictly before d in that order, out[2] = hist[d].
@@ -387,6 +539,56 @@ __device__ void radix_select_topk(const int *keys, const V *vals, int n, int K, 
         for (int i = threadIdx.x; i < n; i += NT) {
             uint32_t b = val_bits(vals[i]);
             uint32_t k = (uint32_t)keys[i];
+            if (b == t && (k & rm) == rp) atomicAdd(&hist[(k >> shift) & 255u], 1u);
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) find_digit<false>(hist, rem, sint);
+        __syncthreads();
+        rp |= (uint32_t)sint[0] << shift;
+        rm |= 0xFFu << shift;
+        rem -= sint[1];
+        __syncthreads();
+    }
+    rowcut = (int)rp;
+}
+
+// radix_select_topk over W per-warp segments: warp w's entries are (keys, vals)[0, n) of
+// its own slice (pointers and n differ per warp); the histograms are CTA-wide.
+template <int NT, typename V>
+__device__ void radix_select_topk_seg(const int *keys, const V *vals, int n, int K, uint32_t &t,
+                                      int &rowcut, unsigned *hist, int *sint) {
+    const int lane = lane_id();
+    uint32_t prefix = 0, mask = 0;
+    int rem = K, eq = 0;
+    for (int shift = 24; shift >= 0; shift -= 8) {
+        for (int i = threadIdx.x; i < 256; i += NT) hist[i] = 0;
+        __syncthreads();
+        for (int i = lane; i < n; i += 32) {
+            const uint32_t b = val_bits(vals[i]);
+            if ((b & mask) == prefix) atomicAdd(&hist[(b >> shift) & 255u], 1u);
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) find_digit<true>(hist, rem, sint);
+        __syncthreads();
+        const uint32_t d = (uint32_t)sint[0];
+        rem -= sint[1];
+        eq = sint[2];
+        prefix |= d << shift;
+        mask |= 0xFFu << shift;
+        __syncthreads();
+    }
+    t = prefix;
+    if (rem == eq) {
+        rowcut = 0x7fffffff;
+        return;
+    }
+    uint32_t rp = 0, rm = 0;
+    for (int shift = 24; shift >= 0; shift -= 8) {
+        for (int i = threadIdx.x; i < 256; i += NT) hist[i] = 0;
+        __syncthreads();
+        for (int i = lane; i < n; i += 32) {
+            const uint32_t b = val_bits(vals[i]);
+            const uint32_t k = (uint32_t)keys[i];
             if (b == t && (k & rm) == rp) atomicAdd(&hist[(k >> shift) & 255u], 1u);
         }
         __syncthreads();

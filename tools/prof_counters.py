@@ -16,11 +16,13 @@ ctx = M.context()
 A = ctx.preprocess(M.CSC.from_host(G))
 out, st = ctx.iterate(A, M.Params())
 M.prof_read(reset=True)
-for fb in [-1, 0, 1, 2, 3, 4, 5]:
+for fb in [int(x) for x in (sys.argv[2].split(",") if len(sys.argv) > 2 else ["-1", "2", "4"])]:
     out, st = ctx.iterate(A, M.Params(force_bin=fb))
     torch.cuda.synchronize()
     v = M.prof_read(reset=True)
     calls, passes, prods, acyc, ecyc, cols = v[:6]
+    cc = max(cols, 1)
     print(f"force_bin={fb:2d} ms={st['ms'][3]:7.2f} calls={calls} passes/call={passes/max(calls,1):.2f} "
           f"products/call={prods/max(calls,1):.1f} acc_cycles/product/warp={acyc/max(prods,1):.1f} "
-          f"epi_cycles/col={ecyc/max(cols,1):.0f} cols={cols} bins={st['bin_cols']}")
+          f"epi_cycles/col={ecyc/cc:.0f} [compact {v[6]/cc:.0f} select {v[7]/cc:.0f} sums {v[8]/cc:.0f} "
+          f"sort+write {v[9]/cc:.0f}] cols={cols} bins={st['bin_cols']}")
