@@ -45,6 +45,7 @@ struct mcl_ctx {
     int64_t gbin_budget = (int64_t)32 << 30;  // bytes of fp64 global-bin tables live at once
     float alpha = 1.2f;     // table sizing: need = alpha * Cohen estimate + 16
     float max_load = 0.5f;  // bin when need <= max_load * cap
+    bool order_lists = true;  // MinHash locality order of the bin work lists
 };
 
 namespace {
@@ -232,11 +233,28 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
     RC(scratch_t(c, "rowpart", (size_t)std::max<int64_t>(pr.A->ncols, 1) * 33, &rowpart));
     CK(launch_rowpart(pr.A->ncols, pr.A->col_ptr, pr.A->row_idx, pr.A->nrows, rowpart, c->stream));
     base.rowpart = rowpart;
+    // locality order of the work lists (MCLX_ORDER=0 turns it off)
+    int32_t *colbin = nullptr;
+    uint32_t *okey = nullptr;
+    int64_t *ohist = nullptr, *ooffs = nullptr;
+    void *otmp = nullptr;
+    if (c->order_lists) {
+        const int64_t nbk = (int64_t)kAllBins << kOrderBits;
+        RC(scratch_t(c, "colbin", (size_t)std::max<int64_t>(n, 1), &colbin));
+        RC(scratch_t(c, "order_key", (size_t)std::max<int64_t>(n, 1), &okey));
+        RC(scratch_t(c, "order_hist", (size_t)nbk, &ohist));
+        RC(scratch_t(c, "order_offs", (size_t)nbk + 1, &ooffs));
+        RC(scratch(c, "order_scan_tmp", scan_tmp_bytes(nbk), &otmp));
+        CK(launch_minhash_key(n, pr.B->col_ptr, pr.B->row_idx, pr.cb, okey, c->stream));
+    }
 
 
     // Rounds: 0 sizes by the caller's estimate / exact sizes; 1 re-runs overflowed
     // columns with 4x the estimate; 2 with the exact upper bound min(f_j, m), which
-    // cannot overflow (load <= 1/2 < the 7/8 fill limit).
+    // cannot overflow (load <= 1/2 < the 7/8 fill limit).  Retried columns run in the
+    // CTA-shared-table family: a private-family column can also overflow when its output
+    // rows crowd into one warp's row range (inputs whose labels carry locality), and a
+    // shared table has no such skew.
     int64_t ncls = n;
     const int32_t *cls_list = nullptr;
     const int nrounds = 3;
@@ -256,14 +274,18 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
         ca.alpha = round == 0 ? c->alpha : 4.0f * c->alpha;
         ca.max_load = round == 2 ? 0.5f : c->max_load;
         ca.force_bin = force_bin < 0 ? -1 : force_bin % kFamily;
-        ca.force_family = force_bin < 0 ? -1 : force_bin / kFamily;
+        ca.force_family = force_bin >= 0 ? force_bin / kFamily : round > 0 ? 1 : -1;
         ca.list_stride = std::max<int64_t>(n, 1);
         ca.bin_count = counts;
         ca.lists = lists;
         ca.gcap_col = gcap_col;
         ca.bin_flops = bflops;
         ca.bin_nnzb = bnnzb;
+        ca.colbin = colbin;
         CK(launch_classify(ca, c->stream));
+        if (colbin)
+            CK(launch_order_lists(ncls, cls_list, colbin, okey, ohist, ooffs, otmp, lists,
+                                  ca.list_stride, c->stream));
         int hc[2 * kAllBins + 1];
         unsigned long long hf[3 * kAllBins];
         RC(readback(c, counts, sizeof(int) * NB1, hc));
@@ -768,6 +790,7 @@ int mcl_ctx_create(mcl_ctx_t *out, int device, void *stream, mcl_alloc_fn alloc,
     c->sms = prop.multiProcessorCount;
     if (const char *e = getenv("MCLX_ALPHA")) c->alpha = (float)atof(e);
     if (const char *e = getenv("MCLX_MAX_LOAD")) c->max_load = (float)atof(e);
+    if (const char *e = getenv("MCLX_ORDER")) c->order_lists = atoi(e) != 0;
     if (const char *e = getenv("MCLX_GBIN_BUDGET_MB")) c->gbin_budget = (int64_t)atoll(e) << 20;
     if (cudaMallocHost(&c->pin, 4096) != cudaSuccess) {
         delete c;

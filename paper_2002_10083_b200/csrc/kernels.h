@@ -109,8 +109,18 @@ struct ClassifyArgs {
     int32_t *gcap_col;       // [ncols_out]
     unsigned long long *bin_flops;  // [kNumBins + 1]
     unsigned long long *bin_nnzb;   // [kNumBins + 1] sum of nnz(B_*j)
+    int32_t *colbin;         // optional [ncols_out]: the bin chosen for each column
 };
 cudaError_t launch_classify(const ClassifyArgs &c, cudaStream_t s);
+// Locality order of the bin work lists: key[j] = min over rows i of B_*j of a hash of
+// i (a MinHash of the column's row set, so columns with similar row sets -- the same
+// family / cluster -- get equal keys); the lists are rewritten sorted by (bin, key >> 16).
+constexpr int kOrderBits = 16;
+cudaError_t launch_minhash_key(int64_t n, const int64_t *bcp, const int32_t *brow, int64_t cb,
+                               uint32_t *key, cudaStream_t s);
+cudaError_t launch_order_lists(int64_t n, const int32_t *cols, const int32_t *colbin,
+                               const uint32_t *key, int64_t *hist, int64_t *offs, void *scan_tmp,
+                               int32_t *lists, int64_t list_stride, cudaStream_t s);
 cudaError_t launch_global_layout(int count, const int32_t *list, const int32_t *gcap_col,
                                  int32_t *gcap, int64_t *gcap64, cudaStream_t s);
 cudaError_t launch_kcap(int64_t ncols, const int64_t *flops, int64_t m, int kmax, int64_t *kcap,

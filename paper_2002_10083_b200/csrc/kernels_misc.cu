@@ -215,7 +215,10 @@ __global__ void k_classify(ClassifyArgs c) {
          i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t col = c.cols ? c.cols[i] : i;
         const int64_t f = c.flops[col];
-        if (f == 0) continue;
+        if (f == 0) {
+            if (c.colbin) c.colbin[col] = -1;
+            continue;
+        }
         const int64_t ub = f < c.m ? f : c.m;
         int64_t need = ub;
         if (c.exact) {
@@ -235,6 +238,7 @@ __global__ void k_classify(ClassifyArgs c) {
         const int bb = fam * kFamily + b;
         const int pos = atomicAdd(&c.bin_count[bb], 1);
         c.lists[(int64_t)bb * c.list_stride + pos] = (int32_t)col;
+        if (c.colbin) c.colbin[col] = bb;
         atomicAdd(&c.bin_flops[bb], (unsigned long long)f);
         atomicAdd(&c.bin_nnzb[bb], (unsigned long long)nb);
         if (b == kNumBins) {
@@ -251,6 +255,92 @@ cudaError_t launch_classify(const ClassifyArgs &c, cudaStream_t s) {
     if (b > 148 * 16) b = 148 * 16;
     ++g_launches;
     k_classify<<<(int)b, 256, 0, s>>>(c);
+    return cudaGetLastError();
+}
+
+__device__ __forceinline__ uint32_t fmix32(uint32_t h) {
+    h ^= h >> 16;
+    h *= 0x85ebca6bu;
+    h ^= h >> 13;
+    h *= 0xc2b2ae35u;
+    h ^= h >> 16;
+    return h;
+}
+
+// warp per column: key[j] = min_{i in rows(B_*j)} fmix32(i)
+__global__ void k_minhash_key(int64_t n, const int64_t *bcp, const int32_t *brow, int64_t cb,
+                              uint32_t *key) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t j = w0; j < n; j += nw) {
+        const int64_t q0 = bcp[cb + j], q1 = bcp[cb + j + 1];
+        uint32_t k = 0xffffffffu;
+        for (int64_t q = q0 + lane; q < q1; q += 32) {
+            const uint32_t h = fmix32((uint32_t)__ldg(brow + q));
+            k = h < k ? h : k;
+        }
+        k = __reduce_min_sync(0xffffffffu, k);
+        if (lane == 0) key[j] = k;
+    }
+}
+
+cudaError_t launch_minhash_key(int64_t n, const int64_t *bcp, const int32_t *brow, int64_t cb,
+                               uint32_t *key, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    int64_t b = (n + 7) / 8;
+    if (b > 148 * 16) b = 148 * 16;
+    ++g_launches;
+    k_minhash_key<<<(int)b, 256, 0, s>>>(n, bcp, brow, cb, key);
+    return cudaGetLastError();
+}
+
+__device__ __forceinline__ int64_t order_bucket(int32_t bb, uint32_t key) {
+    return ((int64_t)bb << kOrderBits) | (int64_t)(key >> (32 - kOrderBits));
+}
+
+__global__ void k_order_hist(int64_t n, const int32_t *cols, const int32_t *colbin,
+                             const uint32_t *key, int64_t *hist) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t col = cols ? cols[i] : (int32_t)i;
+        const int32_t bb = colbin[col];
+        if (bb < 0) continue;
+        atomicAdd(reinterpret_cast<unsigned long long *>(&hist[order_bucket(bb, key[col])]), 1ull);
+    }
+}
+
+// offs: exclusive scan of hist (offs[b << kOrderBits] = start of bin b); hist is reused
+// as the per-bucket cursor
+__global__ void k_order_scatter(int64_t n, const int32_t *cols, const int32_t *colbin,
+                                const uint32_t *key, const int64_t *offs, int64_t *cursor,
+                                int32_t *lists, int64_t list_stride) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t col = cols ? cols[i] : (int32_t)i;
+        const int32_t bb = colbin[col];
+        if (bb < 0) continue;
+        const int64_t bk = order_bucket(bb, key[col]);
+        const int64_t pos = offs[bk] + (int64_t)atomicAdd(reinterpret_cast<unsigned long long *>(&cursor[bk]), 1ull);
+        lists[(int64_t)bb * list_stride + (pos - offs[(int64_t)bb << kOrderBits])] = col;
+    }
+}
+
+cudaError_t launch_order_lists(int64_t n, const int32_t *cols, const int32_t *colbin,
+                               const uint32_t *key, int64_t *hist, int64_t *offs, void *scan_tmp,
+                               int32_t *lists, int64_t list_stride, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    const int64_t nbk = (int64_t)kAllBins << kOrderBits;
+    cudaError_t e = cudaMemsetAsync(hist, 0, sizeof(int64_t) * nbk, s);
+    if (e != cudaSuccess) return e;
+    int64_t b = (n + 255) / 256;
+    if (b > 148 * 16) b = 148 * 16;
+    ++g_launches;
+    k_order_hist<<<(int)b, 256, 0, s>>>(n, cols, colbin, key, hist);
+    if ((e = launch_scan_i64(hist, offs, nbk, scan_tmp, s)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(hist, 0, sizeof(int64_t) * nbk, s)) != cudaSuccess) return e;
+    ++g_launches;
+    k_order_scatter<<<(int)b, 256, 0, s>>>(n, cols, colbin, key, offs, hist, lists, list_stride);
     return cudaGetLastError();
 }
 

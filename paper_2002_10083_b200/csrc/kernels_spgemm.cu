@@ -42,6 +42,7 @@ __device__ unsigned long long g_prof[12];
 constexpr int kParts = 32;  // row ranges of the rowpart index
 constexpr int kItems = 4;   // sub-segment chunks whose gathers a warp keeps in flight
 
+
 // Open addressing with linear probing, four keys per lane at a time.  Phase 1 finds
 // the slot of every (row) -- the first probe of all four is issued back to back, and
 // lanes that collide or insert a new key resolve in a warp-uniform loop (claims by
@@ -104,6 +105,24 @@ __device__ __forceinline__ int group_size_for(int64_t avg) {
     return avg >= 24 ? 32 : avg >= 12 ? 16 : avg >= 6 ? 8 : 4;
 }
 
+// old = p ? atomicCAS(addr, kEmptyKey, val) : dflt, as one predicated instruction (the
+// compiler otherwise wraps every CAS in a divergent branch)
+__device__ __forceinline__ int cas_if(bool p, int *addr, int val, int dflt) {
+    int old = dflt;
+    if (__isShared(addr)) {
+        const unsigned a = (unsigned)__cvta_generic_to_shared(addr);
+        asm volatile(
+            "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %1, 0;\n\t"
+            "@q atom.shared.cas.b32 %0, [%2], %3, %4;\n\t}"
+            : "+r"(old)
+            : "r"((int)p), "r"(a), "r"(kEmptyKey), "r"(val)
+            : "memory");
+    } else if (p) {
+        old = atomicCAS(addr, kEmptyKey, val);
+    }
+    return old;
+}
+
 // Insert one (row, v) per valid lane into this warp's private slice (keys, vals)[0, scap).
 // The valid lanes hold distinct rows (one sub-segment), so after the slots are found the
 // value update is a plain read-modify-write.  Open addressing with linear probing; empty
@@ -145,8 +164,100 @@ __device__ __forceinline__ bool warp_insert(int *keys, V *vals, uint32_t scap, b
     return true;
 }
 
+// kItems inserts per lane at once (item u: lanes hold distinct rows of one sub-segment;
+// the same row may appear in several items).  All slots are probed first and one
+// warp-uniform loop resolves misses / claims for every item, so a call that needs a claim
+// pays the vote + fill count once for all items, not once per item.  The value updates
+// then run item by item with a warp barrier between them: that is what keeps two lanes
+// holding the same row in different items from losing an update.
+template <int MODE, typename V, int NI>
+__device__ __forceinline__ bool warp_insert_n(int *keys, V *vals, uint32_t scap, const bool (&valid)[NI],
+                                              const int (&row)[NI], const V (&v)[NI], int &fill,
+                                              int limit, unsigned &passes) {
+    const unsigned FULL = 0xffffffffu;
+    volatile int *vk = keys;
+    uint32_t s[NI];
+    int k[NI];
+    bool need[NI];
+#pragma unroll
+    for (int u = 0; u < NI; u++) {
+        s[u] = hash_slot(row[u], scap);
+        k[u] = valid[u] ? vk[s[u]] : row[u];
+    }
+    bool any = false;
+#ifdef MCLX_FIRST_CLAIM
+    // an empty home slot is claimed right away (predicated CAS, no branch per item)
+    int claims0 = 0;
+#pragma unroll
+    for (int u = 0; u < NI; u++) {
+        const bool try_claim = valid[u] && k[u] == kEmptyKey;
+        const int old = cas_if(try_claim, &keys[s[u]], row[u], k[u]);
+        claims0 += try_claim && old == kEmptyKey;
+        k[u] = (try_claim && old == kEmptyKey) ? row[u] : old;
+    }
+    fill += __reduce_add_sync(FULL, claims0);
+    if (fill > limit) return false;
+#endif
+#pragma unroll
+    for (int u = 0; u < NI; u++) {
+        need[u] = k[u] != row[u];
+        any |= need[u];
+    }
+    while (__any_sync(FULL, any)) {
+        passes++;
+        int claims = 0;
+        any = false;
+#pragma unroll
+        for (int u = 0; u < NI; u++) {
+            if (need[u]) {
+                if (k[u] == kEmptyKey) {
+                    const int old = atomicCAS(&keys[s[u]], kEmptyKey, row[u]);
+                    if (old == kEmptyKey) {
+                        claims++;
+                        need[u] = false;
+                    } else {
+                        k[u] = old;  // taken by another lane / item: re-examine
+                        need[u] = old != row[u];
+                    }
+                } else {
+                    s[u] = (s[u] + 1 == scap) ? 0u : s[u] + 1;
+                    k[u] = vk[s[u]];
+                    need[u] = k[u] != row[u];
+                }
+            }
+            any |= need[u];
+        }
+        fill += __reduce_add_sync(FULL, claims);
+        if (fill > limit) return false;
+    }
+    if (MODE != kSym) {
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < NI; u++) {
+            if (valid[u]) vals[s[u]] += v[u];
+            __syncwarp();
+        }
+    }
+    return true;
+}
+
+// Resident CTAs per SM that a private-family bin's table allows (table + ~3 KB static
+// shared memory out of 228 KB, at most 2048 threads): the launch bound then gives the
+// compiler 65536 / (that x NT) registers -- occupancy is set by the table anyway -- so the
+// software-pipelined gathers stay in registers.
 template <int CAP, int NT, int MODE, bool GLOBAL, bool ATOMIC>
-__global__ void __launch_bounds__(NT, (1024 / NT > 32 ? 32 : 1024 / NT)) k_bin(BinArgs a) {
+constexpr int bin_min_blocks() {
+    if (ATOMIC) return 1024 / NT > 32 ? 32 : 1024 / NT;
+    if (GLOBAL) return 2048 / NT / 2;
+    const int tbl = CAP * (MODE == kSym ? 4 : 8) + 3072;
+    int b = (228 * 1024) / tbl;
+    b = b < 2048 / NT ? b : 2048 / NT;
+    b = b < 32 ? b : 32;
+    return b < 1 ? 1 : b;
+}
+
+template <int CAP, int NT, int MODE, bool GLOBAL, bool ATOMIC>
+__global__ void __launch_bounds__(NT, (bin_min_blocks<CAP, NT, MODE, GLOBAL, ATOMIC>())) k_bin(BinArgs a) {
     using V = typename std::conditional<GLOBAL, double, float>::type;
     extern __shared__ __align__(16) unsigned char dsm[];
     __shared__ unsigned hist[256];
@@ -279,6 +390,9 @@ __global__ void __launch_bounds__(NT, (1024 / NT > 32 ? 32 : 1024 / NT)) k_bin(B
         } else {
             // ---- accumulate C_*j = sum_k b_kj A_*k: warp `warp` handles rows of its range
             unsigned prof_passes = 0, prof_calls = 0, prof_valid = 0;
+#ifdef MCLX_EXPT
+            float prof_sink = 0.f;
+#endif
 #ifdef MCLX_PROF
             const long long prof_t0 = clock64();
 #endif
@@ -289,13 +403,18 @@ __global__ void __launch_bounds__(NT, (1024 / NT > 32 ? 32 : 1024 / NT)) k_bin(B
             const int64_t bj = a.cb + col;
             const int64_t q0 = a.bcp[bj], q1 = a.bcp[bj + 1];
             int fill = 0;
-            for (int64_t e0 = q0; e0 < q1 && ok; e0 += 32) {
-                // lane l holds the descriptor of segment e0 + l (this warp's sub-segment)
-                int64_t dlo = 0;
-                int dlen = 0;
-                float db = 0.f;
-                if (e0 + lane < q1) {
-                    const int k = __ldg(a.brow + e0 + lane);
+            // Software pipeline over batches.  A batch is kItems sub-segments side by side,
+            // 32 rows of each (chunk c); a group is 32 consecutive segments of B_*j whose
+            // descriptors (this warp's sub-segment: start, length, b_kj) sit one per lane.
+            // The gathers of batch i+1 -- and the descriptor loads of the group after the
+            // next -- are issued before batch i is inserted, so each warp always has a
+            // batch of loads in flight while it works on the hash table.
+            auto load_desc = [&](int64_t g, int64_t &dlo, int &dlen, float &db) {
+                dlo = 0;
+                dlen = 0;
+                db = 0.f;
+                if (g + lane < q1) {
+                    const int k = __ldg(a.brow + g + lane);
                     const int64_t base = __ldg(a.acp + k);
                     if (W == 1) {
                         dlo = base;
@@ -306,55 +425,105 @@ __global__ void __launch_bounds__(NT, (1024 / NT > 32 ? 32 : 1024 / NT)) k_bin(B
                         dlo = base + p0;
                         dlen = p1 - p0;
                     }
-                    db = __ldg(a.bval + e0 + lane);
+                    db = __ldg(a.bval + g + lane);
                 }
-                const int ncnt = (int)((q1 - e0) < 32 ? (q1 - e0) : 32);
-                // kItems segments side by side; chunks of 32 rows of each per step
-                for (int eb = 0; eb < ncnt && ok; eb += kItems) {
-                    int64_t lo_u[kItems];
-                    int len_u[kItems];
-                    float b_u[kItems];
-                    int maxlen = 0;
+            };
+            // batch at (group g, first segment eb, chunk c) -> registers; returns the
+            // longest sub-segment of the batch (chunks continue while c + 32 < it)
+            auto fetch = [&](int64_t g, int eb, int c, int64_t dlo, int dlen, float db, int (&rr)[kItems],
+                             float (&av)[kItems], float (&bb)[kItems]) {
+                const int ncnt = (int)((q1 - g) < 32 ? (q1 - g) : 32);
+                const int t = c + lane;
+                int ml = 0;
     #pragma unroll
-                    for (int u = 0; u < kItems; u++) {
-                        const int e = eb + u;
-                        lo_u[u] = __shfl_sync(0xffffffffu, dlo, e & 31);
-                        len_u[u] = __shfl_sync(0xffffffffu, dlen, e & 31);
-                        b_u[u] = __shfl_sync(0xffffffffu, db, e & 31);
-                        if (e >= ncnt) len_u[u] = 0;
-                        maxlen = len_u[u] > maxlen ? len_u[u] : maxlen;
-                    }
-                    for (int c = 0; c < maxlen && ok; c += 32) {
-                        int rr[kItems];
-                        V vv[kItems];
-                        bool vl[kItems];
-                        const int t = c + lane;
-    #pragma unroll
-                        for (int u = 0; u < kItems; u++) {
-                            vl[u] = t < len_u[u];
-                            rr[u] = vl[u] ? __ldg(a.arow + lo_u[u] + t) : -1;
-                            vv[u] = V(0);
-                            if (MODE != kSym && vl[u]) {
-                                const float av = __ldg(a.aval + lo_u[u] + t);
-                                vv[u] = GLOBAL ? (V)av * (V)b_u[u] : (V)(av * b_u[u]);
-                            }
-                        }
-    #pragma unroll
-                        for (int u = 0; u < kItems; u++) {
-    #ifdef MCLX_PROF
-                        prof_calls++;
-                        prof_valid += __popc(__ballot_sync(0xffffffffu, vl[u]));
+                for (int u = 0; u < kItems; u++) {
+                    const int e = eb + u;
+                    const int64_t lo = __shfl_sync(0xffffffffu, dlo, e & 31);
+                    int len = __shfl_sync(0xffffffffu, dlen, e & 31);
+                    bb[u] = __shfl_sync(0xffffffffu, db, e & 31);
+                    if (e >= ncnt) len = 0;
+                    ml = len > ml ? len : ml;
+                    const bool v = t < len;
+                    rr[u] = v ? __ldg(a.arow + lo + t) : -1;
+                    av[u] = 0.f;
+                    if (MODE != kSym && v) {
+#if defined(MCLX_EXPT) && MCLX_EXPT == 2
+                        av[u] = 0.5f;  // experiment: no value gathers
+#else
+                        av[u] = __ldg(a.aval + lo + t);
 #endif
-                        if (!warp_insert<MODE, V>(wkeys, wvals, scap, vl[u], rr[u], vv[u], fill, limit,
-                                                  prof_passes)) {
-                                ok = false;
-                                break;
-                            }
-                        }
                     }
                 }
+                return ml;
+            };
+            int64_t g = q0;
+            int64_t clo, nlo;
+            int clen, nlen;
+            float cdb, ndb;
+            load_desc(g, clo, clen, cdb);
+            load_desc(g + 32, nlo, nlen, ndb);
+            int eb = 0, c = 0;
+            int rr[kItems];
+            float av[kItems], bb[kItems];
+            int ml = g < q1 ? fetch(g, eb, c, clo, clen, cdb, rr, av, bb) : 0;
+            while (g < q1 && ok) {
+                // position of the next batch
+                int neb = eb, nc = c + 32;
+                int64_t ng = g;
+                if (nc >= ml) {
+                    nc = 0;
+                    neb = eb + kItems;
+                    const int ncnt = (int)((q1 - g) < 32 ? (q1 - g) : 32);
+                    if (neb >= ncnt) {
+                        neb = 0;
+                        ng = g + 32;
+                        clo = nlo;
+                        clen = nlen;
+                        cdb = ndb;
+                        load_desc(ng + 32, nlo, nlen, ndb);
+                    }
+                }
+                int nrr[kItems];
+                float nav[kItems], nbb[kItems];
+                const int nml = ng < q1 ? fetch(ng, neb, nc, clo, clen, cdb, nrr, nav, nbb) : 0;
+                // insert the current batch
+                bool vl[kItems];
+                V vv[kItems];
+    #pragma unroll
+                for (int u = 0; u < kItems; u++) {
+                    vl[u] = rr[u] >= 0;
+                    vv[u] = GLOBAL ? (V)av[u] * (V)bb[u] : (V)(av[u] * bb[u]);
+                }
+#ifdef MCLX_PROF
+    #pragma unroll
+                for (int u = 0; u < kItems; u++) {
+                    prof_calls++;
+                    prof_valid += __popc(__ballot_sync(0xffffffffu, vl[u]));
+                }
+#endif
+#if defined(MCLX_EXPT) && MCLX_EXPT == 1
+                // experiment: gathers only
+                for (int u = 0; u < kItems; u++) prof_sink += vl[u] ? (float)rr[u] * (float)vv[u] : 0.f;
+#else
+                if (!warp_insert_n<MODE, V, kItems>(wkeys, wvals, scap, vl, rr, vv, fill, limit,
+                                                    prof_passes))
+                    ok = false;
+#endif
+    #pragma unroll
+                for (int u = 0; u < kItems; u++) {
+                    rr[u] = nrr[u];
+                    av[u] = nav[u];
+                    bb[u] = nbb[u];
+                }
+                g = ng;
+                eb = neb;
+                c = nc;
+                ml = nml;
             }
             fresh = lane == 0 ? fill : 0;
+#ifdef MCLX_EXPT
+            if (prof_sink == 1234.5f) atomicAdd(&g_prof[11], 1ull);
+#endif
 #ifdef MCLX_PROF
             if (lane == 0) {
                 PROF_ADD(0, prof_calls);

@@ -153,14 +153,16 @@ def cliques_noise(n: int = 20000, clique: int = 190, noise_per_vertex: float = 1
 
 def protein_like(n: int = 500_000, zipf_a: float = 2.1, fam_cap: int = 2000,
                  complete_max: int = 257, draw_k: int = 128, super_size: int = 10,
-                 super_mean: float = 10.0, uniform_mean: float = 2.0, seed: int = 3) -> Csc:
+                 super_mean: float = 10.0, uniform_mean: float = 2.0, seed: int = 3,
+                 permute: bool = True) -> Csc:
     """C3/C5 protein-similarity-like graph.
 
     Family sizes ~ Zipf(zipf_a) capped at ``fam_cap``.  Intra-family: complete if
     size <= complete_max, else every vertex draws ``draw_k`` in-family partners;
     weights U[0.3,1.0).  Superfamilies of ``super_size`` consecutive families:
     Poisson(super_mean) partners per vertex inside the superfamily, U[0.05,0.4).
-    Plus Poisson(uniform_mean) uniform partners per vertex, U[0.01,0.2)."""
+    Plus Poisson(uniform_mean) uniform partners per vertex, U[0.01,0.2).
+    ``permute=False`` keeps vertices numbered family by family (labels with locality)."""
     rng = np.random.default_rng(seed)
     sizes = []
     tot = 0
@@ -216,7 +218,7 @@ def protein_like(n: int = 500_000, zipf_a: float = 2.1, fam_cap: int = 2000,
 
     perm = rng.permutation(n)
     return pairs_to_symmetric_csc(n, np.concatenate([fi, sv, uv]), np.concatenate([fj, sj, uj]),
-                                  np.concatenate([fw, sw, uw]), perm)
+                                  np.concatenate([fw, sw, uw]), perm if permute else None)
 
 
 def rmat(scale: int = 22, edge_factor: int = 32, a: float = 0.57, b: float = 0.19,

@@ -278,6 +278,19 @@ def test_iterate_c1_second_iteration_all_bins():
         kept_parity(host_mat(Ag), Cr1, info, (1e-4, 1100, 1400, 0.9))
 
 
+def test_iterate_label_locality():
+    """Vertices numbered family by family: a column's output rows crowd into one warp's
+    row range, so private row-range slices overflow and the columns must be re-run in the
+    CTA-shared-table family (regression: this used to fail after exact re-binning)."""
+    A = f32(O.preprocess(synth.protein_like(n=30_000, seed=5, permute=False)))
+    Ag, st = M.iterate(dev(A), M.Params())
+    Cr, fl = O.expand(A)
+    _, info = O.prune_inflate(Cr, 1e-4, 1100, 1400, 0.9, 2.0)
+    kept_parity(host_mat(Ag), Cr, info, (1e-4, 1100, 1400, 0.9))
+    assert st["flops"] == int(fl.sum())
+    assert st["retries"] > 0
+
+
 @pytest.mark.parametrize("scale", [12, 14])
 def test_rmat_iterate_parity(scale):
     """R-MAT (C4 shape: skewed degrees, hub columns) -- one fused iteration vs the oracle."""

@@ -1,0 +1,7 @@
+#!/bin/bash
+# development: build libmclx.so and the -DMCLX_PROF copy (tools/libmclx_prof.so)
+set -e
+cd "$(dirname "$0")/.."
+MCLX_NVCC_EXTRA=-DMCLX_PROF python -c "from paper_2002_10083_b200 import _build; _build.build(force=True)"
+cp paper_2002_10083_b200/libmclx.so tools/libmclx_prof.so
+python -c "from paper_2002_10083_b200 import _build; _build.build(force=True)"
