@@ -113,6 +113,9 @@ typedef struct {
     int64_t bin_out[MCL_NUM_BINS + 1];       /* entries the bin wrote (fused: kept entries)     */
     int64_t comm_bytes;      /* bytes this rank received in SUMMA broadcasts                    */
     int64_t peak_partial;    /* peak live nnz of SUMMA stage partials (Alg. 2 schedule)         */
+    int64_t split_cols;      /* columns run as row-range parts (counted in bin MCL_NUM_BINS too) */
+    int64_t split_items;     /* row-range parts run                                             */
+    float split_ms;          /* device time of the split path (included in bin_ms[MCL_NUM_BINS])*/
 } mcl_stats_t;
 
 /* Allocator callbacks: device memory, stream-ordered.  NULL callbacks select the

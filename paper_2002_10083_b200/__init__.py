@@ -69,7 +69,8 @@ class StatsT(C.Structure):
                 ("peak_bytes", C.c_int64), ("launches", C.c_int64),
                 ("bin_ms", C.c_float * (NUM_BINS + 1)), ("bin_nnzb", C.c_int64 * (NUM_BINS + 1)),
                 ("bin_out", C.c_int64 * (NUM_BINS + 1)), ("comm_bytes", C.c_int64),
-                ("peak_partial", C.c_int64)]
+                ("peak_partial", C.c_int64), ("split_cols", C.c_int64),
+                ("split_items", C.c_int64), ("split_ms", C.c_float)]
 
     def as_dict(self) -> dict:
         d = {k: getattr(self, k) for k, _ in self._fields_}

@@ -46,6 +46,10 @@ struct mcl_ctx {
     float alpha = 1.2f;     // table sizing: need = alpha * Cohen estimate + 16
     float max_load = 0.5f;  // bin when need <= max_load * cap
     bool order_lists = true;  // MinHash locality order of the bin work lists
+    bool split = true;        // row-range split of big fused columns (MCLX_SPLIT=0: off)
+    int64_t split_budget = (int64_t)4 << 30;  // staging bytes per chunk of split parts
+    int64_t split_min_need = INT64_MAX;       // MCLX_SPLIT_MIN_NEED: split smaller columns too
+    int64_t split_part_need = kPartNeed;      // MCLX_SPLIT_PART_NEED (<= kPartNeed; tests)
 };
 
 namespace {
@@ -208,6 +212,153 @@ int cohen(mcl_ctx *c, const Prod &pr, int r, uint64_t seed, float *est, float *k
     return MCL_OK;
 }
 
+// Split columns (fused mode): a column too big for one CTA's shared-memory table is
+// processed as P row-range parts (rowparts [p 32/P, (p+1) 32/P)), one CTA each with a
+// shared-memory table (kPart), which writes the part's entries, rows sorted, to a
+// staging slot.  Per chunk of columns (staging bounded by split_budget) the parts are
+// stitched -- parts are row ranges, so concatenation keeps rows sorted -- into an
+// unpruned CSC that k_prune turns into the pruned / inflated columns (Alg. 1 l.4-5).
+// The tables stay on chip, unlike the global bin's, and a column's work spreads over P
+// SMs.  A part that overflows flags its column for the next round.
+int run_split(mcl_ctx *c, const Prod &pr, int nsplit, int32_t *split_list,
+              const int32_t *split_P, BinArgs a, unsigned long long *out_count,
+              int64_t *nitems_out) {
+    std::vector<int32_t> hl((size_t)nsplit), hP((size_t)pr.n);
+    CK(cudaMemcpyAsync(hl.data(), split_list, sizeof(int32_t) * nsplit, cudaMemcpyDeviceToHost,
+                       c->stream));
+    CK(cudaMemcpyAsync(hP.data(), split_P, sizeof(int32_t) * pr.n, cudaMemcpyDeviceToHost,
+                       c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    // variant by the virtual part count P (parts sized for T = split_part_need distinct
+    // rows): <= 32 parts of kPartCap slots; 64: 32 parts of 2 kPartCap slots; more: 32
+    // parts with fp64 global tables of 2 P T / 32 slots (load <= 1/2), small enough that
+    // the live tables of all resident parts stay near L2 size
+    auto variant_of = [](int P) { return P <= 32 ? 0 : P == 64 ? 1 : 2; };
+    std::stable_partition(hl.begin(), hl.end(), [&](int32_t col) { return variant_of(hP[col]) == 0; });
+    std::stable_partition(hl.begin(), hl.end(), [&](int32_t col) { return variant_of(hP[col]) <= 1; });
+    const int64_t cap_of[3] = {kPartCap, 2 * kPartCap, 0};
+    std::vector<int64_t> hoff((size_t)nsplit + 1, 0);   // first item of each column
+    std::vector<int64_t> hstg;                          // staging offset of each item
+    std::vector<int64_t> hgcap;                         // global table slots of each item
+    hstg.reserve((size_t)nsplit * 4 + 1);
+    int64_t stg = 0;
+    for (int s2 = 0; s2 < nsplit; s2++) {
+        const int P = hP[hl[s2]], v = variant_of(P);
+        const int parts = P < 32 ? P : 32;
+        hoff[s2 + 1] = hoff[s2] + parts;
+        const int64_t tcap = v == 2 ? std::max<int64_t>((int64_t)P * c->split_part_need / 16, 1024)
+                                    : cap_of[v];
+        for (int q = 0; q < parts; q++) {
+            hstg.push_back(stg);
+            stg += tcap - tcap / 8;  // the 7/8 fill limit bounds a part's entries
+            hgcap.push_back(v == 2 ? tcap : 0);
+        }
+    }
+    hstg.push_back(stg);
+    const int64_t nitems = hoff[nsplit];
+    *nitems_out = nitems;
+    // chunks: whole columns of one variant, staging (x2: staged + stitched) within budget
+    const int64_t budget = std::max<int64_t>(c->split_budget / 16, 1 << 16);  // entries
+    std::vector<int> cuts{0};
+    for (int s2 = 0; s2 < nsplit; s2++) {
+        const int s0 = cuts.back();
+        if (s2 == s0) continue;
+        const bool vchange = variant_of(hP[hl[s2]]) != variant_of(hP[hl[s0]]);
+        const bool full = hstg[hoff[s2 + 1]] - hstg[hoff[s0]] > budget;
+        if (vchange || full) cuts.push_back(s2);
+    }
+    cuts.push_back(nsplit);
+    const int nchunks = (int)cuts.size() - 1;
+    int64_t chunk_items = 0, chunk_stg = 0, chunk_g = 0;
+    for (int q = 0; q < nchunks; q++) {
+        const int64_t i0 = hoff[cuts[q]], i1 = hoff[cuts[q + 1]];
+        chunk_items = std::max(chunk_items, i1 - i0);
+        chunk_stg = std::max(chunk_stg, hstg[i1] - hstg[i0]);
+        int64_t g = 0;
+        for (int64_t i = i0; i < i1; i++) g += hgcap[i];
+        chunk_g = std::max(chunk_g, g);
+    }
+    // device copies: reordered column list, item layout
+    std::vector<int64_t> hgoff((size_t)nitems + 1, 0);
+    for (int64_t i = 0; i < nitems; i++) hgoff[i + 1] = hgoff[i] + hgcap[i];
+    int64_t *ioff, *stg_off, *goff, *stg_cnt, *sioff, *ccp;
+    int32_t *item_col, *item_pr, *stg_row, *crow, *colmap, *gcap;
+    float *stg_val, *cval;
+    int *ccount;
+    void *tmp;
+    RC(scratch_t(c, "split_ioff", (size_t)nsplit + 1, &ioff));
+    RC(scratch_t(c, "split_stg_off", (size_t)nitems + 1, &stg_off));
+    RC(scratch_t(c, "split_goff", (size_t)nitems + 1, &goff));
+    RC(scratch_t(c, "split_gcap", (size_t)nitems + 1, &gcap));
+    RC(scratch_t(c, "split_item_col", (size_t)nitems, &item_col));
+    RC(scratch_t(c, "split_item_pr", (size_t)nitems, &item_pr));
+    RC(scratch_t(c, "split_counts", (size_t)2 * nchunks, &ccount));
+    RC(scratch_t(c, "split_stg_cnt", (size_t)chunk_items, &stg_cnt));
+    RC(scratch_t(c, "split_sioff", (size_t)chunk_items + 1, &sioff));
+    RC(scratch_t(c, "split_stg_row", (size_t)chunk_stg, &stg_row));
+    RC(scratch_t(c, "split_stg_val", (size_t)chunk_stg, &stg_val));
+    RC(scratch_t(c, "split_crow", (size_t)chunk_stg, &crow));
+    RC(scratch_t(c, "split_cval", (size_t)chunk_stg, &cval));
+    RC(scratch_t(c, "split_ccp", (size_t)nsplit + 1, &ccp));
+    RC(scratch_t(c, "split_colmap", (size_t)nsplit, &colmap));
+    RC(scratch(c, "split_scan_tmp", scan_tmp_bytes(chunk_items + 1), &tmp));
+    int *gkeys = nullptr;
+    double *gvals = nullptr;
+    if (chunk_g > 0) {
+        RC(scratch_t(c, "split_gkeys", (size_t)chunk_g, &gkeys));
+        RC(scratch_t(c, "split_gvals", (size_t)chunk_g, &gvals));
+    }
+    std::vector<int> hcnt((size_t)2 * nchunks, 0);
+    for (int q = 0; q < nchunks; q++) hcnt[q] = (int)(hoff[cuts[q + 1]] - hoff[cuts[q]]);
+    std::vector<int32_t> hgcap32(hgcap.begin(), hgcap.end());
+    CK(cudaMemcpyAsync(split_list, hl.data(), sizeof(int32_t) * nsplit, cudaMemcpyHostToDevice,
+                       c->stream));
+    CK(cudaMemcpyAsync(ioff, hoff.data(), sizeof(int64_t) * (nsplit + 1), cudaMemcpyHostToDevice,
+                       c->stream));
+    CK(cudaMemcpyAsync(stg_off, hstg.data(), sizeof(int64_t) * (nitems + 1), cudaMemcpyHostToDevice,
+                       c->stream));
+    CK(cudaMemcpyAsync(goff, hgoff.data(), sizeof(int64_t) * (nitems + 1), cudaMemcpyHostToDevice,
+                       c->stream));
+    CK(cudaMemcpyAsync(gcap, hgcap32.data(), sizeof(int32_t) * nitems, cudaMemcpyHostToDevice,
+                       c->stream));
+    CK(cudaMemcpyAsync(ccount, hcnt.data(), sizeof(int) * 2 * nchunks, cudaMemcpyHostToDevice,
+                       c->stream));
+    CK(launch_split_items(nsplit, split_list, split_P, ioff, item_col, item_pr, c->stream));
+    int occ[3];
+    for (int v = 0; v < 3; v++) occ[v] = std::max(1, part_occupancy(v));
+    const int pgrid = (int)std::min<int64_t>(std::max<int64_t>(pr.n, 1), (int64_t)c->sms * 8);
+    for (int q = 0; q < nchunks; q++) {
+        const int s0 = cuts[q], nc = cuts[q + 1] - cuts[q];
+        const int64_t item0 = hoff[s0], nit = hoff[cuts[q + 1]] - item0;
+        const int v = variant_of(hP[hl[s0]]);
+        // staging offsets relative to the chunk: stg_off[i] - stg_off[item0]
+        BinArgs ap = a;
+        ap.list = item_col + item0;
+        ap.item_pr = item_pr + item0;
+        ap.count = ccount + q;
+        ap.counter = ccount + nchunks + q;
+        ap.stg_off = stg_off + item0;
+        ap.stg_row = stg_row - hstg[item0];
+        ap.stg_val = stg_val - hstg[item0];
+        ap.stg_cnt = stg_cnt;
+        if (v == 2) {
+            ap.goff = goff + item0;
+            ap.gcap = gcap + item0;
+            ap.gkeys = gkeys - hgoff[item0];
+            ap.gvals = gvals - hgoff[item0];
+        }
+        CK(launch_part(v, ap, (int)std::min<int64_t>(nit, (int64_t)occ[v] * c->sms), c->stream));
+        CK(launch_scan_i64(stg_cnt, sioff, nit, tmp, c->stream));
+        CK(launch_split_stitch(nc, ioff + s0, item0, item_col + item0, sioff, a.col_flag, ccp, colmap,
+                               c->stream));
+        CK(launch_split_gather(nit, stg_cnt, stg_off + item0, stg_row - hstg[item0],
+                               stg_val - hstg[item0], sioff, crow, cval, c->stream));
+        CK(launch_prune(nc, ccp, crow, cval, a.soff, a.s_row, a.s_val, a.s_cnt, a.chaos,
+                        a.chaos_max, a.pp, pgrid, c->stream, colmap, out_count));
+    }
+    return MCL_OK;
+}
+
 // Classify the columns of a product into bins and run every bin kernel in `mode`;
 // columns whose table overflowed (estimate too small) are re-binned with the exact
 // bound min(f_j, m) and re-run.  `base` carries the mode's outputs.
@@ -249,6 +400,17 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
     }
 
 
+    // split columns (kFused only): big columns as row-range parts, see run_split
+    const bool use_split = c->split && mode == kFused && pr.A->ncols > 0;
+    int32_t *split_list = nullptr, *split_P = nullptr;
+    int *split_count = nullptr, *col_flag = nullptr;
+    if (use_split) {
+        RC(scratch_t(c, "split_list", (size_t)std::max<int64_t>(n, 1), &split_list));
+        RC(scratch_t(c, "split_P", (size_t)std::max<int64_t>(n, 1), &split_P));
+        RC(scratch_t(c, "split_count", 2, &split_count));
+        RC(scratch_t(c, "col_flag", (size_t)std::max<int64_t>(n, 1), &col_flag));
+    }
+
     // Rounds: 0 sizes by the caller's estimate / exact sizes; 1 re-runs overflowed
     // columns with 4x the estimate; 2 with the exact upper bound min(f_j, m), which
     // cannot overflow (load <= 1/2 < the 7/8 fill limit).  Retried columns run in the
@@ -282,6 +444,17 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
         ca.bin_flops = bflops;
         ca.bin_nnzb = bnnzb;
         ca.colbin = colbin;
+        if (use_split && round < 2) {
+            // the exact round stays in the global bin, which cannot overflow
+            ca.split_max = INT64_MAX;  // the global-table variant takes any size
+            ca.split_min = c->split_min_need;
+            ca.split_part_need = c->split_part_need;
+            ca.split_count = split_count;
+            ca.split_list = split_list;
+            ca.split_P = split_P;
+            CK(cudaMemsetAsync(split_count, 0, sizeof(int), c->stream));
+            CK(cudaMemsetAsync(col_flag, 0, sizeof(int) * std::max<int64_t>(n, 1), c->stream));
+        }
         CK(launch_classify(ca, c->stream));
         if (colbin)
             CK(launch_order_lists(ncls, cls_list, colbin, okey, ohist, ooffs, otmp, lists,
@@ -289,12 +462,44 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
         int hc[2 * kAllBins + 1];
         unsigned long long hf[3 * kAllBins];
         RC(readback(c, counts, sizeof(int) * NB1, hc));
+        int nsplit = 0;
+        if (ca.split_max > 0) RC(readback(c, split_count, sizeof(int), &nsplit));
         RC(readback(c, bflops, sizeof(unsigned long long) * 2 * NB1, hf));
         if (st && round == 0) {
             for (int b = 0; b < NB1; b++) {
                 st->bin_cols[b % kFamily] += hc[b];
                 st->bin_flops[b % kFamily] += (int64_t)hf[b];
                 st->bin_nnzb[b % kFamily] += (int64_t)hf[NB1 + b];
+            }
+            st->bin_cols[kNumBins] += nsplit;  // split columns are reported with the global bin
+        }
+        if (nsplit > 0) {
+            BinArgs a = base;
+            a.acp = pr.A->col_ptr;
+            a.arow = pr.A->row_idx;
+            a.aval = pr.A->val;
+            a.m = pr.A->nrows;
+            a.bcp = pr.B->col_ptr;
+            a.brow = pr.B->row_idx;
+            a.bval = pr.B->val;
+            a.cb = pr.cb;
+            a.flops = f;
+            a.retry_list = retry_list;
+            a.retry_count = retry_count;
+            a.err_flag = err;
+            a.col_flag = col_flag;
+            CK(cudaEventRecord(c->bev[2 * kNumBins], c->stream));
+            int64_t nitems = 0;
+            RC(run_split(c, pr, nsplit, split_list, split_P, a, bout + kNumBins, &nitems));
+            CK(cudaEventRecord(c->bev[2 * kNumBins + 1], c->stream));
+            if (st) {
+                float ms = 0.f;
+                CK(cudaEventSynchronize(c->bev[2 * kNumBins + 1]));
+                CK(cudaEventElapsedTime(&ms, c->bev[2 * kNumBins], c->bev[2 * kNumBins + 1]));
+                st->bin_ms[kNumBins] += ms;
+                st->split_ms += ms;
+                if (round == 0) st->split_cols += nsplit;
+                st->split_items += nitems;
             }
         }
         bool launched[kAllBins] = {};
@@ -791,6 +996,11 @@ int mcl_ctx_create(mcl_ctx_t *out, int device, void *stream, mcl_alloc_fn alloc,
     if (const char *e = getenv("MCLX_ALPHA")) c->alpha = (float)atof(e);
     if (const char *e = getenv("MCLX_MAX_LOAD")) c->max_load = (float)atof(e);
     if (const char *e = getenv("MCLX_ORDER")) c->order_lists = atoi(e) != 0;
+    if (const char *e = getenv("MCLX_SPLIT")) c->split = atoi(e) != 0;
+    if (const char *e = getenv("MCLX_SPLIT_BUDGET_MB")) c->split_budget = (int64_t)atoll(e) << 20;
+    if (const char *e = getenv("MCLX_SPLIT_MIN_NEED")) c->split_min_need = atoll(e);
+    if (const char *e = getenv("MCLX_SPLIT_PART_NEED"))
+        c->split_part_need = std::max<int64_t>(16, std::min<int64_t>(kPartNeed, atoll(e)));
     if (const char *e = getenv("MCLX_GBIN_BUDGET_MB")) c->gbin_budget = (int64_t)atoll(e) << 20;
     if (cudaMallocHost(&c->pin, 4096) != cudaSuccess) {
         delete c;

@@ -20,7 +20,9 @@ __host__ __device__ constexpr int bin_cap(int b) {
 
 constexpr int kFp64Terms = 16384;  // nnz(B_*j) above which a column accumulates in fp64 (T)
 
-enum Mode { kSym = 0, kNum = 1, kFused = 2 };
+// kPart: one row-range part of a split column (see run_bins): accumulate only the rows of
+// rowparts [p0, p1) and write the part's entries, rows sorted, to its staging slot
+enum Mode { kSym = 0, kNum = 1, kFused = 2, kPart = 3 };
 
 // Host-side count of kernel launches issued by this library (reported in mcl_stats_t).
 extern int64_t g_launches;
@@ -62,7 +64,22 @@ struct BinArgs {
     int *err_flag;
     unsigned long long *bin_out;  // this bin's output-entry counter (kFused)
     PruneParams pp;
+    // kPart: item i = part [p0, p1) (item_pr[i] = p0 | p1 << 8) of column list[i]
+    const int32_t *item_pr;
+    const int64_t *stg_off;                             // staging offset of each item
+    int32_t *stg_row;
+    float *stg_val;
+    int64_t *stg_cnt;
+    int *col_flag;                                      // [ncols_out] overflowed split columns
 };
+// the shared-table bin that runs the parts of split columns (table slots, threads)
+constexpr int kPartCap = 8192;
+constexpr int kPartThreads = 512;
+constexpr int kPartNeed = kPartCap / 2;  // distinct rows a part is sized for (load 1/2)
+// part variants: 0 kPartCap-slot shared table, 1 2*kPartCap-slot shared table,
+// 2 fp64 global-memory tables (goff / gcap per item)
+cudaError_t launch_part(int variant, const BinArgs &a, int grid, cudaStream_t s);
+int part_occupancy(int variant);
 
 // Two kernel families share the bins: private row-range slices (bin b = 0..kNumBins) for
 // columns whose average gathered segment is long, and a CTA-shared atomic table
@@ -110,7 +127,28 @@ struct ClassifyArgs {
     unsigned long long *bin_flops;  // [kNumBins + 1]
     unsigned long long *bin_nnzb;   // [kNumBins + 1] sum of nnz(B_*j)
     int32_t *colbin;         // optional [ncols_out]: the bin chosen for each column
+    // split columns (kFused): global-bin columns with need <= split_max are processed
+    // as split_P[col] row-range parts (a power of two, 2..32) instead
+    int64_t split_max;       // 0 disables
+    int64_t split_min;       // also split smaller columns with need > split_min (tests)
+    int64_t split_part_need; // distinct rows a part is sized for (kPartNeed)
+    int *split_count;
+    int32_t *split_list;
+    int32_t *split_P;
 };
+// items of the split columns: item ioff[s] + p = part p of split column s
+cudaError_t launch_split_items(int nsplit, const int32_t *split_list, const int32_t *split_P,
+                               const int64_t *ioff, int32_t *item_col, int32_t *item_pr,
+                               cudaStream_t s);
+// stitch the parts of split columns [s0, s0 + nc) (items from ioff[s0]) into an unpruned
+// CSC: ccp from the scanned part counts sioff; colmap = product column, or -1 when a part
+// overflowed (the column is re-run in a later round)
+cudaError_t launch_split_stitch(int nc, const int64_t *ioff, int64_t item0, const int32_t *item_col,
+                                const int64_t *sioff, const int *col_flag, int64_t *ccp,
+                                int32_t *colmap, cudaStream_t s);
+cudaError_t launch_split_gather(int64_t nitems, const int64_t *stg_cnt, const int64_t *stg_off,
+                                const int32_t *stg_row, const float *stg_val, const int64_t *sioff,
+                                int32_t *crow, float *cval, cudaStream_t s);
 cudaError_t launch_classify(const ClassifyArgs &c, cudaStream_t s);
 // Locality order of the bin work lists: key[j] = min over rows i of B_*j of a hash of
 // i (a MinHash of the column's row set, so columns with similar row sets -- the same
@@ -137,7 +175,8 @@ cudaError_t launch_copy_cols(int64_t ncols, const int64_t *cnt, const int64_t *s
 cudaError_t launch_prune(int64_t ncols, const int64_t *ccp, const int32_t *crow, const float *cval,
                          const int64_t *soff, int32_t *srow, float *sval, int64_t *scnt,
                          float *chaos, float *chaos_max, const PruneParams &pp, int grid,
-                         cudaStream_t s);
+                         cudaStream_t s, const int32_t *colmap = nullptr,
+                         unsigned long long *out_count = nullptr);
 cudaError_t launch_cohen_keys(int64_t m, int64_t row0, int r, uint64_t seed, float *X,
                               float *keys_out, cudaStream_t s);
 cudaError_t launch_cohen_min(int64_t ncols, const int64_t *cp, const int32_t *row, int64_t c0,

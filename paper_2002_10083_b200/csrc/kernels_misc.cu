@@ -232,6 +232,19 @@ __global__ void k_classify(ClassifyArgs c) {
         while (b < kNumBins && (double)need > c.max_load * bin_cap(b)) b++;
         if (nb > kFp64Terms) b = kNumBins;
         if (c.force_bin > b && c.force_bin <= kNumBins) b = c.force_bin;
+        if ((b == kNumBins || need > c.split_min) && c.split_max > 0 && need <= c.split_max &&
+            c.force_bin < 0) {
+            // row-range split, sized by the virtual part count P (a power of two, parts of
+            // ~kPartNeed distinct rows); P > 32 runs 32 parts with bigger tables
+            int P = 2;
+            while ((int64_t)P * c.split_part_need < need) P <<= 1;
+            c.split_P[col] = P;
+            c.split_list[atomicAdd(c.split_count, 1)] = (int32_t)col;
+            if (c.colbin) c.colbin[col] = -1;
+            atomicAdd(&c.bin_flops[kNumBins], (unsigned long long)f);
+            atomicAdd(&c.bin_nnzb[kNumBins], (unsigned long long)nb);
+            continue;
+        }
         // family: short average segments go to the CTA-shared atomic table
         const bool shortseg = f < (int64_t)kShortSegment * nb;
         const int fam = c.force_family >= 0 ? c.force_family : (shortseg ? 1 : 0);
@@ -255,6 +268,79 @@ cudaError_t launch_classify(const ClassifyArgs &c, cudaStream_t s) {
     if (b > 148 * 16) b = 148 * 16;
     ++g_launches;
     k_classify<<<(int)b, 256, 0, s>>>(c);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ split columns
+__global__ void k_split_items(int nsplit, const int32_t *split_list, const int32_t *split_P,
+                              const int64_t *ioff, int32_t *item_col, int32_t *item_pr) {
+    for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < nsplit; s += gridDim.x * blockDim.x) {
+        const int32_t col = split_list[s];
+        const int P = split_P[col] < 32 ? split_P[col] : 32;
+        const int step = 32 / P;
+        const int64_t i0 = ioff[s];
+        for (int p = 0; p < P; p++) {
+            item_col[i0 + p] = col;
+            item_pr[i0 + p] = (p * step) | ((p + 1) * step) << 8;
+        }
+    }
+}
+cudaError_t launch_split_items(int nsplit, const int32_t *split_list, const int32_t *split_P,
+                               const int64_t *ioff, int32_t *item_col, int32_t *item_pr,
+                               cudaStream_t s) {
+    if (nsplit <= 0) return cudaSuccess;
+    ++g_launches;
+    k_split_items<<<(nsplit + 255) / 256, 256, 0, s>>>(nsplit, split_list, split_P, ioff, item_col,
+                                                      item_pr);
+    return cudaGetLastError();
+}
+
+__global__ void k_split_stitch(int nc, const int64_t *ioff, int64_t item0, const int32_t *item_col,
+                               const int64_t *sioff, const int *col_flag, int64_t *ccp,
+                               int32_t *colmap) {
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c <= nc; c += gridDim.x * blockDim.x) {
+        const int64_t i = ioff[c] - item0;  // first item of chunk column c (or the end)
+        ccp[c] = sioff[i];
+        if (c < nc) {
+            const int32_t col = item_col[i];
+            colmap[c] = col_flag[col] ? -1 : col;
+        }
+    }
+}
+cudaError_t launch_split_stitch(int nc, const int64_t *ioff, int64_t item0, const int32_t *item_col,
+                                const int64_t *sioff, const int *col_flag, int64_t *ccp,
+                                int32_t *colmap, cudaStream_t s) {
+    ++g_launches;
+    k_split_stitch<<<(nc + 256) / 256, 256, 0, s>>>(nc, ioff, item0, item_col, sioff, col_flag, ccp,
+                                                   colmap);
+    return cudaGetLastError();
+}
+
+// warp per item: copy its staged (sorted) entries to the stitched column
+__global__ void k_split_gather(int64_t nitems, const int64_t *stg_cnt, const int64_t *stg_off,
+                               const int32_t *stg_row, const float *stg_val, const int64_t *sioff,
+                               int32_t *crow, float *cval) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = w0; i < nitems; i += nw) {
+        const int64_t n = stg_cnt[i];
+        const int64_t src = stg_off[i], dst = sioff[i];
+        for (int64_t e = lane; e < n; e += 32) {
+            crow[dst + e] = stg_row[src + e];
+            cval[dst + e] = stg_val[src + e];
+        }
+    }
+}
+cudaError_t launch_split_gather(int64_t nitems, const int64_t *stg_cnt, const int64_t *stg_off,
+                                const int32_t *stg_row, const float *stg_val, const int64_t *sioff,
+                                int32_t *crow, float *cval, cudaStream_t s) {
+    if (nitems <= 0) return cudaSuccess;
+    int64_t b = (nitems + 7) / 8;
+    if (b > 148 * 16) b = 148 * 16;
+    ++g_launches;
+    k_split_gather<<<(int)b, 256, 0, s>>>(nitems, stg_cnt, stg_off, stg_row, stg_val, sioff, crow,
+                                          cval);
     return cudaGetLastError();
 }
 
@@ -463,15 +549,19 @@ __global__ void __launch_bounds__(kPruneNT)
     k_prune(int64_t ncols, const int64_t *__restrict__ ccp, const int32_t *__restrict__ crow,
             const float *__restrict__ cval, const int64_t *__restrict__ soff,
             int32_t *__restrict__ srow, float *__restrict__ sval, int64_t *__restrict__ scnt,
-            float *__restrict__ chaos_out, float *chaos_max, PruneParams pp) {
+            float *__restrict__ chaos_out, float *chaos_max, PruneParams pp,
+            const int32_t *__restrict__ colmap, unsigned long long *out_count) {
     __shared__ unsigned hist[256];
     __shared__ int sint[4];
     __shared__ double sred[kPruneNT / 32];
     __shared__ int sscan[kPruneNT / 32];
     const int tid = threadIdx.x;
-    for (int64_t col = blockIdx.x; col < ncols; col += gridDim.x) {
-        const int64_t base = ccp[col];
-        const int nnz = (int)(ccp[col + 1] - base);
+    for (int64_t ci = blockIdx.x; ci < ncols; ci += gridDim.x) {
+        // output column: colmap[ci] (split columns; -1 = skip), else ci
+        const int64_t col = colmap ? (int64_t)colmap[ci] : ci;
+        if (col < 0) continue;
+        const int64_t base = ccp[ci];
+        const int nnz = (int)(ccp[ci + 1] - base);
         const int32_t *rows = crow + base;
         const float *vals = cval + base;
         int mloc = 0;
@@ -543,6 +633,7 @@ __global__ void __launch_bounds__(kPruneNT)
             scnt[col] = kept;
             if (chaos_out) chaos_out[col] = chaos;
             atomic_max_nonneg_float(chaos_max, chaos);
+            if (out_count) atomicAdd(out_count, (unsigned long long)kept);
         }
         __syncthreads();
     }
@@ -551,11 +642,11 @@ __global__ void __launch_bounds__(kPruneNT)
 cudaError_t launch_prune(int64_t ncols, const int64_t *ccp, const int32_t *crow, const float *cval,
                          const int64_t *soff, int32_t *srow, float *sval, int64_t *scnt,
                          float *chaos, float *chaos_max, const PruneParams &pp, int grid,
-                         cudaStream_t s) {
+                         cudaStream_t s, const int32_t *colmap, unsigned long long *out_count) {
     if (ncols <= 0) return cudaSuccess;
     ++g_launches;
     k_prune<<<grid, kPruneNT, 0, s>>>(ncols, ccp, crow, cval, soff, srow, sval, scnt, chaos,
-                                      chaos_max, pp);
+                                      chaos_max, pp, colmap, out_count);
     return cudaGetLastError();
 }
 

@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(NT, (bin_min_blocks<CAP, NT, MODE, GLOBAL, ATO
     __shared__ int sint[4];
     __shared__ double sred[NT / 32];
     __shared__ int sscan[NT / 32];
-    __shared__ int s_col, s_idx, s_ovf;
+    __shared__ int s_col, s_idx, s_ovf, s_pr;
     __shared__ int swi[2][NT / 32];
     __shared__ double swd[4][NT / 32];
     constexpr int W = NT / 32;         // warps = row-range owners
@@ -280,6 +280,7 @@ __global__ void __launch_bounds__(NT, (bin_min_blocks<CAP, NT, MODE, GLOBAL, ATO
             s_idx = idx;
             s_col = idx < count ? a.list[idx] : -1;
             s_ovf = 0;
+            if (MODE == kPart) s_pr = idx < count ? a.item_pr[idx] : 0;
         }
         __syncthreads();
         const int col = s_col;
@@ -322,7 +323,11 @@ __global__ void __launch_bounds__(NT, (bin_min_blocks<CAP, NT, MODE, GLOBAL, ATO
             const int64_t bj = a.cb + col;
             const int64_t q0 = a.bcp[bj], q1 = a.bcp[bj + 1];
             const int64_t nb = q1 - q0;
-            const int g = group_size_for(nb > 0 ? a.flops[col] / (4 * nb) : 0);
+            // a part sees (p1 - p0) / 32 of every segment on average
+            const int64_t fcol = MODE == kPart
+                                     ? a.flops[col] * ((s_pr >> 8) - (s_pr & 0xff)) / kParts
+                                     : a.flops[col];
+            const int g = group_size_for(nb > 0 ? fcol / (4 * nb) : 0);
             const int lane_g = lane & (g - 1);
             const int grp = tid / g;        // group index in the CTA
             const int ngrp = NT / g;
@@ -332,8 +337,16 @@ __global__ void __launch_bounds__(NT, (bin_min_blocks<CAP, NT, MODE, GLOBAL, ATO
                 if (tid < cnt) {
                     const int k = __ldg(a.brow + c0 + tid);
                     const int64_t st = __ldg(a.acp + k);
-                    st_start[tid] = st;
-                    st_k[tid] = (int)(__ldg(a.acp + k + 1) - st);  // segment length
+                    if (MODE == kPart) {
+                        // the part's rows: positions [rowpart[k][p0], rowpart[k][p1]) of A_*k
+                        const int *pk = a.rowpart + (int64_t)k * (kParts + 1);
+                        const int r0 = __ldg(pk + (s_pr & 0xff)), r1 = __ldg(pk + (s_pr >> 8));
+                        st_start[tid] = st + r0;
+                        st_k[tid] = r1 - r0;
+                    } else {
+                        st_start[tid] = st;
+                        st_k[tid] = (int)(__ldg(a.acp + k + 1) - st);  // segment length
+                    }
                     st_b[tid] = __ldg(a.bval + c0 + tid);
                 }
                 __syncthreads();
@@ -541,7 +554,16 @@ __global__ void __launch_bounds__(NT, (bin_min_blocks<CAP, NT, MODE, GLOBAL, ATO
         if (!ok && lane == 0) s_ovf = 1;
         __syncthreads();
         if (s_ovf) {
-            if (tid == 0) a.retry_list[atomicAdd(a.retry_count, 1)] = col;
+            if (tid == 0) {
+                if (MODE == kPart) {
+                    // the whole split column is re-run (once, whichever part overflowed)
+                    a.stg_cnt[idx] = 0;
+                    if (atomicExch(&a.col_flag[col], 1) == 0)
+                        a.retry_list[atomicAdd(a.retry_count, 1)] = col;
+                } else {
+                    a.retry_list[atomicAdd(a.retry_count, 1)] = col;
+                }
+            }
             continue;  // loop head re-syncs before s_col is rewritten
         }
 
@@ -701,6 +723,14 @@ __global__ void __launch_bounds__(NT, (bin_min_blocks<CAP, NT, MODE, GLOBAL, ATO
                                   [](V v) { return (float)v; }, sscan);
                 continue;
             }
+            if (MODE == kPart) {
+                // nnz <= the 7/8 fill limit <= stg_cap
+                const int64_t dst = a.stg_off[idx];
+                sort_write<NT, V>(keys, vals, nnz, (int)cap, a.stg_row + dst, a.stg_val + dst,
+                                  [](V v) { return (float)v; }, sscan);
+                if (tid == 0) a.stg_cnt[idx] = nnz;
+                continue;
+            }
 
     #ifdef MCLX_PROF
             if (tid == 0) PROF_ADD(6, clock64() - prof_e0);  // compaction of the table
@@ -838,6 +868,17 @@ cudaError_t launch_bin(int mode, int bin, const BinArgs &a, int grid, cudaStream
     if (mode == kSym) { MCLX_BIN_SWITCH(kSym, launch_of, a, grid, s) }
     if (mode == kNum) { MCLX_BIN_SWITCH(kNum, launch_of, a, grid, s) }
     MCLX_BIN_SWITCH(kFused, launch_of, a, grid, s)
+}
+
+cudaError_t launch_part(int variant, const BinArgs &a, int grid, cudaStream_t s) {
+    if (variant == 0) return launch_of<kPartCap, kPartThreads, kPart, false, true>(a, grid, s);
+    if (variant == 1) return launch_of<2 * kPartCap, 2 * kPartThreads, kPart, false, true>(a, grid, s);
+    return launch_of<0, kGlobalThreads, kPart, true, true>(a, grid, s);
+}
+int part_occupancy(int variant) {
+    if (variant == 0) return occ_of<kPartCap, kPartThreads, kPart, false, true>();
+    if (variant == 1) return occ_of<2 * kPartCap, 2 * kPartThreads, kPart, false, true>();
+    return occ_of<0, kGlobalThreads, kPart, true, true>();
 }
 
 int bin_occupancy(int mode, int bin) {

@@ -291,6 +291,39 @@ def test_iterate_label_locality():
     assert st["retries"] > 0
 
 
+@pytest.mark.parametrize("graph,min_need,part_need,budget_mb", [
+    ("C2", 600, 0, 0), ("rmat14", 200, 0, 0), ("rmat14", 200, 0, 2), ("C1it1", 100, 0, 0),
+    ("C2", 600, 64, 0), ("rmat14", 200, 16, 0), ("rmat14", 200, 16, 2), ("C1it1", 100, 16, 0)])
+def test_iterate_split_columns(monkeypatch, graph, min_need, part_need, budget_mb):
+    """Row-range split columns (parts stitched, pruned by k_prune), forced onto every
+    column with need > min_need.  part_need > 0 shrinks the parts' target size so the
+    variants with 32 parts of 2x tables and of fp64 global tables run; budget_mb > 0
+    forces many chunks."""
+    monkeypatch.setenv("MCLX_SPLIT_MIN_NEED", str(min_need))
+    if part_need:
+        monkeypatch.setenv("MCLX_SPLIT_PART_NEED", str(part_need))
+    if budget_mb:
+        monkeypatch.setenv("MCLX_SPLIT_BUDGET_MB", str(budget_mb))
+    if graph == "C2":
+        A, params = f32(O.preprocess(synth.config_graph("C2"))), (1e-4, 100, 100, 0.9)
+    elif graph == "rmat14":
+        A, params = f32(O.preprocess(synth.rmat(scale=14, seed=4))), (1e-4, 1100, 1400, 0.9)
+    else:
+        A0 = O.preprocess(synth.planted_partition())
+        A1, _ = O.prune_inflate(O.expand(A0)[0], 1e-4, 1100, 1400, 0.9, 2.0)
+        A, params = f32(A1), (1e-4, 1100, 1400, 0.9)
+    theta, S, R, pct = params
+    ctx = M.Context()  # fresh context: the env knobs are read at creation
+    Ag, st = ctx.iterate(dev(A), M.Params(prune_threshold=theta, select_k=S, recover_k=R,
+                                          recover_pct=pct))
+    Cr, fl = O.expand(A)
+    _, info = O.prune_inflate(Cr, theta, S, R, pct, 2.0)
+    kept_parity(host_mat(Ag), Cr, info, params)
+    assert st["flops"] == int(fl.sum())
+    assert st["chaos"] == pytest.approx(info.chaos.max(), rel=1e-3, abs=1e-5)
+    assert st["bin_cols"][6] > 0
+
+
 @pytest.mark.parametrize("scale", [12, 14])
 def test_rmat_iterate_parity(scale):
     """R-MAT (C4 shape: skewed degrees, hub columns) -- one fused iteration vs the oracle."""
