@@ -116,6 +116,9 @@ typedef struct {
     int64_t split_cols;      /* columns run as row-range parts (counted in bin MCL_NUM_BINS too) */
     int64_t split_items;     /* row-range parts run                                             */
     float split_ms;          /* device time of the split path (included in bin_ms[MCL_NUM_BINS])*/
+    int64_t split_vcols[3];  /* split columns per part variant: 8192-slot shared tables,
+                                16384-slot shared tables, fp64 global tables                    */
+    float split_vms[3];      /* device time per part variant (parts + stitch + prune)           */
 } mcl_stats_t;
 
 /* Allocator callbacks: device memory, stream-ordered.  NULL callbacks select the

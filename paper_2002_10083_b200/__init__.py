@@ -70,11 +70,13 @@ class StatsT(C.Structure):
                 ("bin_ms", C.c_float * (NUM_BINS + 1)), ("bin_nnzb", C.c_int64 * (NUM_BINS + 1)),
                 ("bin_out", C.c_int64 * (NUM_BINS + 1)), ("comm_bytes", C.c_int64),
                 ("peak_partial", C.c_int64), ("split_cols", C.c_int64),
-                ("split_items", C.c_int64), ("split_ms", C.c_float)]
+                ("split_items", C.c_int64), ("split_ms", C.c_float),
+                ("split_vcols", C.c_int64 * 3), ("split_vms", C.c_float * 3)]
 
     def as_dict(self) -> dict:
         d = {k: getattr(self, k) for k, _ in self._fields_}
-        for k in ("bin_cols", "bin_flops", "ms", "bin_ms", "bin_nnzb", "bin_out"):
+        for k in ("bin_cols", "bin_flops", "ms", "bin_ms", "bin_nnzb", "bin_out", "split_vcols",
+                  "split_vms"):
             d[k] = list(d[k])
         return d
 

@@ -39,6 +39,7 @@ struct mcl_ctx {
     cudaEvent_t bev[2 * kAllBins] = {};
     cudaEvent_t pev[6] = {};  // phases of the distributed prune
     cudaEvent_t sev[3] = {};  // SUMMA iteration (ev[] is reused by the stage products)
+    cudaEvent_t vev[2] = {};  // split path, per part variant
     // 2D Sparse-SUMMA grid (mcl_ctx_set_grid): world / row / column communicators
     int pr = 1, pc = 1, rank = 0;
     ncclComm_t world = nullptr, rowc = nullptr, colc = nullptr;
@@ -50,6 +51,7 @@ struct mcl_ctx {
     int64_t split_budget = (int64_t)4 << 30;  // staging bytes per chunk of split parts
     int64_t split_min_need = INT64_MAX;       // MCLX_SPLIT_MIN_NEED: split smaller columns too
     int64_t split_part_need = kPartNeed;      // MCLX_SPLIT_PART_NEED (<= kPartNeed; tests)
+    int64_t fp64_terms = kFp64Terms;          // MCLX_FP64_TERMS (tests)
 };
 
 namespace {
@@ -222,7 +224,7 @@ int cohen(mcl_ctx *c, const Prod &pr, int r, uint64_t seed, float *est, float *k
 // SMs.  A part that overflows flags its column for the next round.
 int run_split(mcl_ctx *c, const Prod &pr, int nsplit, int32_t *split_list,
               const int32_t *split_P, BinArgs a, unsigned long long *out_count,
-              int64_t *nitems_out) {
+              int64_t *nitems_out, mcl_stats_t *st) {
     std::vector<int32_t> hl((size_t)nsplit), hP((size_t)pr.n);
     CK(cudaMemcpyAsync(hl.data(), split_list, sizeof(int32_t) * nsplit, cudaMemcpyDeviceToHost,
                        c->stream));
@@ -230,28 +232,29 @@ int run_split(mcl_ctx *c, const Prod &pr, int nsplit, int32_t *split_list,
                        c->stream));
     CK(cudaStreamSynchronize(c->stream));
     // variant by the virtual part count P (parts sized for T = split_part_need distinct
-    // rows): <= 32 parts of kPartCap slots; 64: 32 parts of 2 kPartCap slots; more: 32
-    // parts with fp64 global tables of 2 P T / 32 slots (load <= 1/2), small enough that
-    // the live tables of all resident parts stay near L2 size
-    auto variant_of = [](int P) { return P <= 32 ? 0 : P == 64 ? 1 : 2; };
-    std::stable_partition(hl.begin(), hl.end(), [&](int32_t col) { return variant_of(hP[col]) == 0; });
-    std::stable_partition(hl.begin(), hl.end(), [&](int32_t col) { return variant_of(hP[col]) <= 1; });
-    const int64_t cap_of[3] = {kPartCap, 2 * kPartCap, 0};
+    // rows): <= 32 parts of kPartCap slots; 64: 32 parts of 2 kPartCap slots; more
+    // (outputs dense in a sizable share of the rows, or long fp64 sums): 32 dense fp64
+    // row tiles (kernels_dense.cu), staging capacity min(part rows, 2 P T / 32 + 256)
+    auto variant_of = [](int P) {
+        return (P & kSplitFp64) ? 3 : P <= 32 ? 0 : P == 64 ? 1 : 2;
+    };
+    for (int v = 0; v < 3; v++)
+        std::stable_partition(hl.begin(), hl.end(), [&](int32_t col) { return variant_of(hP[col]) <= v; });
+    const int64_t cap_of[2] = {kPartCap, 2 * kPartCap};
     std::vector<int64_t> hoff((size_t)nsplit + 1, 0);   // first item of each column
     std::vector<int64_t> hstg;                          // staging offset of each item
-    std::vector<int64_t> hgcap;                         // global table slots of each item
     hstg.reserve((size_t)nsplit * 4 + 1);
     int64_t stg = 0;
     for (int s2 = 0; s2 < nsplit; s2++) {
-        const int P = hP[hl[s2]], v = variant_of(P);
+        const int v = variant_of(hP[hl[s2]]), P = hP[hl[s2]] & ~kSplitFp64;
         const int parts = P < 32 ? P : 32;
         hoff[s2 + 1] = hoff[s2] + parts;
-        const int64_t tcap = v == 2 ? std::max<int64_t>((int64_t)P * c->split_part_need / 16, 1024)
-                                    : cap_of[v];
+        const int64_t prow = (pr.A->nrows + kParts - 1) / kParts + 1;
+        const int64_t dcap = std::min<int64_t>(prow, (int64_t)P * c->split_part_need / 16 + 256);
         for (int q = 0; q < parts; q++) {
             hstg.push_back(stg);
-            stg += tcap - tcap / 8;  // the 7/8 fill limit bounds a part's entries
-            hgcap.push_back(v == 2 ? tcap : 0);
+            // the 7/8 fill limit bounds a hashed part's entries
+            stg += v >= 2 ? dcap : cap_of[v] - cap_of[v] / 8;
         }
     }
     hstg.push_back(stg);
@@ -269,27 +272,20 @@ int run_split(mcl_ctx *c, const Prod &pr, int nsplit, int32_t *split_list,
     }
     cuts.push_back(nsplit);
     const int nchunks = (int)cuts.size() - 1;
-    int64_t chunk_items = 0, chunk_stg = 0, chunk_g = 0;
+    int64_t chunk_items = 0, chunk_stg = 0;
     for (int q = 0; q < nchunks; q++) {
         const int64_t i0 = hoff[cuts[q]], i1 = hoff[cuts[q + 1]];
         chunk_items = std::max(chunk_items, i1 - i0);
         chunk_stg = std::max(chunk_stg, hstg[i1] - hstg[i0]);
-        int64_t g = 0;
-        for (int64_t i = i0; i < i1; i++) g += hgcap[i];
-        chunk_g = std::max(chunk_g, g);
     }
     // device copies: reordered column list, item layout
-    std::vector<int64_t> hgoff((size_t)nitems + 1, 0);
-    for (int64_t i = 0; i < nitems; i++) hgoff[i + 1] = hgoff[i] + hgcap[i];
-    int64_t *ioff, *stg_off, *goff, *stg_cnt, *sioff, *ccp;
-    int32_t *item_col, *item_pr, *stg_row, *crow, *colmap, *gcap;
+    int64_t *ioff, *stg_off, *stg_cnt, *sioff, *ccp;
+    int32_t *item_col, *item_pr, *stg_row, *crow, *colmap;
     float *stg_val, *cval;
     int *ccount;
     void *tmp;
     RC(scratch_t(c, "split_ioff", (size_t)nsplit + 1, &ioff));
     RC(scratch_t(c, "split_stg_off", (size_t)nitems + 1, &stg_off));
-    RC(scratch_t(c, "split_goff", (size_t)nitems + 1, &goff));
-    RC(scratch_t(c, "split_gcap", (size_t)nitems + 1, &gcap));
     RC(scratch_t(c, "split_item_col", (size_t)nitems, &item_col));
     RC(scratch_t(c, "split_item_pr", (size_t)nitems, &item_pr));
     RC(scratch_t(c, "split_counts", (size_t)2 * nchunks, &ccount));
@@ -302,35 +298,41 @@ int run_split(mcl_ctx *c, const Prod &pr, int nsplit, int32_t *split_list,
     RC(scratch_t(c, "split_ccp", (size_t)nsplit + 1, &ccp));
     RC(scratch_t(c, "split_colmap", (size_t)nsplit, &colmap));
     RC(scratch(c, "split_scan_tmp", scan_tmp_bytes(chunk_items + 1), &tmp));
-    int *gkeys = nullptr;
-    double *gvals = nullptr;
-    if (chunk_g > 0) {
-        RC(scratch_t(c, "split_gkeys", (size_t)chunk_g, &gkeys));
-        RC(scratch_t(c, "split_gvals", (size_t)chunk_g, &gvals));
-    }
     std::vector<int> hcnt((size_t)2 * nchunks, 0);
     for (int q = 0; q < nchunks; q++) hcnt[q] = (int)(hoff[cuts[q + 1]] - hoff[cuts[q]]);
-    std::vector<int32_t> hgcap32(hgcap.begin(), hgcap.end());
     CK(cudaMemcpyAsync(split_list, hl.data(), sizeof(int32_t) * nsplit, cudaMemcpyHostToDevice,
                        c->stream));
     CK(cudaMemcpyAsync(ioff, hoff.data(), sizeof(int64_t) * (nsplit + 1), cudaMemcpyHostToDevice,
                        c->stream));
     CK(cudaMemcpyAsync(stg_off, hstg.data(), sizeof(int64_t) * (nitems + 1), cudaMemcpyHostToDevice,
                        c->stream));
-    CK(cudaMemcpyAsync(goff, hgoff.data(), sizeof(int64_t) * (nitems + 1), cudaMemcpyHostToDevice,
-                       c->stream));
-    CK(cudaMemcpyAsync(gcap, hgcap32.data(), sizeof(int32_t) * nitems, cudaMemcpyHostToDevice,
-                       c->stream));
     CK(cudaMemcpyAsync(ccount, hcnt.data(), sizeof(int) * 2 * nchunks, cudaMemcpyHostToDevice,
                        c->stream));
     CK(launch_split_items(nsplit, split_list, split_P, ioff, item_col, item_pr, c->stream));
-    int occ[3];
-    for (int v = 0; v < 3; v++) occ[v] = std::max(1, part_occupancy(v));
+    int occ[4];
+    for (int v = 0; v < 2; v++) occ[v] = std::max(1, part_occupancy(v));
+    occ[2] = std::max(1, dense_part_occupancy(false));
+    occ[3] = std::max(1, dense_part_occupancy(true));
     const int pgrid = (int)std::min<int64_t>(std::max<int64_t>(pr.n, 1), (int64_t)c->sms * 8);
-    for (int q = 0; q < nchunks; q++) {
+    int vprev = -1;
+    for (int q = 0; q <= nchunks; q++) {
+        const int vq = q < nchunks ? variant_of(hP[hl[cuts[q]]]) : -1;
+        if (st && vq != vprev) {  // per-variant device time (chunks are grouped by variant)
+            if (vprev >= 0) {
+                CK(cudaEventRecord(c->vev[1], c->stream));
+                CK(cudaEventSynchronize(c->vev[1]));
+                float ms = 0.f;
+                CK(cudaEventElapsedTime(&ms, c->vev[0], c->vev[1]));
+                st->split_vms[vprev < 3 ? vprev : 2] += ms;
+            }
+            if (vq >= 0) CK(cudaEventRecord(c->vev[0], c->stream));
+        }
+        vprev = vq;
+        if (q == nchunks) break;
         const int s0 = cuts[q], nc = cuts[q + 1] - cuts[q];
         const int64_t item0 = hoff[s0], nit = hoff[cuts[q + 1]] - item0;
-        const int v = variant_of(hP[hl[s0]]);
+        const int v = vq;
+        if (st) st->split_vcols[v < 3 ? v : 2] += nc;
         // staging offsets relative to the chunk: stg_off[i] - stg_off[item0]
         BinArgs ap = a;
         ap.list = item_col + item0;
@@ -341,13 +343,9 @@ int run_split(mcl_ctx *c, const Prod &pr, int nsplit, int32_t *split_list,
         ap.stg_row = stg_row - hstg[item0];
         ap.stg_val = stg_val - hstg[item0];
         ap.stg_cnt = stg_cnt;
-        if (v == 2) {
-            ap.goff = goff + item0;
-            ap.gcap = gcap + item0;
-            ap.gkeys = gkeys - hgoff[item0];
-            ap.gvals = gvals - hgoff[item0];
-        }
-        CK(launch_part(v, ap, (int)std::min<int64_t>(nit, (int64_t)occ[v] * c->sms), c->stream));
+        const int grid = (int)std::min<int64_t>(nit, (int64_t)occ[v] * c->sms);
+        if (v >= 2) CK(launch_dense_part(v == 3, ap, grid, c->stream));
+        else CK(launch_part(v, ap, grid, c->stream));
         CK(launch_scan_i64(stg_cnt, sioff, nit, tmp, c->stream));
         CK(launch_split_stitch(nc, ioff + s0, item0, item_col + item0, sioff, a.col_flag, ccp, colmap,
                                c->stream));
@@ -444,6 +442,7 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
         ca.bin_flops = bflops;
         ca.bin_nnzb = bnnzb;
         ca.colbin = colbin;
+        ca.fp64_terms = c->fp64_terms;
         if (use_split && round < 2) {
             // the exact round stays in the global bin, which cannot overflow
             ca.split_max = INT64_MAX;  // the global-table variant takes any size
@@ -490,7 +489,7 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
             a.col_flag = col_flag;
             CK(cudaEventRecord(c->bev[2 * kNumBins], c->stream));
             int64_t nitems = 0;
-            RC(run_split(c, pr, nsplit, split_list, split_P, a, bout + kNumBins, &nitems));
+            RC(run_split(c, pr, nsplit, split_list, split_P, a, bout + kNumBins, &nitems, st));
             CK(cudaEventRecord(c->bev[2 * kNumBins + 1], c->stream));
             if (st) {
                 float ms = 0.f;
@@ -999,6 +998,7 @@ int mcl_ctx_create(mcl_ctx_t *out, int device, void *stream, mcl_alloc_fn alloc,
     if (const char *e = getenv("MCLX_SPLIT")) c->split = atoi(e) != 0;
     if (const char *e = getenv("MCLX_SPLIT_BUDGET_MB")) c->split_budget = (int64_t)atoll(e) << 20;
     if (const char *e = getenv("MCLX_SPLIT_MIN_NEED")) c->split_min_need = atoll(e);
+    if (const char *e = getenv("MCLX_FP64_TERMS")) c->fp64_terms = atoll(e);
     if (const char *e = getenv("MCLX_SPLIT_PART_NEED"))
         c->split_part_need = std::max<int64_t>(16, std::min<int64_t>(kPartNeed, atoll(e)));
     if (const char *e = getenv("MCLX_GBIN_BUDGET_MB")) c->gbin_budget = (int64_t)atoll(e) << 20;
@@ -1010,6 +1010,7 @@ int mcl_ctx_create(mcl_ctx_t *out, int device, void *stream, mcl_alloc_fn alloc,
     for (int i = 0; i < 2 * kAllBins; i++) cudaEventCreate(&c->bev[i]);
     for (int i = 0; i < 6; i++) cudaEventCreate(&c->pev[i]);
     for (int i = 0; i < 3; i++) cudaEventCreate(&c->sev[i]);
+    for (int i = 0; i < 2; i++) cudaEventCreate(&c->vev[i]);
     for (int m = 0; m < 3; m++)
         for (int b = 0; b < kAllBins; b++) c->occ[m][b] = bin_occupancy(m, b);
     if (cudaGetLastError() != cudaSuccess) {
@@ -1044,6 +1045,8 @@ int mcl_ctx_destroy(mcl_ctx_t c) {
         if (c->pev[i]) cudaEventDestroy(c->pev[i]);
     for (int i = 0; i < 3; i++)
         if (c->sev[i]) cudaEventDestroy(c->sev[i]);
+    for (int i = 0; i < 2; i++)
+        if (c->vev[i]) cudaEventDestroy(c->vev[i]);
     if (c->pin) cudaFreeHost(c->pin);
     delete c;
     return MCL_OK;

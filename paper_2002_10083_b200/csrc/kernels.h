@@ -76,8 +76,16 @@ struct BinArgs {
 constexpr int kPartCap = 8192;
 constexpr int kPartThreads = 512;
 constexpr int kPartNeed = kPartCap / 2;  // distinct rows a part is sized for (load 1/2)
-// part variants: 0 kPartCap-slot shared table, 1 2*kPartCap-slot shared table,
-// 2 fp64 global-memory tables (goff / gcap per item)
+constexpr int kParts = 32;  // row ranges of the rowpart index (k_rowpart)
+// dense bin (kernels_dense.cu): 32 row-tile parts per column, fp64 tiles in shared memory
+constexpr int kDenseThreads = 1024;
+constexpr int kDenseTileBytes = 196608;  // a dense part's tile per pass (192 KB)
+// split_P flag: the column needs fp64 accumulation (more than kFp64Terms segments)
+constexpr int kSplitFp64 = 1 << 30;
+cudaError_t launch_dense_part(bool fp64, const BinArgs &a, int grid, cudaStream_t s);
+int dense_part_occupancy(bool fp64);
+// part variants: 0 kPartCap-slot shared table, 1 2*kPartCap-slot shared table
+// (variants 2 / 3, dense fp32 / fp64 row tiles: launch_dense_part)
 cudaError_t launch_part(int variant, const BinArgs &a, int grid, cudaStream_t s);
 int part_occupancy(int variant);
 
@@ -132,6 +140,7 @@ struct ClassifyArgs {
     int64_t split_max;       // 0 disables
     int64_t split_min;       // also split smaller columns with need > split_min (tests)
     int64_t split_part_need; // distinct rows a part is sized for (kPartNeed)
+    int64_t fp64_terms;      // nnz(B_*j) above which a column accumulates in fp64 (kFp64Terms)
     int *split_count;
     int32_t *split_list;
     int32_t *split_P;

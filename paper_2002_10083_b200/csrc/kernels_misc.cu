@@ -230,7 +230,7 @@ __global__ void k_classify(ClassifyArgs c) {
         const int64_t nb = c.bcp[c.cb + col + 1] - c.bcp[c.cb + col];
         int b = 0;
         while (b < kNumBins && (double)need > c.max_load * bin_cap(b)) b++;
-        if (nb > kFp64Terms) b = kNumBins;
+        if (nb > c.fp64_terms) b = kNumBins;
         if (c.force_bin > b && c.force_bin <= kNumBins) b = c.force_bin;
         if ((b == kNumBins || need > c.split_min) && c.split_max > 0 && need <= c.split_max &&
             c.force_bin < 0) {
@@ -238,6 +238,8 @@ __global__ void k_classify(ClassifyArgs c) {
             // ~kPartNeed distinct rows); P > 32 runs 32 parts with bigger tables
             int P = 2;
             while ((int64_t)P * c.split_part_need < need) P <<= 1;
+            // long sums (T): only the dense fp64 variant accumulates in fp64
+            if (nb > c.fp64_terms) P = (P < 128 ? 128 : P) | kSplitFp64;
             c.split_P[col] = P;
             c.split_list[atomicAdd(c.split_count, 1)] = (int32_t)col;
             if (c.colbin) c.colbin[col] = -1;
@@ -276,7 +278,8 @@ __global__ void k_split_items(int nsplit, const int32_t *split_list, const int32
                               const int64_t *ioff, int32_t *item_col, int32_t *item_pr) {
     for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < nsplit; s += gridDim.x * blockDim.x) {
         const int32_t col = split_list[s];
-        const int P = split_P[col] < 32 ? split_P[col] : 32;
+        const int Pv = split_P[col] & ~kSplitFp64;
+        const int P = Pv < 32 ? Pv : 32;
         const int step = 32 / P;
         const int64_t i0 = ioff[s];
         for (int p = 0; p < P; p++) {
@@ -555,87 +558,14 @@ __global__ void __launch_bounds__(kPruneNT)
     __shared__ int sint[4];
     __shared__ double sred[kPruneNT / 32];
     __shared__ int sscan[kPruneNT / 32];
-    const int tid = threadIdx.x;
     for (int64_t ci = blockIdx.x; ci < ncols; ci += gridDim.x) {
         // output column: colmap[ci] (split columns; -1 = skip), else ci
         const int64_t col = colmap ? (int64_t)colmap[ci] : ci;
         if (col < 0) continue;
         const int64_t base = ccp[ci];
         const int nnz = (int)(ccp[ci + 1] - base);
-        const int32_t *rows = crow + base;
-        const float *vals = cval + base;
-        int mloc = 0;
-        double sloc = 0.0;
-        for (int i = tid; i < nnz; i += kPruneNT) {
-            double v = (double)vals[i];
-            if (v >= pp.theta) {
-                mloc++;
-                sloc += v;
-            }
-        }
-        const int m = block_sum<kPruneNT, int>(mloc, sscan);
-        const double s = block_sum<kPruneNT, double>(sloc, sred);
-        int64_t K;
-        const int br = prune_branch(pp, nnz, m, s, K);
-        uint32_t t = 0;
-        int rowcut = 0, sel;
-        if (br == 0) {
-            sel = 0;
-        } else if (K >= nnz) {
-            sel = 2;
-        } else {
-            radix_select_topk<kPruneNT, float>(rows, vals, nnz, (int)K, t, rowcut, hist, sint);
-            sel = 1;
-        }
-        auto keep = [&](int k, float v) {
-            if (sel == 0) return (double)v >= pp.theta;
-            if (sel == 2) return true;
-            uint32_t b = val_bits(v);
-            return b > t || (b == t && k <= rowcut);
-        };
-        double sv = 0.0, mx = 0.0, sq = 0.0, sr = 0.0;
-        for (int i = tid; i < nnz; i += kPruneNT) {
-            float v = vals[i];
-            if (keep(rows[i], v)) {
-                double d = (double)v;
-                sv += d;
-                mx = d > mx ? d : mx;
-                sq += d * d;
-                sr += pow_r(d, pp);
-            }
-        }
-        sv = block_sum<kPruneNT, double>(sv, sred);
-        mx = block_max<kPruneNT, double>(mx, sred);
-        sq = block_sum<kPruneNT, double>(sq, sred);
-        sr = block_sum<kPruneNT, double>(sr, sred);
-        const int64_t dst = soff[col];
-        int kept = 0;
-        for (int c = 0; c < nnz; c += kPruneNT) {
-            const int i = c + tid;
-            int f = 0;
-            int r = 0;
-            float v = 0.f;
-            if (i < nnz) {
-                r = rows[i];
-                v = vals[i];
-                f = keep(r, v) ? 1 : 0;
-            }
-            int tot;
-            const int pos = block_excl_scan<kPruneNT>(f, sscan, tot);
-            if (f) {
-                srow[dst + kept + pos] = r;
-                sval[dst + kept + pos] = (float)(pow_r((double)v, pp) / sr);
-            }
-            kept += tot;
-        }
-        const float chaos = kept > 0 ? (float)((double)kept * (mx / sv - sq / (sv * sv))) : 0.0f;
-        if (tid == 0) {
-            scnt[col] = kept;
-            if (chaos_out) chaos_out[col] = chaos;
-            atomic_max_nonneg_float(chaos_max, chaos);
-            if (out_count) atomicAdd(out_count, (unsigned long long)kept);
-        }
-        __syncthreads();
+        prune_column<kPruneNT>(crow + base, cval + base, nnz, col, soff, srow, sval, scnt, chaos_out,
+                               chaos_max, out_count, pp, hist, sint, sred, sscan);
     }
 }
 

@@ -39,7 +39,6 @@ __device__ unsigned long long g_prof[12];
 #define PROF_ADD(i, v) ((void)0)
 #endif
 
-constexpr int kParts = 32;  // row ranges of the rowpart index
 constexpr int kItems = 4;   // sub-segment chunks whose gathers a warp keeps in flight
 
 
@@ -872,13 +871,11 @@ cudaError_t launch_bin(int mode, int bin, const BinArgs &a, int grid, cudaStream
 
 cudaError_t launch_part(int variant, const BinArgs &a, int grid, cudaStream_t s) {
     if (variant == 0) return launch_of<kPartCap, kPartThreads, kPart, false, true>(a, grid, s);
-    if (variant == 1) return launch_of<2 * kPartCap, 2 * kPartThreads, kPart, false, true>(a, grid, s);
-    return launch_of<0, kGlobalThreads, kPart, true, true>(a, grid, s);
+    return launch_of<2 * kPartCap, 2 * kPartThreads, kPart, false, true>(a, grid, s);
 }
 int part_occupancy(int variant) {
     if (variant == 0) return occ_of<kPartCap, kPartThreads, kPart, false, true>();
-    if (variant == 1) return occ_of<2 * kPartCap, 2 * kPartThreads, kPart, false, true>();
-    return occ_of<0, kGlobalThreads, kPart, true, true>();
+    return occ_of<2 * kPartCap, 2 * kPartThreads, kPart, false, true>();
 }
 
 int bin_occupancy(int mode, int bin) {

@@ -646,4 +646,91 @@ __device__ __forceinline__ void atomic_max_nonneg_float(float *addr, float v) {
     atomicMax(reinterpret_cast<int *>(addr), __float_as_int(v));
 }
 
+// Alg. 1 lines 4-5 on one unpruned column (rows ascending, in global memory, read by the
+// whole CTA): threshold stats, branch (Q5, Q7, Q8), exact top-K by radix select,
+// renormalise + chaos (Q9), Hadamard power r and renormalise (Q1).  The kept
+// entries are extracted in row order with a block scan, so the output stays sorted.
+// Writes srow/sval at soff[col], scnt[col], chaos_out[col] (if given) and folds the
+// chaos into *chaos_max and the kept count into *out_count (if given).  All NT threads call.
+template <int NT>
+__device__ void prune_column(const int32_t *rows, const float *vals, int nnz, int64_t col,
+                             const int64_t *soff, int32_t *srow, float *sval, int64_t *scnt,
+                             float *chaos_out, float *chaos_max, unsigned long long *out_count,
+                             const PruneParams &pp, unsigned *hist, int *sint, double *sred,
+                             int *sscan) {
+    const int tid = threadIdx.x;
+    int mloc = 0;
+    double sloc = 0.0;
+    for (int i = tid; i < nnz; i += NT) {
+        double v = (double)vals[i];
+        if (v >= pp.theta) {
+            mloc++;
+            sloc += v;
+        }
+    }
+    const int m = block_sum<NT, int>(mloc, sscan);
+    const double s = block_sum<NT, double>(sloc, sred);
+    int64_t K;
+    const int br = prune_branch(pp, nnz, m, s, K);
+    uint32_t t = 0;
+    int rowcut = 0, sel;
+    if (br == 0) {
+        sel = 0;
+    } else if (K >= nnz) {
+        sel = 2;
+    } else {
+        radix_select_topk<NT, float>(rows, vals, nnz, (int)K, t, rowcut, hist, sint);
+        sel = 1;
+    }
+    auto keep = [&](int k, float v) {
+        if (sel == 0) return (double)v >= pp.theta;
+        if (sel == 2) return true;
+        uint32_t b = val_bits(v);
+        return b > t || (b == t && k <= rowcut);
+    };
+    double sv = 0.0, mx = 0.0, sq = 0.0, sr = 0.0;
+    for (int i = tid; i < nnz; i += NT) {
+        float v = vals[i];
+        if (keep(rows[i], v)) {
+            double d = (double)v;
+            sv += d;
+            mx = d > mx ? d : mx;
+            sq += d * d;
+            sr += pow_r(d, pp);
+        }
+    }
+    sv = block_sum<NT, double>(sv, sred);
+    mx = block_max<NT, double>(mx, sred);
+    sq = block_sum<NT, double>(sq, sred);
+    sr = block_sum<NT, double>(sr, sred);
+    const int64_t dst = soff[col];
+    int kept = 0;
+    for (int c = 0; c < nnz; c += NT) {
+        const int i = c + tid;
+        int f = 0;
+        int r = 0;
+        float v = 0.f;
+        if (i < nnz) {
+            r = rows[i];
+            v = vals[i];
+            f = keep(r, v) ? 1 : 0;
+        }
+        int tot;
+        const int pos = block_excl_scan<NT>(f, sscan, tot);
+        if (f) {
+            srow[dst + kept + pos] = r;
+            sval[dst + kept + pos] = (float)(pow_r((double)v, pp) / sr);
+        }
+        kept += tot;
+    }
+    const float chaos = kept > 0 ? (float)((double)kept * (mx / sv - sq / (sv * sv))) : 0.0f;
+    if (tid == 0) {
+        scnt[col] = kept;
+        if (chaos_out) chaos_out[col] = chaos;
+        atomic_max_nonneg_float(chaos_max, chaos);
+        if (out_count) atomicAdd(out_count, (unsigned long long)kept);
+    }
+    __syncthreads();
+}
+
 }  // namespace mclx

@@ -291,15 +291,20 @@ def test_iterate_label_locality():
     assert st["retries"] > 0
 
 
-@pytest.mark.parametrize("graph,min_need,part_need,budget_mb", [
-    ("C2", 600, 0, 0), ("rmat14", 200, 0, 0), ("rmat14", 200, 0, 2), ("C1it1", 100, 0, 0),
-    ("C2", 600, 64, 0), ("rmat14", 200, 16, 0), ("rmat14", 200, 16, 2), ("C1it1", 100, 16, 0)])
-def test_iterate_split_columns(monkeypatch, graph, min_need, part_need, budget_mb):
+@pytest.mark.parametrize("graph,min_need,part_need,budget_mb,fp64_terms", [
+    ("C2", 600, 0, 0, 0), ("rmat14", 200, 0, 0, 0), ("rmat14", 200, 0, 2, 0),
+    ("C1it1", 100, 0, 0, 0), ("C2", 600, 64, 0, 0), ("rmat14", 200, 16, 0, 0),
+    ("rmat14", 200, 16, 2, 0), ("C1it1", 100, 16, 0, 0), ("C2", 600, 0, 0, 64),
+    ("rmat14", 200, 0, 0, 32)])
+def test_iterate_split_columns(monkeypatch, graph, min_need, part_need, budget_mb, fp64_terms):
     """Row-range split columns (parts stitched, pruned by k_prune), forced onto every
     column with need > min_need.  part_need > 0 shrinks the parts' target size so the
-    variants with 32 parts of 2x tables and of fp64 global tables run; budget_mb > 0
+    variants with 32 parts of 2x tables and of dense fp32 row tiles run; fp64_terms > 0
+    lowers the long-sum threshold so columns run as dense fp64 tiles; budget_mb > 0
     forces many chunks."""
     monkeypatch.setenv("MCLX_SPLIT_MIN_NEED", str(min_need))
+    if fp64_terms:
+        monkeypatch.setenv("MCLX_FP64_TERMS", str(fp64_terms))
     if part_need:
         monkeypatch.setenv("MCLX_SPLIT_PART_NEED", str(part_need))
     if budget_mb:

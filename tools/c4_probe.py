@@ -22,7 +22,8 @@ print(f"scale {scale}: n={A.ncols} nnz={A.nnz} flops={st['flops']:.3e} fused ms=
 print("bin_cols ", st["bin_cols"])
 print("bin_flops", [f"{x:.2e}" for x in st["bin_flops"]])
 print("bin_ms   ", [round(x, 1) for x in st["bin_ms"]])
-print(f"split: cols {st['split_cols']} items {st['split_items']} ms {st['split_ms']:.1f} retries {st['retries']}")
+print(f"split: cols {st['split_cols']} items {st['split_items']} ms {st['split_ms']:.1f} retries {st['retries']}"
+      f" per variant cols {st['split_vcols']} ms {[round(x, 1) for x in st['split_vms']]}")
 # flops per column on the host (f_j = sum over k in A_*j of nnz(A_*k))
 cp, rw, _ = A.to_host()
 deg = np.diff(cp)
