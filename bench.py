@@ -334,38 +334,66 @@ def run_gpu(args):
             "alg_bytes_formula": "8*flops_bin + 24*nnz(B cols of bin) + 8*kept_out + 16*cols"}
 
     # ---- e2e: host buffers in, host buffers out, through the public API.  Pinned host
-    # buffers are allocated once, outside the timed region; every step copies A_0 in,
-    # runs mcl_iterate and copies A_1 (col_ptr, rows, vals) back.
+    # buffers are allocated once, outside the timed region; every step copies this rank's
+    # operand (A_0, or its SUMMA block / column range) in, runs the iteration and copies
+    # this rank's result block (col_ptr, rows, vals) back.  Time: max over ranks; bytes:
+    # summed over ranks.
     e2e = None
-    if world == 1 and args.e2e_steps > 0:
+    if args.e2e_steps > 0:
         hc = A.colptr.cpu().pin_memory()
         hr = A.rows.cpu().pin_memory()
         hv = A.vals.cpu().pin_memory()
         h2d = hc.numel() * 8 + hr.numel() * 4 + hv.numel() * 4
-        probe, _ = ctx.iterate(A, params)
-        cap = int(probe.nnz * 1.25) + 1024
-        oc = torch.empty(probe.colptr.numel(), dtype=torch.int64, pin_memory=True)
+
+        def result_block(out):
+            if mode == "colpart":  # this rank's columns of the gathered iterate
+                c = out.colptr[b: e + 1]
+                return c - c[0], out.rows[int(c[0]): int(c[-1])], out.vals[int(c[0]): int(c[-1])]
+            return out.colptr, out.rows, out.vals
+
+        probe, _ = step()
+        pc_, pr_, pv_ = result_block(probe)
+        cap = int(pr_.numel() * 1.25) + 1024
+        oc = torch.empty(pc_.numel(), dtype=torch.int64, pin_memory=True)
         orw = torch.empty(cap, dtype=torch.int32, pin_memory=True)
         ov = torch.empty(cap, dtype=torch.float32, pin_memory=True)
-        del probe
+        del probe, pc_, pr_, pv_
         d2h = 0
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(args.e2e_steps):
             Ah = M.CSC(A.nrows, A.ncols, hc.to(dev, non_blocking=True), hr.to(dev, non_blocking=True),
-                       hv.to(dev, non_blocking=True))
-            out, _ = ctx.iterate(Ah, params)
-            nz = out.nnz
-            oc.copy_(out.colptr, non_blocking=True)
-            orw[:nz].copy_(out.rows, non_blocking=True)
-            ov[:nz].copy_(out.vals, non_blocking=True)
-            d2h = oc.numel() * 8 + nz * 8
-            del out, Ah
+                       hv.to(dev, non_blocking=True), row0=A.row0, col0=A.col0, n_global=A.n_global)
+            if mode == "fused":
+                out, _ = ctx.iterate(Ah, params)
+            elif mode == "summa":
+                out, _ = ctx.summa_iterate(Ah, params)
+            else:
+                blk, _ = ctx.iterate(Ah, params, cols=(b, e))
+                out = allgather_csc(dist, M, blk, n, Ah.nrows, dev)
+            c_, r_, v_ = result_block(out)
+            nz = r_.numel()
+            if nz > orw.numel():
+                raise RuntimeError("e2e: result larger than the preallocated host buffer")
+            oc[: c_.numel()].copy_(c_, non_blocking=True)
+            orw[:nz].copy_(r_, non_blocking=True)
+            ov[:nz].copy_(v_, non_blocking=True)
+            d2h = c_.numel() * 8 + nz * 8
+            del out, Ah, c_, r_, v_
         e1.record(stream)
         torch.cuda.synchronize()
         e2e_ms = e0.elapsed_time(e1) / args.e2e_steps
+        if world > 1:
+            t = torch.tensor([e2e_ms, float(h2d), float(d2h)], dtype=torch.float64, device=dev)
+            tl = [torch.zeros_like(t) for _ in range(world)]
+            dist.all_gather(tl, t)
+            e2e_ms = max(float(x[0]) for x in tl)
+            h2d = sum(float(x[1]) for x in tl)
+            d2h = sum(float(x[2]) for x in tl)
         e2e = {"value": flops_total / (e2e_ms / 1e3) / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": e2e_ms}
