@@ -141,8 +141,8 @@ def oracle_sample(A, target_flops: float, seed: int, params: dict):
     return float(f.sum()), dt, len(cols)
 
 
-def workload_name(cfg, n, nnz):
-    return f"{cfg} (SURVEY §8(d)) n={n} nnz(A0)={nnz}, MCL iteration 0, fused mcl_iterate"
+def workload_name(cfg, n, nnz, it=0):
+    return (f"{cfg} (SURVEY §8(d)) n={n} nnz(A{it})={nnz}, MCL iteration {it}, fused mcl_iterate")
 
 
 def run_reference(args):
@@ -248,9 +248,11 @@ def run_gpu(args):
     ctx = M.context()
     A = ctx.preprocess(Gd)
     del Gd
+    params = M.Params(**CONFIG_PARAMS[args.config])
+    for _ in range(args.iters):  # untimed: the timed step runs iteration `iters` (A_iters)
+        A, _ = ctx.iterate(A, params)
     n = A.ncols
     nnz0 = A.nnz
-    params = M.Params(**CONFIG_PARAMS[args.config])
     b = (n * rank) // world
     e = (n * (rank + 1)) // world
     mode = "fused" if world == 1 else args.mode
@@ -326,7 +328,8 @@ def run_gpu(args):
     achieved = alg_bytes / (bin_ms[dom] / 1e3) / 1e9 if bin_ms[dom] > 0 else 0.0
     peak, peak_src = measured_peaks()
     kname = f"k_bin<fused,bin{dom}>"
-    traffic = load_traffic(f"{args.config}:{kname}")
+    it_tag = "" if args.iters == 0 else f"-it{args.iters}"
+    traffic = load_traffic(f"{args.config}{it_tag}:{kname}")
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic, "kernel": kname,
             "kernel_ms": bin_ms[dom], "share_of_step": bin_ms[dom] / (ms_per_step),
@@ -415,7 +418,7 @@ def run_gpu(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
-            "config": {"workload": workload_name(args.config, n, nnz0), "config": args.config,
+            "config": {"workload": workload_name(args.config, n, nnz0, args.iters), "config": args.config,
                        "global_batch": n, "flops_per_step": flops_total,
                        "nnz_out": int(s0["nnz_out"]) if world == 1 else None,
                        "parallelism": "1 GPU" if world == 1 else (
@@ -432,6 +435,12 @@ def run_gpu(args):
                        "ms_raw": s0["ms"],
                        "bin_cols": s0["bin_cols"], "bin_ms": bin_ms,
                        "bin_flops": s0["bin_flops"], "retries": int(s0["retries"]),
+                       "split": {"cols": int(s0["split_cols"]), "items": int(s0["split_items"]),
+                                 "ms": s0["split_ms"],
+                                 "variant_cols": s0["split_vcols"],
+                                 "variant_ms": s0["split_vms"],
+                                 "variants": ["hashed 8192-slot parts", "hashed 16384-slot parts",
+                                              "dense row tiles"]},
                        "step_ms_min": min(step_ms), "step_ms_max": max(step_ms)},
             "roofline": roof,
             "cpu_baseline": cpu,
@@ -453,6 +462,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C3", choices=list(CONFIG_PARAMS))
     ap.add_argument("--scale", type=float, default=1.0)
+    ap.add_argument("--iters", type=int, default=0,
+                    help="untimed MCL iterations before the timed one (1: C3's heaviest, it1)")
     ap.add_argument("--mode", default="summa", choices=["colpart", "summa"],
                     help="N>1: the 2D Sparse-SUMMA (default) or column partition + all-gather")
     ap.add_argument("--grid", default=None, help="pr x pc for --mode summa, e.g. 2x2 (default "

@@ -43,6 +43,8 @@ struct mcl_ctx {
     // 2D Sparse-SUMMA grid (mcl_ctx_set_grid): world / row / column communicators
     int pr = 1, pc = 1, rank = 0;
     ncclComm_t world = nullptr, rowc = nullptr, colc = nullptr;
+    cudaStream_t cstream = nullptr;          // SUMMA stage broadcasts (pipelined)
+    cudaEvent_t qev[5] = {};                 // ready[2], free[2], start
     int64_t gbin_budget = (int64_t)32 << 30;  // bytes of fp64 global-bin tables live at once
     float alpha = 1.2f;     // table sizing: need = alpha * Cohen estimate + 16
     float max_load = 0.5f;  // bin when need <= max_load * cap
@@ -52,6 +54,7 @@ struct mcl_ctx {
     int64_t split_min_need = INT64_MAX;       // MCLX_SPLIT_MIN_NEED: split smaller columns too
     int64_t split_part_need = kPartNeed;      // MCLX_SPLIT_PART_NEED (<= kPartNeed; tests)
     int64_t fp64_terms = kFp64Terms;          // MCLX_FP64_TERMS (tests)
+    bool split_private = true;                // MCLX_SPLIT_PRIVATE=0: P <= 4 parts shared-table too
 };
 
 namespace {
@@ -235,18 +238,25 @@ int run_split(mcl_ctx *c, const Prod &pr, int nsplit, int32_t *split_list,
     // rows): <= 32 parts of kPartCap slots; 64: 32 parts of 2 kPartCap slots; more
     // (outputs dense in a sizable share of the rows, or long fp64 sums): 32 dense fp64
     // row tiles (kernels_dense.cu), staging capacity min(part rows, 2 P T / 32 + 256)
-    auto variant_of = [](int P) {
-        return (P & kSplitFp64) ? 3 : P <= 32 ? 0 : P == 64 ? 1 : 2;
+    // variants: 4 (P <= 16: private row-range slices, 8 warps over the part's >= 8 rowparts
+    // of the 128-way index), 0 (P = 32, or MCLX_SPLIT_PRIVATE=0: CTA-shared tables), 1, 2, 3
+    auto variant_of = [&](int Pf) {
+        const int P = Pf & ~(kSplitFp64 | kSplitShared);
+        return (Pf & kSplitFp64) ? 3
+               : P <= 16 && c->split_private && !(Pf & kSplitShared) ? 4
+               : P <= 32 ? 0 : P == 64 ? 1 : 2;
     };
-    for (int v = 0; v < 3; v++)
-        std::stable_partition(hl.begin(), hl.end(), [&](int32_t col) { return variant_of(hP[col]) <= v; });
+    const int vorder[5] = {4, 0, 1, 2, 3};
+    for (int o = 4; o >= 0; o--)  // stable: variant order 4, 0, 1, 2, 3; columns keep their order
+        std::stable_partition(hl.begin(), hl.end(),
+                              [&](int32_t col) { return variant_of(hP[col]) == vorder[o]; });
     const int64_t cap_of[2] = {kPartCap, 2 * kPartCap};
     std::vector<int64_t> hoff((size_t)nsplit + 1, 0);   // first item of each column
     std::vector<int64_t> hstg;                          // staging offset of each item
     hstg.reserve((size_t)nsplit * 4 + 1);
     int64_t stg = 0;
     for (int s2 = 0; s2 < nsplit; s2++) {
-        const int v = variant_of(hP[hl[s2]]), P = hP[hl[s2]] & ~kSplitFp64;
+        const int v = variant_of(hP[hl[s2]]), P = hP[hl[s2]] & ~(kSplitFp64 | kSplitShared);
         const int parts = P < 32 ? P : 32;
         hoff[s2 + 1] = hoff[s2] + parts;
         const int64_t prow = (pr.A->nrows + kParts - 1) / kParts + 1;
@@ -254,7 +264,8 @@ int run_split(mcl_ctx *c, const Prod &pr, int nsplit, int32_t *split_list,
         for (int q = 0; q < parts; q++) {
             hstg.push_back(stg);
             // the 7/8 fill limit bounds a hashed part's entries
-            stg += v >= 2 ? dcap : cap_of[v] - cap_of[v] / 8;
+            const int64_t tc = v == 1 ? cap_of[1] : cap_of[0];
+            stg += (v == 2 || v == 3) ? dcap : tc - tc / 8;
         }
     }
     hstg.push_back(stg);
@@ -309,8 +320,19 @@ int run_split(mcl_ctx *c, const Prod &pr, int nsplit, int32_t *split_list,
     CK(cudaMemcpyAsync(ccount, hcnt.data(), sizeof(int) * 2 * nchunks, cudaMemcpyHostToDevice,
                        c->stream));
     CK(launch_split_items(nsplit, split_list, split_P, ioff, item_col, item_pr, c->stream));
-    int occ[4];
+    bool any_private = false;
+    for (int s2 = 0; s2 < nsplit && !any_private; s2++) any_private = variant_of(hP[hl[s2]]) == 4;
+    if (any_private) {  // the 128-way row index of A for private-slice parts
+        int *rp_fine;
+        RC(scratch_t(c, "rowpart_fine", (size_t)std::max<int64_t>(pr.A->ncols, 1) * (kFineParts + 1),
+                     &rp_fine));
+        CK(launch_rowpart(pr.A->ncols, pr.A->col_ptr, pr.A->row_idx, pr.A->nrows, rp_fine, c->stream,
+                          kFineParts));
+        a.rowpart_fine = rp_fine;
+    }
+    int occ[5];
     for (int v = 0; v < 2; v++) occ[v] = std::max(1, part_occupancy(v));
+    occ[4] = std::max(1, part_occupancy(4));
     occ[2] = std::max(1, dense_part_occupancy(false));
     occ[3] = std::max(1, dense_part_occupancy(true));
     const int pgrid = (int)std::min<int64_t>(std::max<int64_t>(pr.n, 1), (int64_t)c->sms * 8);
@@ -323,7 +345,7 @@ int run_split(mcl_ctx *c, const Prod &pr, int nsplit, int32_t *split_list,
                 CK(cudaEventSynchronize(c->vev[1]));
                 float ms = 0.f;
                 CK(cudaEventElapsedTime(&ms, c->vev[0], c->vev[1]));
-                st->split_vms[vprev < 3 ? vprev : 2] += ms;
+                st->split_vms[vprev == 4 ? 0 : vprev < 3 ? vprev : 2] += ms;
             }
             if (vq >= 0) CK(cudaEventRecord(c->vev[0], c->stream));
         }
@@ -332,7 +354,7 @@ int run_split(mcl_ctx *c, const Prod &pr, int nsplit, int32_t *split_list,
         const int s0 = cuts[q], nc = cuts[q + 1] - cuts[q];
         const int64_t item0 = hoff[s0], nit = hoff[cuts[q + 1]] - item0;
         const int v = vq;
-        if (st) st->split_vcols[v < 3 ? v : 2] += nc;
+        if (st) st->split_vcols[v == 4 ? 0 : v < 3 ? v : 2] += nc;
         // staging offsets relative to the chunk: stg_off[i] - stg_off[item0]
         BinArgs ap = a;
         ap.list = item_col + item0;
@@ -344,7 +366,7 @@ int run_split(mcl_ctx *c, const Prod &pr, int nsplit, int32_t *split_list,
         ap.stg_val = stg_val - hstg[item0];
         ap.stg_cnt = stg_cnt;
         const int grid = (int)std::min<int64_t>(nit, (int64_t)occ[v] * c->sms);
-        if (v >= 2) CK(launch_dense_part(v == 3, ap, grid, c->stream));
+        if (v == 2 || v == 3) CK(launch_dense_part(v == 3, ap, grid, c->stream));
         else CK(launch_part(v, ap, grid, c->stream));
         CK(launch_scan_i64(stg_cnt, sioff, nit, tmp, c->stream));
         CK(launch_split_stitch(nc, ioff + s0, item0, item_col + item0, sioff, a.col_flag, ccp, colmap,
@@ -999,6 +1021,7 @@ int mcl_ctx_create(mcl_ctx_t *out, int device, void *stream, mcl_alloc_fn alloc,
     if (const char *e = getenv("MCLX_SPLIT_BUDGET_MB")) c->split_budget = (int64_t)atoll(e) << 20;
     if (const char *e = getenv("MCLX_SPLIT_MIN_NEED")) c->split_min_need = atoll(e);
     if (const char *e = getenv("MCLX_FP64_TERMS")) c->fp64_terms = atoll(e);
+    if (const char *e = getenv("MCLX_SPLIT_PRIVATE")) c->split_private = atoi(e) != 0;
     if (const char *e = getenv("MCLX_SPLIT_PART_NEED"))
         c->split_part_need = std::max<int64_t>(16, std::min<int64_t>(kPartNeed, atoll(e)));
     if (const char *e = getenv("MCLX_GBIN_BUDGET_MB")) c->gbin_budget = (int64_t)atoll(e) << 20;
@@ -1047,6 +1070,9 @@ int mcl_ctx_destroy(mcl_ctx_t c) {
         if (c->sev[i]) cudaEventDestroy(c->sev[i]);
     for (int i = 0; i < 2; i++)
         if (c->vev[i]) cudaEventDestroy(c->vev[i]);
+    for (int i = 0; i < 5; i++)
+        if (c->qev[i]) cudaEventDestroy(c->qev[i]);
+    if (c->cstream) cudaStreamDestroy(c->cstream);
     if (c->pin) cudaFreeHost(c->pin);
     delete c;
     return MCL_OK;
@@ -1448,6 +1474,10 @@ int mcl_ctx_set_grid(mcl_ctx_t c, int pr, int pc, int rank, const unsigned char 
     const int gi = rank / pc, gj = rank % pc;
     NC(ncclCommSplit(c->world, gi, gj, &c->rowc, nullptr));
     NC(ncclCommSplit(c->world, gj, gi, &c->colc, nullptr));
+    if (!c->cstream) {
+        CK(cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking));
+        for (int i = 0; i < 5; i++) CK(cudaEventCreateWithFlags(&c->qev[i], cudaEventDisableTiming));
+    }
     c->pr = pr;
     c->pc = pc;
     c->rank = rank;
@@ -1573,60 +1603,93 @@ int mcl_summa_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, 
                        c->stream));
     CK(cudaStreamSynchronize(c->stream));
 
-    // ---- stages: broadcast panels, local product, Alg. 2 binary merge
+    // ---- stages: broadcast panels, local product, Alg. 2 binary merge.
+    // Pipelined: the panels of stage q+1 are prepared and broadcast on the comm stream
+    // (double-buffered) while stage q's product runs on the compute stream.
+    std::vector<int64_t> a0s((size_t)s, 0);  // A-panel offsets in my block (owner stages)
+    for (int q = 0; q < s; q++) {
+        const int64_t k0 = cut(n, s, q);
+        if ((int64_t)q * pc / s == gj) RC(readback(c, A->col_ptr + (k0 - A->col0), sizeof(int64_t), &a0s[q]));
+    }
+    struct Panels {
+        int64_t *acp, *bcp, *first, *cnt;
+        int32_t *arow, *brow;
+        float *aval, *bval;
+    } buf[2];
+    int64_t max_a = 1, max_b = 1, max_k = 1;
+    for (int q = 0; q < s; q++) {
+        const int ca = (int)((int64_t)q * pc / s), rb = (int)((int64_t)q * pr / s);
+        max_a = std::max(max_a, table[(size_t)2 * s * (gi * pc + ca) + 2 * q]);
+        max_b = std::max(max_b, table[(size_t)2 * s * (rb * pc + gj) + 2 * q + 1]);
+        max_k = std::max(max_k, cut(n, s, q + 1) - cut(n, s, q));
+    }
+    for (int i = 0; i < 2; i++) {
+        const std::string t = std::to_string(i);
+        RC(scratch_t(c, ("pa_cp" + t).c_str(), (size_t)max_k + 1, &buf[i].acp));
+        RC(scratch_t(c, ("pa_row" + t).c_str(), (size_t)max_a, &buf[i].arow));
+        RC(scratch_t(c, ("pa_val" + t).c_str(), (size_t)max_a, &buf[i].aval));
+        RC(scratch_t(c, ("pb_cp" + t).c_str(), (size_t)nj + 1, &buf[i].bcp));
+        RC(scratch_t(c, ("pb_row" + t).c_str(), (size_t)max_b, &buf[i].brow));
+        RC(scratch_t(c, ("pb_val" + t).c_str(), (size_t)max_b, &buf[i].bval));
+        RC(scratch_t(c, ("pb_first" + t).c_str(), (size_t)std::max<int64_t>(nj, 1), &buf[i].first));
+        RC(scratch_t(c, ("pb_cnt" + t).c_str(), (size_t)std::max<int64_t>(nj, 1), &buf[i].cnt));
+    }
+    cudaStream_t cs = c->cstream;
+    CK(cudaEventRecord(c->qev[4], c->stream));  // A, bcp_own ready
+    CK(cudaStreamWaitEvent(cs, c->qev[4], 0));
+    auto issue_comm = [&](int q) -> int {
+        const int64_t k0 = cut(n, s, q), k1 = cut(n, s, q + 1), kq = k1 - k0;
+        const int ca = (int)((int64_t)q * pc / s), rb = (int)((int64_t)q * pr / s);
+        const int64_t nnzA = table[(size_t)2 * s * (gi * pc + ca) + 2 * q];
+        const int64_t nnzB = table[(size_t)2 * s * (rb * pc + gj) + 2 * q + 1];
+        Panels &P = buf[q & 1];
+        if (q >= 2) CK(cudaStreamWaitEvent(cs, c->qev[2 + (q & 1)], 0));  // product q-2 done
+        if (ca == gj) {
+            CK(launch_rebase_colptr(kq + 1, A->col_ptr + (k0 - A->col0), P.acp, cs));
+            if (nnzA) {
+                CK(cudaMemcpyAsync(P.arow, A->row_idx + a0s[q], sizeof(int32_t) * nnzA,
+                                   cudaMemcpyDeviceToDevice, cs));
+                CK(cudaMemcpyAsync(P.aval, A->val + a0s[q], sizeof(float) * nnzA,
+                                   cudaMemcpyDeviceToDevice, cs));
+            }
+        }
+        if (rb == gi) {
+            const int64_t *ocp = bcp_own + (int64_t)q * (nj + 1);
+            CK(launch_rowslice_count(nj, A->col_ptr, A->row_idx, k0 - A->row0, k1 - A->row0, P.first,
+                                     P.cnt, cs));
+            CK(cudaMemcpyAsync(P.bcp, ocp, sizeof(int64_t) * (nj + 1), cudaMemcpyDeviceToDevice, cs));
+            CK(launch_rowslice_copy(nj, P.first, P.bcp, A->row_idx, A->val, k0 - A->row0, P.brow,
+                                    P.bval, cs));
+        }
+        NC(ncclGroupStart());
+        NC(ncclBroadcast(P.acp, P.acp, kq + 1, ncclInt64, ca, c->rowc, cs));
+        if (nnzA) {
+            NC(ncclBroadcast(P.arow, P.arow, nnzA, ncclInt32, ca, c->rowc, cs));
+            NC(ncclBroadcast(P.aval, P.aval, nnzA, ncclFloat32, ca, c->rowc, cs));
+        }
+        NC(ncclBroadcast(P.bcp, P.bcp, nj + 1, ncclInt64, rb, c->colc, cs));
+        if (nnzB) {
+            NC(ncclBroadcast(P.brow, P.brow, nnzB, ncclInt32, rb, c->colc, cs));
+            NC(ncclBroadcast(P.bval, P.bval, nnzB, ncclFloat32, rb, c->colc, cs));
+        }
+        NC(ncclGroupEnd());
+        CK(cudaEventRecord(c->qev[q & 1], cs));  // panels of stage q ready
+        return MCL_OK;
+    };
     std::vector<mcl_csc_t> stack;
     int64_t comm_bytes = 0, peak_partial = 0, live_partial = 0, flops = 0;
     float bin_ms[kNumBins + 1] = {};
     int64_t bin_flops[kNumBins + 1] = {}, bin_cols[kNumBins + 1] = {}, bin_nnzb[kNumBins + 1] = {},
             bin_out[kNumBins + 1] = {};
-    int rc = MCL_OK;
+    int rc = issue_comm(0);
     for (int q = 0; q < s && rc == MCL_OK; q++) {
+        if (q + 1 < s && (rc = issue_comm(q + 1)) != MCL_OK) break;
         const int64_t k0 = cut(n, s, q), k1 = cut(n, s, q + 1), kq = k1 - k0;
         const int ca = (int)((int64_t)q * pc / s), rb = (int)((int64_t)q * pr / s);
         const int64_t nnzA = table[(size_t)2 * s * (gi * pc + ca) + 2 * q];
         const int64_t nnzB = table[(size_t)2 * s * (rb * pc + gj) + 2 * q + 1];
-        int64_t *pacp, *pbcp;
-        int32_t *parow, *pbrow;
-        float *paval, *pbval;
-        RC(scratch_t(c, "pa_cp", (size_t)kq + 1, &pacp));
-        RC(scratch_t(c, "pa_row", (size_t)std::max<int64_t>(nnzA, 1), &parow));
-        RC(scratch_t(c, "pa_val", (size_t)std::max<int64_t>(nnzA, 1), &paval));
-        RC(scratch_t(c, "pb_cp", (size_t)nj + 1, &pbcp));
-        RC(scratch_t(c, "pb_row", (size_t)std::max<int64_t>(nnzB, 1), &pbrow));
-        RC(scratch_t(c, "pb_val", (size_t)std::max<int64_t>(nnzB, 1), &pbval));
-        if (ca == gj) {
-            const int64_t *cps = A->col_ptr + (k0 - A->col0);
-            CK(launch_rebase_colptr(kq + 1, cps, pacp, c->stream));
-            int64_t a0 = 0;
-            RC(readback(c, cps, sizeof(int64_t), &a0));
-            if (nnzA) {
-                CK(cudaMemcpyAsync(parow, A->row_idx + a0, sizeof(int32_t) * nnzA,
-                                   cudaMemcpyDeviceToDevice, c->stream));
-                CK(cudaMemcpyAsync(paval, A->val + a0, sizeof(float) * nnzA, cudaMemcpyDeviceToDevice,
-                                   c->stream));
-            }
-        }
-        if (rb == gi) {
-            const int64_t *ocp = bcp_own + (int64_t)q * (nj + 1);
-            CK(launch_rowslice_count(nj, A->col_ptr, A->row_idx, k0 - A->row0, k1 - A->row0, first,
-                                     cnt, c->stream));
-            CK(cudaMemcpyAsync(pbcp, ocp, sizeof(int64_t) * (nj + 1), cudaMemcpyDeviceToDevice,
-                               c->stream));
-            CK(launch_rowslice_copy(nj, first, pbcp, A->row_idx, A->val, k0 - A->row0, pbrow, pbval,
-                                    c->stream));
-        }
-        NC(ncclGroupStart());
-        NC(ncclBroadcast(pacp, pacp, kq + 1, ncclInt64, ca, c->rowc, c->stream));
-        if (nnzA) {
-            NC(ncclBroadcast(parow, parow, nnzA, ncclInt32, ca, c->rowc, c->stream));
-            NC(ncclBroadcast(paval, paval, nnzA, ncclFloat32, ca, c->rowc, c->stream));
-        }
-        NC(ncclBroadcast(pbcp, pbcp, nj + 1, ncclInt64, rb, c->colc, c->stream));
-        if (nnzB) {
-            NC(ncclBroadcast(pbrow, pbrow, nnzB, ncclInt32, rb, c->colc, c->stream));
-            NC(ncclBroadcast(pbval, pbval, nnzB, ncclFloat32, rb, c->colc, c->stream));
-        }
-        NC(ncclGroupEnd());
+        Panels &PB = buf[q & 1];
+        CK(cudaStreamWaitEvent(c->stream, c->qev[q & 1], 0));
         if (ca != gj) comm_bytes += (kq + 1) * 8 + nnzA * 8;
         if (rb != gi) comm_bytes += (nj + 1) * 8 + nnzB * 8;
         mcl_csc_t Pa, Pb, Pq;
@@ -1638,20 +1701,21 @@ int mcl_summa_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, 
         Pa.row0 = A->row0;
         Pa.col0 = k0;
         Pa.n_global = n;
-        Pa.col_ptr = pacp;
-        Pa.row_idx = parow;
-        Pa.val = paval;
+        Pa.col_ptr = PB.acp;
+        Pa.row_idx = PB.arow;
+        Pa.val = PB.aval;
         Pb.nrows = kq;
         Pb.ncols = nj;
         Pb.nnz = nnzB;
         Pb.row0 = k0;
         Pb.col0 = A->col0;
         Pb.n_global = n;
-        Pb.col_ptr = pbcp;
-        Pb.row_idx = pbrow;
-        Pb.val = pbval;
+        Pb.col_ptr = PB.bcp;
+        Pb.row_idx = PB.brow;
+        Pb.val = PB.bval;
         mcl_stats_t sst;
         if ((rc = spgemm_impl(c, &Pa, &Pb, 0, nj, pin, &Pq, &sst)) != MCL_OK) break;
+        CK(cudaEventRecord(c->qev[2 + (q & 1)], c->stream));  // buffer q&1 free again
         flops += sst.flops;
         for (int b = 0; b <= kNumBins; b++) {
             bin_ms[b] += sst.bin_ms[b];
@@ -1719,6 +1783,7 @@ int mcl_summa_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, 
         st->phases = 1;
         st->estimator_used = 1;
         float sm3 = -1.f, sm4 = -1.f;
+        cudaEventSynchronize(c->sev[2]);
         cudaEventElapsedTime(&sm3, c->sev[0], c->sev[1]);
         cudaEventElapsedTime(&sm4, c->sev[1], c->sev[2]);
         cudaGetLastError();

@@ -39,6 +39,7 @@ struct BinArgs {
     int64_t cb;
     const int64_t *flops;  // [ncols_out]
     const int *rowpart;    // [A.ncols][33] row-range index of A (see kernels_spgemm.cu)
+    const int *rowpart_fine;  // [A.ncols][129] (split parts of the private family)
     // work list of this bin
     const int32_t *list;
     const int *count;
@@ -77,11 +78,14 @@ constexpr int kPartCap = 8192;
 constexpr int kPartThreads = 512;
 constexpr int kPartNeed = kPartCap / 2;  // distinct rows a part is sized for (load 1/2)
 constexpr int kParts = 32;  // row ranges of the rowpart index (k_rowpart)
+constexpr int kFineParts = 128;  // the finer index used by private-slice split parts
 // dense bin (kernels_dense.cu): 32 row-tile parts per column, fp64 tiles in shared memory
 constexpr int kDenseThreads = 1024;
 constexpr int kDenseTileBytes = 196608;  // a dense part's tile per pass (192 KB)
 // split_P flag: the column needs fp64 accumulation (more than kFp64Terms segments)
 constexpr int kSplitFp64 = 1 << 30;
+// split_P flag: short sub-segments, run the parts in the CTA-shared-table family
+constexpr int kSplitShared = 1 << 29;
 cudaError_t launch_dense_part(bool fp64, const BinArgs &a, int grid, cudaStream_t s);
 int dense_part_occupancy(bool fp64);
 // part variants: 0 kPartCap-slot shared table, 1 2*kPartCap-slot shared table
@@ -105,7 +109,7 @@ size_t bin_smem_bytes(int mode, int bin);
 
 // rowpart[k][i] = first position in A_*k whose row >= ceil(i*m/32), i = 0..32
 cudaError_t launch_rowpart(int64_t ncols, const int64_t *cp, const int32_t *row, int64_t m,
-                           int *rowpart, cudaStream_t s);
+                           int *rowpart, cudaStream_t s, int nparts = 32);
 
 // misc kernels (kernels_misc.cu)
 cudaError_t launch_flops(int64_t ncols, const int64_t *acp, const int64_t *bcp,

@@ -41,30 +41,39 @@ cudaError_t launch_flops(int64_t ncols, const int64_t *acp, const int64_t *bcp,
 // ------------------------------------------------------------------ row-range index of A
 // rowpart[k][i] = lower_bound(rows of A_*k, ceil(i*m/32)) - col_ptr[k], i = 0..32.  One
 // warp per column; lane i binary-searches boundary i (independent searches).
+// NP-way row-partition index (NP = 32, or kFineParts = 128 for split parts): P[k][i] =
+// first position of A_*k with row >= ceil(i m / NP); boundary 4i of the 128-way index
+// equals boundary i of the 32-way one.
+template <int NP>
 __global__ void k_rowpart(int64_t ncols, const int64_t *__restrict__ cp,
                           const int32_t *__restrict__ row, int64_t m, int *__restrict__ P) {
     const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = lane_id();
     for (int64_t k = w; k < ncols; k += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         const int64_t a = cp[k], b = cp[k + 1];
-        const int64_t bound = ((int64_t)lane * m + 31) / 32;
-        int64_t lo = a, hi = b;
-        while (lo < hi) {
-            const int64_t mid = (lo + hi) >> 1;
-            if ((int64_t)__ldg(row + mid) < bound) lo = mid + 1;
-            else hi = mid;
+    #pragma unroll
+        for (int q = 0; q < NP / 32; q++) {
+            const int part = lane + 32 * q;
+            const int64_t bound = ((int64_t)part * m + NP - 1) / NP;
+            int64_t lo = a, hi = b;
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                if ((int64_t)__ldg(row + mid) < bound) lo = mid + 1;
+                else hi = mid;
+            }
+            P[k * (NP + 1) + part] = (int)(lo - a);
         }
-        P[k * 33 + lane] = (int)(lo - a);
-        if (lane == 0) P[k * 33 + 32] = (int)(b - a);
+        if (lane == 0) P[k * (NP + 1) + NP] = (int)(b - a);
     }
 }
 cudaError_t launch_rowpart(int64_t ncols, const int64_t *cp, const int32_t *row, int64_t m,
-                           int *rowpart, cudaStream_t s) {
+                           int *rowpart, cudaStream_t s, int nparts) {
     if (ncols <= 0) return cudaSuccess;
     int64_t blocks = (ncols * 32 + 255) / 256;
     if (blocks > 148 * 32) blocks = 148 * 32;
     ++g_launches;
-    k_rowpart<<<(int)blocks, 256, 0, s>>>(ncols, cp, row, m, rowpart);
+    if (nparts == kFineParts) k_rowpart<kFineParts><<<(int)blocks, 256, 0, s>>>(ncols, cp, row, m, rowpart);
+    else k_rowpart<32><<<(int)blocks, 256, 0, s>>>(ncols, cp, row, m, rowpart);
     return cudaGetLastError();
 }
 
@@ -240,6 +249,9 @@ __global__ void k_classify(ClassifyArgs c) {
             while ((int64_t)P * c.split_part_need < need) P <<= 1;
             // long sums (T): only the dense fp64 variant accumulates in fp64
             if (nb > c.fp64_terms) P = (P < 128 ? 128 : P) | kSplitFp64;
+            // private-slice parts give each of 8 warps 1/(8P) of every segment: below
+            // kShortSegment / 2 rows on average the lanes idle, so use the shared table
+            else if (f < (int64_t)(kShortSegment / 2) * nb * 8 * P) P |= kSplitShared;
             c.split_P[col] = P;
             c.split_list[atomicAdd(c.split_count, 1)] = (int32_t)col;
             if (c.colbin) c.colbin[col] = -1;
@@ -278,7 +290,7 @@ __global__ void k_split_items(int nsplit, const int32_t *split_list, const int32
                               const int64_t *ioff, int32_t *item_col, int32_t *item_pr) {
     for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < nsplit; s += gridDim.x * blockDim.x) {
         const int32_t col = split_list[s];
-        const int Pv = split_P[col] & ~kSplitFp64;
+        const int Pv = split_P[col] & ~(kSplitFp64 | kSplitShared);
         const int P = Pv < 32 ? Pv : 32;
         const int step = 32 / P;
         const int64_t i0 = ioff[s];

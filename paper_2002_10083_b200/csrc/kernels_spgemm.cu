@@ -428,7 +428,15 @@ __global__ void __launch_bounds__(NT, (bin_min_blocks<CAP, NT, MODE, GLOBAL, ATO
                 if (g + lane < q1) {
                     const int k = __ldg(a.brow + g + lane);
                     const int64_t base = __ldg(a.acp + k);
-                    if (W == 1) {
+                    if (MODE == kPart) {
+                        // a split part: the warps divide its fine rowparts [4 p0, 4 p1)
+                        constexpr int F = kFineParts / kParts;
+                        const int pp0 = F * (s_pr & 0xff), pstep = (F * (s_pr >> 8) - pp0) / W;
+                        const int *pk = a.rowpart_fine + (int64_t)k * (kFineParts + 1) + pp0 + warp * pstep;
+                        const int p0 = __ldg(pk), p1 = __ldg(pk + pstep);
+                        dlo = base + p0;
+                        dlen = p1 - p0;
+                    } else if (W == 1) {
                         dlo = base;
                         dlen = (int)(__ldg(a.acp + k + 1) - base);
                     } else {
@@ -591,7 +599,7 @@ __global__ void __launch_bounds__(NT, (bin_min_blocks<CAP, NT, MODE, GLOBAL, ATO
             if (tid == 0) PROF_ADD(6, clock64() - prof_e0);  // compaction of the slices
             const long long prof_e1 = clock64();
 #endif
-            if (MODE == kNum) {
+            if (MODE == kNum || MODE == kPart) {
                 if (lane == 0) swi[0][warp] = cnt_w;
                 __syncthreads();
                 int off = 0, tot = 0;
@@ -599,10 +607,20 @@ __global__ void __launch_bounds__(NT, (bin_min_blocks<CAP, NT, MODE, GLOBAL, ATO
                     off += w2 < warp ? swi[0][w2] : 0;
                     tot += swi[0][w2];
                 }
-                const int64_t dst = a.c_cp[col];
-                if (tid == 0 && a.c_cp[col + 1] - dst != tot) atomicExch(a.err_flag, 1);
-                warp_sort_write<V>(wk, wv, cnt_w, (int)scap, a.c_row + dst + off,
-                                   a.c_val + dst + off, [](V v) { return (float)v; });
+                int32_t *orow;
+                float *oval;
+                if (MODE == kNum) {
+                    const int64_t dst = a.c_cp[col];
+                    if (tid == 0 && a.c_cp[col + 1] - dst != tot) atomicExch(a.err_flag, 1);
+                    orow = a.c_row + dst;
+                    oval = a.c_val + dst;
+                } else {  // split part: its staging slot (tot <= the 7/8 fill limit)
+                    orow = a.stg_row + a.stg_off[idx];
+                    oval = a.stg_val + a.stg_off[idx];
+                    if (tid == 0) a.stg_cnt[idx] = tot;
+                }
+                warp_sort_write<V>(wk, wv, cnt_w, (int)scap, orow + off, oval + off,
+                                   [](V v) { return (float)v; });
                 __syncthreads();
                 continue;
             }
@@ -871,11 +889,14 @@ cudaError_t launch_bin(int mode, int bin, const BinArgs &a, int grid, cudaStream
 
 cudaError_t launch_part(int variant, const BinArgs &a, int grid, cudaStream_t s) {
     if (variant == 0) return launch_of<kPartCap, kPartThreads, kPart, false, true>(a, grid, s);
-    return launch_of<2 * kPartCap, 2 * kPartThreads, kPart, false, true>(a, grid, s);
+    if (variant == 1) return launch_of<2 * kPartCap, 2 * kPartThreads, kPart, false, true>(a, grid, s);
+    // private row-range slices (bin 4 configuration): parts of >= 8 fine rowparts
+    return launch_of<kPartCap, kPartCap / 32, kPart, false, false>(a, grid, s);
 }
 int part_occupancy(int variant) {
     if (variant == 0) return occ_of<kPartCap, kPartThreads, kPart, false, true>();
-    return occ_of<2 * kPartCap, 2 * kPartThreads, kPart, false, true>();
+    if (variant == 1) return occ_of<2 * kPartCap, 2 * kPartThreads, kPart, false, true>();
+    return occ_of<kPartCap, kPartCap / 32, kPart, false, false>();
 }
 
 int bin_occupancy(int mode, int bin) {

@@ -295,7 +295,7 @@ def test_iterate_label_locality():
     ("C2", 600, 0, 0, 0), ("rmat14", 200, 0, 0, 0), ("rmat14", 200, 0, 2, 0),
     ("C1it1", 100, 0, 0, 0), ("C2", 600, 64, 0, 0), ("rmat14", 200, 16, 0, 0),
     ("rmat14", 200, 16, 2, 0), ("C1it1", 100, 16, 0, 0), ("C2", 600, 0, 0, 64),
-    ("rmat14", 200, 0, 0, 32)])
+    ("rmat14", 200, 0, 0, 32), ("C2", 600, 0, 0, -1), ("C1it1", 100, 0, 0, -1)])
 def test_iterate_split_columns(monkeypatch, graph, min_need, part_need, budget_mb, fp64_terms):
     """Row-range split columns (parts stitched, pruned by k_prune), forced onto every
     column with need > min_need.  part_need > 0 shrinks the parts' target size so the
@@ -303,8 +303,10 @@ def test_iterate_split_columns(monkeypatch, graph, min_need, part_need, budget_m
     lowers the long-sum threshold so columns run as dense fp64 tiles; budget_mb > 0
     forces many chunks."""
     monkeypatch.setenv("MCLX_SPLIT_MIN_NEED", str(min_need))
-    if fp64_terms:
+    if fp64_terms > 0:
         monkeypatch.setenv("MCLX_FP64_TERMS", str(fp64_terms))
+    if fp64_terms < 0:  # parts of P <= 4 in the CTA-shared family instead of private slices
+        monkeypatch.setenv("MCLX_SPLIT_PRIVATE", "0")
     if part_need:
         monkeypatch.setenv("MCLX_SPLIT_PART_NEED", str(part_need))
     if budget_mb:
