@@ -100,7 +100,8 @@ typedef struct {
     float chaos;             /* max_j chaos_j of the pruned, renormalised columns (Q9)          */
     int32_t phases;          /* column batches used                                             */
     int32_t retries;         /* columns re-run after a hash-table overflow                      */
-    int32_t estimator_used;  /* 1 exact symbolic, 2 Cohen                                       */
+    int32_t estimator_used;  /* 1 exact symbolic, 2 Cohen, 3 Cohen-binned numeric into upper-bound
+                                slots min(f_j, m) + compaction (unfused products, no symbolic) */
     int64_t bin_cols[MCL_NUM_BINS + 1];
     int64_t bin_flops[MCL_NUM_BINS + 1];
     float ms[8];             /* per stage: 0 flops/bin, 1 estimate, 2 symbolic, 3 numeric

@@ -54,6 +54,7 @@ struct mcl_ctx {
     int64_t split_min_need = INT64_MAX;       // MCLX_SPLIT_MIN_NEED: split smaller columns too
     int64_t split_part_need = kPartNeed;      // MCLX_SPLIT_PART_NEED (<= kPartNeed; tests)
     int64_t fp64_terms = kFp64Terms;          // MCLX_FP64_TERMS (tests)
+    int64_t cap_budget = (int64_t)16 << 30;   // unfused products: upper-bound slots up to this
     bool split_private = true;                // MCLX_SPLIT_PRIVATE=0: P <= 4 parts shared-table too
 };
 
@@ -240,10 +241,12 @@ int run_split(mcl_ctx *c, const Prod &pr, int nsplit, int32_t *split_list,
     // row tiles (kernels_dense.cu), staging capacity min(part rows, 2 P T / 32 + 256)
     // variants: 4 (P <= 16: private row-range slices, 8 warps over the part's >= 8 rowparts
     // of the 128-way index), 0 (P = 32, or MCLX_SPLIT_PRIVATE=0: CTA-shared tables), 1, 2, 3
+    // (the private family addresses A with 32-bit offsets)
+    const bool priv = c->split_private && pr.A->nnz < ((int64_t)1 << 32);
     auto variant_of = [&](int Pf) {
         const int P = Pf & ~(kSplitFp64 | kSplitShared);
         return (Pf & kSplitFp64) ? 3
-               : P <= 16 && c->split_private && !(Pf & kSplitShared) ? 4
+               : P <= 16 && priv && !(Pf & kSplitShared) ? 4
                : P <= 32 ? 0 : P == 64 ? 1 : 2;
     };
     const int vorder[5] = {4, 0, 1, 2, 3};
@@ -456,7 +459,9 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
         ca.alpha = round == 0 ? c->alpha : 4.0f * c->alpha;
         ca.max_load = round == 2 ? 0.5f : c->max_load;
         ca.force_bin = force_bin < 0 ? -1 : force_bin % kFamily;
-        ca.force_family = force_bin >= 0 ? force_bin / kFamily : round > 0 ? 1 : -1;
+        // the private family addresses A with 32-bit offsets
+        const bool big_a = pr.A->nnz >= ((int64_t)1 << 32);
+        ca.force_family = force_bin >= 0 ? force_bin / kFamily : (round > 0 || big_a) ? 1 : -1;
         ca.list_stride = std::max<int64_t>(n, 1);
         ca.bin_count = counts;
         ca.lists = lists;
@@ -691,7 +696,28 @@ int spgemm_impl(mcl_ctx *c, const mcl_csc_t *A, const mcl_csc_t *B, int64_t cb, 
     CK(cudaEventRecord(c->ev[1], c->stream));
     RC(cohen(c, pr, p.est_keys, p.seed, est, nullptr));
     CK(cudaEventRecord(c->ev[2], c->stream));
-    RC(symbolic_sizes(c, pr, f, est, p.force_bin, nnzc, nullptr));
+    // Output sizing.  Capacity mode (default when it fits c->cap_budget): every column gets
+    // an upper-bound slot of min(f_j, m) entries, the numeric pass records the true counts
+    // and a scan + copy compacts the result -- no symbolic hashing pass.  Otherwise the
+    // exact symbolic pass sizes the CSC first.
+    int64_t *capcp = nullptr, *ccnt = nullptr;
+    int32_t *crow = nullptr;
+    float *cval = nullptr;
+    bool capacity = false;
+    if (!getenv("MCLX_EXACT_SYMBOLIC")) {
+        RC(scratch_t(c, "cap_cp", (size_t)n + 1, &capcp));
+        RC(scratch_t(c, "cap_cnt", (size_t)std::max<int64_t>(n, 1), &ccnt));
+        CK(launch_kcap(n, f, A->nrows, INT32_MAX, ccnt, c->stream));
+        CK(launch_scan_i64(ccnt, capcp, n, tmp, c->stream));
+        int64_t tcap = 0;
+        RC(readback(c, capcp + n, sizeof(int64_t), &tcap));
+        if (tcap * 8 <= c->cap_budget) {
+            capacity = true;
+            RC(scratch_t(c, "cap_row", (size_t)std::max<int64_t>(tcap, 1), &crow));
+            RC(scratch_t(c, "cap_val", (size_t)std::max<int64_t>(tcap, 1), &cval));
+        }
+    }
+    if (!capacity) RC(symbolic_sizes(c, pr, f, est, p.force_bin, nnzc, nullptr));
     CK(cudaEventRecord(c->ev[3], c->stream));
     C->col_ptr = nullptr;
     mcl_csc_t out;
@@ -700,11 +726,8 @@ int spgemm_impl(mcl_ctx *c, const mcl_csc_t *A, const mcl_csc_t *B, int64_t cb, 
     if (!out.col_ptr) return fail(c, MCL_ERR_OOM, "cannot allocate col_ptr");
     int rc = MCL_OK;
     do {
-        cudaError_t e = launch_scan_i64(nnzc, out.col_ptr, n, tmp, c->stream);
-        if (e != cudaSuccess) { rc = fail(c, MCL_ERR_CUDA, "scan: %s", cudaGetErrorString(e)); break; }
+        cudaError_t e;
         int64_t nnz = 0;
-        if ((rc = readback(c, out.col_ptr + n, sizeof(int64_t), &nnz)) != MCL_OK) break;
-        if ((rc = alloc_rows_vals(c, &out, nnz)) != MCL_OK) break;
         out.nrows = A->nrows;
         out.ncols = n;
         out.row0 = A->row0;
@@ -712,10 +735,28 @@ int spgemm_impl(mcl_ctx *c, const mcl_csc_t *A, const mcl_csc_t *B, int64_t cb, 
         out.n_global = A->n_global ? A->n_global : A->nrows;
         BinArgs base;
         memset(&base, 0, sizeof base);
-        base.c_cp = out.col_ptr;
-        base.c_row = out.row_idx;
-        base.c_val = out.val;
-        if ((rc = run_bins(c, kNum, pr, f, nullptr, nnzc, p.force_bin, base, st)) != MCL_OK) break;
+        if (capacity) {
+            base.c_cp = capcp;
+            base.c_row = crow;
+            base.c_val = cval;
+            base.c_cnt = ccnt;
+            if ((rc = run_bins(c, kNum, pr, f, est, nullptr, p.force_bin, base, st)) != MCL_OK) break;
+            e = launch_scan_i64(ccnt, out.col_ptr, n, tmp, c->stream);
+            if (e != cudaSuccess) { rc = fail(c, MCL_ERR_CUDA, "scan: %s", cudaGetErrorString(e)); break; }
+            if ((rc = readback(c, out.col_ptr + n, sizeof(int64_t), &nnz)) != MCL_OK) break;
+            if ((rc = alloc_rows_vals(c, &out, nnz)) != MCL_OK) break;
+            e = launch_copy_cols(n, ccnt, capcp, crow, cval, out.col_ptr, out.row_idx, out.val, c->stream);
+            if (e != cudaSuccess) { rc = fail(c, MCL_ERR_CUDA, "copy: %s", cudaGetErrorString(e)); break; }
+        } else {
+            e = launch_scan_i64(nnzc, out.col_ptr, n, tmp, c->stream);
+            if (e != cudaSuccess) { rc = fail(c, MCL_ERR_CUDA, "scan: %s", cudaGetErrorString(e)); break; }
+            if ((rc = readback(c, out.col_ptr + n, sizeof(int64_t), &nnz)) != MCL_OK) break;
+            if ((rc = alloc_rows_vals(c, &out, nnz)) != MCL_OK) break;
+            base.c_cp = out.col_ptr;
+            base.c_row = out.row_idx;
+            base.c_val = out.val;
+            if ((rc = run_bins(c, kNum, pr, f, nullptr, nnzc, p.force_bin, base, st)) != MCL_OK) break;
+        }
         CK(cudaEventRecord(c->ev[4], c->stream));
         e = launch_reduce_i64(f, n, tot, c->stream);
         if (e != cudaSuccess) { rc = fail(c, MCL_ERR_CUDA, "reduce: %s", cudaGetErrorString(e)); break; }
@@ -733,7 +774,7 @@ int spgemm_impl(mcl_ctx *c, const mcl_csc_t *A, const mcl_csc_t *B, int64_t cb, 
             st->nnz_out = nnz;
             st->est_nnz = est_tot;
             st->cf = nnz > 0 ? (double)hv[0] / (double)nnz : 0.0;
-            st->estimator_used = 1;
+            st->estimator_used = capacity ? 3 : 1;
             st->ms[0] = elapsed(c, 0, 1);
             st->ms[1] = elapsed(c, 1, 2);
             st->ms[2] = elapsed(c, 2, 3);
@@ -1021,6 +1062,7 @@ int mcl_ctx_create(mcl_ctx_t *out, int device, void *stream, mcl_alloc_fn alloc,
     if (const char *e = getenv("MCLX_SPLIT_BUDGET_MB")) c->split_budget = (int64_t)atoll(e) << 20;
     if (const char *e = getenv("MCLX_SPLIT_MIN_NEED")) c->split_min_need = atoll(e);
     if (const char *e = getenv("MCLX_FP64_TERMS")) c->fp64_terms = atoll(e);
+    if (const char *e = getenv("MCLX_CAP_BUDGET_MB")) c->cap_budget = (int64_t)atoll(e) << 20;
     if (const char *e = getenv("MCLX_SPLIT_PRIVATE")) c->split_private = atoi(e) != 0;
     if (const char *e = getenv("MCLX_SPLIT_PART_NEED"))
         c->split_part_need = std::max<int64_t>(16, std::min<int64_t>(kPartNeed, atoll(e)));

@@ -52,6 +52,7 @@ struct BinArgs {
     // outputs
     int64_t *sym_nnz;                                   // kSym
     const int64_t *c_cp;                                // kNum
+    int64_t *c_cnt;     // kNum with upper-bound slots: per-column counts (else exact c_cp)
     int32_t *c_row;
     float *c_val;
     const int64_t *soff;                                // kFused

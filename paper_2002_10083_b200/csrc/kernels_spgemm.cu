@@ -421,7 +421,9 @@ __global__ void __launch_bounds__(NT, (bin_min_blocks<CAP, NT, MODE, GLOBAL, ATO
             // The gathers of batch i+1 -- and the descriptor loads of the group after the
             // next -- are issued before batch i is inserted, so each warp always has a
             // batch of loads in flight while it works on the hash table.
-            auto load_desc = [&](int64_t g, int64_t &dlo, int &dlen, float &db) {
+            // A positions as 32-bit offsets (the host routes A with nnz >= 2^32 to the
+            // CTA-shared family): one shuffle per descriptor and one IMAD.WIDE per gather
+            auto load_desc = [&](int64_t g, uint32_t &dlo, int &dlen, float &db) {
                 dlo = 0;
                 dlen = 0;
                 db = 0.f;
@@ -434,15 +436,15 @@ __global__ void __launch_bounds__(NT, (bin_min_blocks<CAP, NT, MODE, GLOBAL, ATO
                         const int pp0 = F * (s_pr & 0xff), pstep = (F * (s_pr >> 8) - pp0) / W;
                         const int *pk = a.rowpart_fine + (int64_t)k * (kFineParts + 1) + pp0 + warp * pstep;
                         const int p0 = __ldg(pk), p1 = __ldg(pk + pstep);
-                        dlo = base + p0;
+                        dlo = (uint32_t)(base + p0);
                         dlen = p1 - p0;
                     } else if (W == 1) {
-                        dlo = base;
+                        dlo = (uint32_t)base;
                         dlen = (int)(__ldg(a.acp + k + 1) - base);
                     } else {
                         const int *pk = a.rowpart + (int64_t)k * (kParts + 1) + warp * PSTEP;
                         const int p0 = __ldg(pk), p1 = __ldg(pk + PSTEP);
-                        dlo = base + p0;
+                        dlo = (uint32_t)(base + p0);
                         dlen = p1 - p0;
                     }
                     db = __ldg(a.bval + g + lane);
@@ -450,7 +452,7 @@ __global__ void __launch_bounds__(NT, (bin_min_blocks<CAP, NT, MODE, GLOBAL, ATO
             };
             // batch at (group g, first segment eb, chunk c) -> registers; returns the
             // longest sub-segment of the batch (chunks continue while c + 32 < it)
-            auto fetch = [&](int64_t g, int eb, int c, int64_t dlo, int dlen, float db, int (&rr)[kItems],
+            auto fetch = [&](int64_t g, int eb, int c, uint32_t dlo, int dlen, float db, int (&rr)[kItems],
                              float (&av)[kItems], float (&bb)[kItems]) {
                 const int ncnt = (int)((q1 - g) < 32 ? (q1 - g) : 32);
                 const int t = c + lane;
@@ -458,26 +460,27 @@ __global__ void __launch_bounds__(NT, (bin_min_blocks<CAP, NT, MODE, GLOBAL, ATO
     #pragma unroll
                 for (int u = 0; u < kItems; u++) {
                     const int e = eb + u;
-                    const int64_t lo = __shfl_sync(0xffffffffu, dlo, e & 31);
+                    const uint32_t lo = __shfl_sync(0xffffffffu, dlo, e & 31);
                     int len = __shfl_sync(0xffffffffu, dlen, e & 31);
                     bb[u] = __shfl_sync(0xffffffffu, db, e & 31);
                     if (e >= ncnt) len = 0;
                     ml = len > ml ? len : ml;
                     const bool v = t < len;
-                    rr[u] = v ? __ldg(a.arow + lo + t) : -1;
+                    const uint32_t q = lo + (uint32_t)t;
+                    rr[u] = v ? __ldg(a.arow + q) : -1;
                     av[u] = 0.f;
                     if (MODE != kSym && v) {
 #if defined(MCLX_EXPT) && MCLX_EXPT == 2
                         av[u] = 0.5f;  // experiment: no value gathers
 #else
-                        av[u] = __ldg(a.aval + lo + t);
+                        av[u] = __ldg(a.aval + q);
 #endif
                     }
                 }
                 return ml;
             };
             int64_t g = q0;
-            int64_t clo, nlo;
+            uint32_t clo, nlo;
             int clen, nlen;
             float cdb, ndb;
             load_desc(g, clo, clen, cdb);
@@ -611,7 +614,11 @@ __global__ void __launch_bounds__(NT, (bin_min_blocks<CAP, NT, MODE, GLOBAL, ATO
                 float *oval;
                 if (MODE == kNum) {
                     const int64_t dst = a.c_cp[col];
-                    if (tid == 0 && a.c_cp[col + 1] - dst != tot) atomicExch(a.err_flag, 1);
+                    if (a.c_cnt) {  // capacity slots: record the count (<= min(f_j, m))
+                        if (tid == 0) a.c_cnt[col] = tot;
+                    } else if (tid == 0 && a.c_cp[col + 1] - dst != tot) {
+                        atomicExch(a.err_flag, 1);
+                    }
                     orow = a.c_row + dst;
                     oval = a.c_val + dst;
                 } else {  // split part: its staging slot (tot <= the 7/8 fill limit)
@@ -735,7 +742,11 @@ __global__ void __launch_bounds__(NT, (bin_min_blocks<CAP, NT, MODE, GLOBAL, ATO
 
             if (MODE == kNum) {
                 const int64_t dst = a.c_cp[col];
-                if (tid == 0 && a.c_cp[col + 1] - dst != nnz) atomicExch(a.err_flag, 1);
+                if (a.c_cnt) {
+                    if (tid == 0) a.c_cnt[col] = nnz;
+                } else if (tid == 0 && a.c_cp[col + 1] - dst != nnz) {
+                    atomicExch(a.err_flag, 1);
+                }
                 sort_write<NT, V>(keys, vals, nnz, (int)cap, a.c_row + dst, a.c_val + dst,
                                   [](V v) { return (float)v; }, sscan);
                 continue;
