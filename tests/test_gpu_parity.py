@@ -405,6 +405,20 @@ def test_full_mcl_clusters_equal(name, params):
     assert abs(len(hist) - ref.iterations) <= 1
 
 
+@pytest.mark.slow
+@pytest.mark.parametrize("shape", ["protein_n5000", "rmat_s12"])
+def test_full_mcl_clusters_equal_small_c3_c4_shapes(shape):
+    """P4 on the C3/C5 (protein-like) and C4 (R-MAT) generators at sizes where the
+    single-threaded oracle runs MCL to convergence in seconds: identical clusters."""
+    G = synth.protein_like(n=5000, seed=3) if shape == "protein_n5000" else synth.rmat(scale=12, seed=4)
+    p = M.Params()
+    labels, k, hist, _ = M.run(dev(G), p)
+    ref = O.mcl(G, theta=1e-4, S=1100, R=1400, pct=0.9, eps=1e-3)
+    assert k == ref.nclusters
+    assert np.array_equal(labels.cpu().numpy(), ref.labels)
+    assert abs(len(hist) - ref.iterations) <= 1
+
+
 # ---------------------------------------------------------------- C3 at full size, sampled
 def _sampled_parity(A32, Ag, params, n_random=200, n_heavy=20, seed=0):
     """Compare sampled columns of the GPU iterate with the oracle, column by column
