@@ -313,6 +313,7 @@ __global__ void __launch_bounds__(NT, (bin_min_blocks<CAP, NT, MODE, GLOBAL, ATO
             __shared__ int st_k[NT];
             __shared__ float st_b[NT];
             __shared__ int s_fill[1];
+            __shared__ int s_next[1];
             if (tid == 0) s_fill[0] = 0;
             __syncthreads();
             // ---- accumulate C_*j = sum_k b_kj A_*k.  Each lane gathers 4 consecutive
@@ -348,15 +349,22 @@ __global__ void __launch_bounds__(NT, (bin_min_blocks<CAP, NT, MODE, GLOBAL, ATO
                     }
                     st_b[tid] = __ldg(a.bval + c0 + tid);
                 }
+                if (tid == 0) s_next[0] = 0;
                 __syncthreads();
-                const int wgrp0 = warp * (32 / g);
-                for (int e0 = 0; e0 < cnt && ok; e0 += ngrp) {
-                    if (e0 + wgrp0 >= cnt) break;  // warp-uniform: no work for this warp's groups
+                // segments are handed out dynamically, 32/g per warp at a time, so warps that
+                // drew short segments take more instead of idling at the batch barrier
+                (void)grp;
+                (void)ngrp;
+                for (;;) {
+                    int e0 = 0;
+                    if (lane == 0) e0 = atomicAdd(&s_next[0], 32 / g);
+                    e0 = __shfl_sync(0xffffffffu, e0, 0);
+                    if (e0 >= cnt || !ok) break;  // warp-uniform
                     if (*vovf) {
                         ok = false;
                         break;
                     }
-                    const int e = e0 + grp;
+                    const int e = e0 + lane / g;
                     int lo = 0, hi = 0;     // valid element window relative to the aligned base
                     float bkj = 0.f;
                     const int *rp = a.arow;
