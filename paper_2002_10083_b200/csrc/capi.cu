@@ -241,12 +241,19 @@ int run_split(mcl_ctx *c, const Prod &pr, int nsplit, int32_t *split_list,
     // row tiles (kernels_dense.cu), staging capacity min(part rows, 2 P T / 32 + 256)
     // variants: 4 (P <= 16: private row-range slices, 8 warps over the part's >= 8 rowparts
     // of the 128-way index), 0 (P = 32, or MCLX_SPLIT_PRIVATE=0: CTA-shared tables), 1, 2, 3
-    // (the private family addresses A with 32-bit offsets)
-    const bool priv = c->split_private && pr.A->nnz < ((int64_t)1 << 32);
+    // (the private family addresses A with 32-bit offsets; its 128-way row index costs a
+    // pass over A, so it is built only when enough columns use it)
+    auto priv_ok = [&](int Pf) {
+        return (Pf & ~(kSplitFp64 | kSplitShared)) <= 16 && !(Pf & (kSplitFp64 | kSplitShared));
+    };
+    int64_t npriv = 0;
+    for (int s2 = 0; s2 < nsplit; s2++) npriv += priv_ok(hP[hl[s2]]);
+    const bool priv = c->split_private && pr.A->nnz < ((int64_t)1 << 32) &&
+                      (npriv >= 4096 || c->split_min_need != INT64_MAX);
     auto variant_of = [&](int Pf) {
         const int P = Pf & ~(kSplitFp64 | kSplitShared);
         return (Pf & kSplitFp64) ? 3
-               : P <= 16 && priv && !(Pf & kSplitShared) ? 4
+               : priv && priv_ok(Pf) ? 4
                : P <= 32 ? 0 : P == 64 ? 1 : 2;
     };
     const int vorder[5] = {4, 0, 1, 2, 3};
