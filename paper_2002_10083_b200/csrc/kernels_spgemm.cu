@@ -11,18 +11,27 @@
 // C_*j = sum_{k in inds(B_*j)} b_kj A_*k (Gustavson in CSC).  One CTA owns
 // one output column at a time (persistent CTAs pull columns from the bin's work list).
 //
-// ACCUMULATION (atomic-free values).  The CTA of a bin has W = NT/32 warps; each warp
-// owns a private slice (cap/W slots) of the column's table and 1/W of the row space: the
-// 32-way row-partition index of A (rowpart[k][i] = first position in A_*k with row >=
-// ceil(i m/32), built once per call) gives every warp its sub-segment of each A_*k.  A warp
-// walks the column's segments on its own (32 segment descriptors loaded by its lanes, one
-// per lane, and broadcast with shuffles -- no CTA barrier), gathers one sub-segment per
-// instruction so the 32 rows of an insert are distinct, claims empty slots with an
-// integer CAS (only new keys) and adds values with a plain LDS/FADD/STS.  Measured on
-// B200 (tools/ubench.cu): shared float atomicAdd is a CAS loop (ATOMS.CAST.SPIN) at
-// ~2.5 lane-ops/cycle/SM, MATCH.ANY ~0.5, plain RMW ~4.5, so neither value atomics nor
-// warp-synchronous matching is used.  Slices are ordered by row range, so the compacted
-// table is grouped by row range for the epilogue.
+// ACCUMULATION, private family (atomic-free values).  The CTA of a bin has W = NT/32
+// warps; each warp owns a private slice (cap/W slots) of the column's table and 1/W of the
+// row space: the 32-way row-partition index of A (rowpart[k][i] = first position in A_*k
+// with row >= ceil(i m/32), built once per call) gives every warp its sub-segment of each
+// A_*k.  A warp walks the column's segments on its own (32 segment descriptors loaded by
+// its lanes, one per lane, and broadcast with shuffles -- no CTA barrier) in batches of
+// kItems sub-segments side by side, 32 rows of each; the gathers of batch i+1 are issued
+// before batch i is inserted.  One warp-uniform probe loop resolves all items of a batch
+// (warp_insert_n): empty slots are claimed with an integer CAS (only new keys), values are
+// added item by item with a plain LDS/FADD/STS (the rows of one item are distinct).
+// Measured on B200 (tools/ubench.cu): shared float atomicAdd is a CAS loop
+// (ATOMS.CAST.SPIN) at ~2.5 lane-ops/cycle/SM, MATCH.ANY ~0.5, plain RMW ~4.5, so neither
+// value atomics nor warp-synchronous matching is used.  Slices are ordered by row range,
+// so the compacted table is grouped by row range for the epilogue.
+//
+// CTA-shared family (short segments, R-MAT-like): one table per CTA, groups of g lanes per
+// segment with 16-byte gathers, warps take segments dynamically, slots resolved first and
+// float atomicAdds issued with the warp reconverged (insert4).
+//
+// kPart: one row-range part of a split column (see run_split in capi.cu), accumulated by
+// either family over the part's rowparts and written, rows sorted, to a staging slot.
 #include <type_traits>
 
 #include "kernels.h"
@@ -104,66 +113,11 @@ __device__ __forceinline__ int group_size_for(int64_t avg) {
     return avg >= 24 ? 32 : avg >= 12 ? 16 : avg >= 6 ? 8 : 4;
 }
 
-// old = p ? atomicCAS(addr, kEmptyKey, val) : dflt, as one predicated instruction (the
-// compiler otherwise wraps every CAS in a divergent branch)
-__device__ __forceinline__ int cas_if(bool p, int *addr, int val, int dflt) {
-    int old = dflt;
-    if (__isShared(addr)) {
-        const unsigned a = (unsigned)__cvta_generic_to_shared(addr);
-        asm volatile(
-            "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %1, 0;\n\t"
-            "@q atom.shared.cas.b32 %0, [%2], %3, %4;\n\t}"
-            : "+r"(old)
-            : "r"((int)p), "r"(a), "r"(kEmptyKey), "r"(val)
-            : "memory");
-    } else if (p) {
-        old = atomicCAS(addr, kEmptyKey, val);
-    }
-    return old;
-}
-
-// Insert one (row, v) per valid lane into this warp's private slice (keys, vals)[0, scap).
-// The valid lanes hold distinct rows (one sub-segment), so after the slots are found the
-// value update is a plain read-modify-write.  Open addressing with linear probing; empty
-// slots are claimed with atomicCAS (lanes of the warp may race for one slot).  `fill`
-// (warp-uniform) counts claimed slots; passing `limit` (7/8 of the slice) reports
-// overflow so the column is re-run in a bigger bin.  All 32 lanes must call.
-template <int MODE, typename V>
-__device__ __forceinline__ bool warp_insert(int *keys, V *vals, uint32_t scap, bool valid, int row,
-                                            V v, int &fill, int limit, unsigned &passes) {
-    const unsigned FULL = 0xffffffffu;
-    uint32_t s = hash_slot(row, scap);
-    volatile int *vk = keys;
-    int k = valid ? vk[s] : row;
-    bool need = k != row;
-    while (__any_sync(FULL, need)) {
-        passes++;
-        bool claimed = false;
-        if (need) {
-            if (k == kEmptyKey) {
-                const int old = atomicCAS(&keys[s], kEmptyKey, row);
-                if (old == kEmptyKey) {
-                    claimed = true;
-                    need = false;
-                } else {
-                    k = old;  // another lane took the slot: re-examine it
-                    need = old != row;
-                }
-            } else {
-                s = (s + 1 == scap) ? 0u : s + 1;
-                k = vk[s];
-                need = k != row;
-            }
-        }
-        fill += __popc(__ballot_sync(FULL, claimed));
-        if (fill > limit) return false;
-    }
-    if (MODE != kSym && valid) vals[s] += v;
-    __syncwarp();
-    return true;
-}
-
-// kItems inserts per lane at once (item u: lanes hold distinct rows of one sub-segment;
+// Insert kItems (row, v) per lane into this warp's private slice (keys, vals)[0, scap):
+// open addressing with linear probing, empty slots claimed with an integer atomicCAS (lanes
+// of the warp may race for one slot), `fill` (warp-uniform) counts claimed slots and
+// passing `limit` (7/8 of the slice) reports overflow so the column is re-run in a bigger
+// bin.  All 32 lanes must call.  (item u: lanes hold distinct rows of one sub-segment;
 // the same row may appear in several items).  All slots are probed first and one
 // warp-uniform loop resolves misses / claims for every item, so a call that needs a claim
 // pays the vote + fill count once for all items, not once per item.  The value updates
@@ -184,19 +138,6 @@ __device__ __forceinline__ bool warp_insert_n(int *keys, V *vals, uint32_t scap,
         k[u] = valid[u] ? vk[s[u]] : row[u];
     }
     bool any = false;
-#ifdef MCLX_FIRST_CLAIM
-    // an empty home slot is claimed right away (predicated CAS, no branch per item)
-    int claims0 = 0;
-#pragma unroll
-    for (int u = 0; u < NI; u++) {
-        const bool try_claim = valid[u] && k[u] == kEmptyKey;
-        const int old = cas_if(try_claim, &keys[s[u]], row[u], k[u]);
-        claims0 += try_claim && old == kEmptyKey;
-        k[u] = (try_claim && old == kEmptyKey) ? row[u] : old;
-    }
-    fill += __reduce_add_sync(FULL, claims0);
-    if (fill > limit) return false;
-#endif
 #pragma unroll
     for (int u = 0; u < NI; u++) {
         need[u] = k[u] != row[u];
@@ -410,9 +351,6 @@ __global__ void __launch_bounds__(NT, (bin_min_blocks<CAP, NT, MODE, GLOBAL, ATO
         } else {
             // ---- accumulate C_*j = sum_k b_kj A_*k: warp `warp` handles rows of its range
             unsigned prof_passes = 0, prof_calls = 0, prof_valid = 0;
-#ifdef MCLX_EXPT
-            float prof_sink = 0.f;
-#endif
 #ifdef MCLX_PROF
             const long long prof_t0 = clock64();
 #endif
@@ -478,11 +416,7 @@ __global__ void __launch_bounds__(NT, (bin_min_blocks<CAP, NT, MODE, GLOBAL, ATO
                     rr[u] = v ? __ldg(a.arow + q) : -1;
                     av[u] = 0.f;
                     if (MODE != kSym && v) {
-#if defined(MCLX_EXPT) && MCLX_EXPT == 2
-                        av[u] = 0.5f;  // experiment: no value gathers
-#else
                         av[u] = __ldg(a.aval + q);
-#endif
                     }
                 }
                 return ml;
@@ -532,14 +466,9 @@ __global__ void __launch_bounds__(NT, (bin_min_blocks<CAP, NT, MODE, GLOBAL, ATO
                     prof_valid += __popc(__ballot_sync(0xffffffffu, vl[u]));
                 }
 #endif
-#if defined(MCLX_EXPT) && MCLX_EXPT == 1
-                // experiment: gathers only
-                for (int u = 0; u < kItems; u++) prof_sink += vl[u] ? (float)rr[u] * (float)vv[u] : 0.f;
-#else
                 if (!warp_insert_n<MODE, V, kItems>(wkeys, wvals, scap, vl, rr, vv, fill, limit,
                                                     prof_passes))
                     ok = false;
-#endif
     #pragma unroll
                 for (int u = 0; u < kItems; u++) {
                     rr[u] = nrr[u];
@@ -552,9 +481,6 @@ __global__ void __launch_bounds__(NT, (bin_min_blocks<CAP, NT, MODE, GLOBAL, ATO
                 ml = nml;
             }
             fresh = lane == 0 ? fill : 0;
-#ifdef MCLX_EXPT
-            if (prof_sink == 1234.5f) atomicAdd(&g_prof[11], 1ull);
-#endif
 #ifdef MCLX_PROF
             if (lane == 0) {
                 PROF_ADD(0, prof_calls);
