@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_dense_part(BinArgs a) {
     __shared__ int st_k[NT];
     __shared__ float st_b[NT];
     __shared__ int sscan[NT / 32];
-    __shared__ int s_col, s_idx, s_pr;
+    __shared__ int s_col, s_idx, s_pr, s_next;
     const int tid = threadIdx.x;
     const int count = *a.count;
     for (;;) {
@@ -60,6 +60,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_dense_part(BinArgs a) {
             s_idx = idx;
             s_col = idx < count ? a.list[idx] : -1;
             s_pr = idx < count ? a.item_pr[idx] : 0;
+            s_next = 0;
         }
         __syncthreads();
         const int col = s_col, idx = s_idx, pr = s_pr;
@@ -73,7 +74,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_dense_part(BinArgs a) {
         const int64_t dst0 = a.stg_off[idx], cap = a.stg_off[idx + 1] - dst0;
         const int64_t fpart = a.flops[col] * (p1 - p0) / kParts;
         const int g = dense_group_size(nb > 0 ? fpart / nb : 0);
-        const int lane_g = tid & (g - 1), grp = tid / g, ngrp = NT / g;
+        const int lane_g = tid & (g - 1);
         int64_t written = 0;
         for (int64_t t0 = r_lo; t0 < r_hi; t0 += TILE) {
             const int tw = (int)((r_hi - t0) < TILE ? (r_hi - t0) : TILE);
@@ -90,20 +91,31 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_dense_part(BinArgs a) {
                     st_b[tid] = __ldg(a.bval + c0 + tid);
                 }
                 __syncthreads();
-                for (int e = grp; e < cnt; e += ngrp) {
+                // segments handed to warps dynamically (32/g at a time), so warps that drew
+                // short segments take more instead of idling at the batch barrier; the row
+                // and value of an entry are loaded together (one round trip, not two)
+                for (;;) {
+                    int e0 = 0;
+                    if ((tid & 31) == 0) e0 = atomicAdd(&s_next, 32 / g);
+                    e0 = __shfl_sync(0xffffffffu, e0, 0);
+                    if (e0 >= cnt) break;
+                    const int e = e0 + (tid & 31) / g;
+                    if (e >= cnt) continue;
                     const int64_t s0 = st_start[e];
                     const int len = st_k[e];
                     const V b = (V)st_b[e];
                     for (int i = lane_g; i < len; i += g) {
                         const int r = __ldg(a.arow + s0 + i);
+                        const float av = __ldg(a.aval + s0 + i);
                         if (r >= t0 + tw) break;  // rows ascend: the rest is past this pass
                         if (r < t0) continue;
-                        const V prod = (V)__ldg(a.aval + s0 + i) * b;
+                        const V prod = (V)av * b;
                         if (prod > V(0)) atomicAdd(&acc[r - t0], prod);
                         else atomic_mark_zero(&acc[r - t0]);  // fp32 underflow: keep the entry
                     }
                 }
                 __syncthreads();
+                if (tid == 0) s_next = 0;
             }
             // the pass's touched rows, in row order
             for (int i0 = 0; i0 < tw; i0 += NT) {
