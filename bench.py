@@ -362,10 +362,32 @@ def run_gpu(args):
         ov = torch.empty(cap, dtype=torch.float32, pin_memory=True)
         del probe, pc_, pr_, pv_
         d2h = 0
+        # Steps are pipelined over three streams: step i+1's H2D (copy stream s_in) and
+        # step i-1's D2H (s_out) run on the copy engines while step i computes; every step
+        # still copies its own input in and its own result out.  Two device input buffers,
+        # events order their reuse; result tensors are recorded on s_out so the caching
+        # allocator keeps them until their D2H completes.
+        s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+        din = [(torch.empty_like(A.colptr), torch.empty_like(A.rows), torch.empty_like(A.vals))
+               for _ in range(2)]
+        ev_in = [torch.cuda.Event() for _ in range(2)]
+        ev_free = [torch.cuda.Event() for _ in range(2)]
 
-        def e2e_step():
-            Ah = M.CSC(A.nrows, A.ncols, hc.to(dev, non_blocking=True), hr.to(dev, non_blocking=True),
-                       hv.to(dev, non_blocking=True), row0=A.row0, col0=A.col0, n_global=A.n_global)
+        def h2d_copy(i):
+            k = i % 2
+            with torch.cuda.stream(s_in):
+                if i >= 2:
+                    s_in.wait_event(ev_free[k])
+                din[k][0].copy_(hc, non_blocking=True)
+                din[k][1].copy_(hr, non_blocking=True)
+                din[k][2].copy_(hv, non_blocking=True)
+                ev_in[k].record(s_in)
+
+        def compute(i):
+            k = i % 2
+            stream.wait_event(ev_in[k])
+            Ah = M.CSC(A.nrows, A.ncols, din[k][0], din[k][1], din[k][2], row0=A.row0, col0=A.col0,
+                       n_global=A.n_global)
             if mode == "fused":
                 out, _ = ctx.iterate(Ah, params)
             elif mode == "summa":
@@ -373,24 +395,50 @@ def run_gpu(args):
             else:
                 blk, _ = ctx.iterate(Ah, params, cols=(b, e))
                 out = allgather_csc(dist, M, blk, n, Ah.nrows, dev)
+            ev_free[k].record(stream)
+            return out
+
+        def d2h_copy(out):
             c_, r_, v_ = result_block(out)
             nz = r_.numel()
             if nz > orw.numel():
                 raise RuntimeError("e2e: result larger than the preallocated host buffer")
-            oc[: c_.numel()].copy_(c_, non_blocking=True)
-            orw[:nz].copy_(r_, non_blocking=True)
-            ov[:nz].copy_(v_, non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(stream)
+            s_out.wait_event(done)
+            with torch.cuda.stream(s_out):
+                # 32 MB pieces: the library's small size readbacks share the D2H copy engine
+                # and would otherwise queue behind one 1.3 GB transfer
+                oc[: c_.numel()].copy_(c_, non_blocking=True)
+                step_ = 8 << 20
+                for o in range(0, nz, step_):
+                    orw[o: min(nz, o + step_)].copy_(r_[o: o + step_], non_blocking=True)
+                    ov[o: min(nz, o + step_)].copy_(v_[o: o + step_], non_blocking=True)
+            for t_ in (c_, r_, v_, out.colptr, out.rows, out.vals):
+                t_.record_stream(s_out)
             return c_.numel() * 8 + nz * 8
 
-        e2e_step()  # untimed: device buffers of the copies come from the caching allocator
+        def run_e2e(steps):
+            h2d_copy(0)
+            nbytes = 0
+            for i in range(steps):
+                if i + 1 < steps:
+                    h2d_copy(i + 1)
+                out = compute(i)
+                nbytes = d2h_copy(out)
+                del out
+            stream.wait_stream(s_out)
+            return nbytes
+
+        run_e2e(3)  # untimed: the caching allocator holds the double-buffered results after this
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        for _ in range(args.e2e_steps):
-            d2h = e2e_step()
+        s_in.wait_event(e0)
+        d2h = run_e2e(args.e2e_steps)
         e1.record(stream)
         torch.cuda.synchronize()
         e2e_ms = e0.elapsed_time(e1) / args.e2e_steps
@@ -472,7 +520,7 @@ def main():
                     help="N>1: the 2D Sparse-SUMMA (default) or column partition + all-gather")
     ap.add_argument("--grid", default=None, help="pr x pc for --mode summa, e.g. 2x2 (default "
                     "1xN: whole columns per rank, stages accumulated in the fused kernel)")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-flops", type=float, default=5e8)
     ap.add_argument("--ref-flops", type=float, default=2e8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
