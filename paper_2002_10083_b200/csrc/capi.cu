@@ -44,6 +44,8 @@ struct mcl_ctx {
     int pr = 1, pc = 1, rank = 0;
     ncclComm_t world = nullptr, rowc = nullptr, colc = nullptr;
     cudaStream_t cstream = nullptr;          // SUMMA stage broadcasts (pipelined)
+    float *cohen_M_pre = nullptr;            // a precomputed Cohen first layer for the next call
+    int cohen_M_r = 0;
     cudaEvent_t qev[5] = {};                 // ready[2], free[2], start
     int64_t gbin_budget = (int64_t)32 << 30;  // bytes of fp64 global-bin tables live at once
     float alpha = 1.2f;     // table sizing: need = alpha * Cohen estimate + 16
@@ -209,11 +211,19 @@ struct Prod {
 
 // Cohen estimate for the output columns of a product.
 int cohen(mcl_ctx *c, const Prod &pr, int r, uint64_t seed, float *est, float *keys_out) {
-    float *X, *M;
-    RC(scratch_t(c, "cohen_X", (size_t)std::max<int64_t>(pr.A->nrows, 1) * r, &X));
-    RC(scratch_t(c, "cohen_M", (size_t)std::max<int64_t>(pr.A->ncols, 1) * r, &M));
-    CK(launch_cohen_keys(pr.A->nrows, pr.A->row0, r, seed, X, keys_out, c->stream));
-    CK(launch_cohen_min(pr.A->ncols, pr.A->col_ptr, pr.A->row_idx, 0, X, r, M, nullptr, c->stream));
+    float *M;
+    if (c->cohen_M_pre && c->cohen_M_r == r) {
+        // the first layer was computed distributedly (SUMMA 1 x N: each rank its own
+        // column block, then broadcast), see mcl_summa_iterate
+        M = c->cohen_M_pre;
+        c->cohen_M_pre = nullptr;
+    } else {
+        float *X;
+        RC(scratch_t(c, "cohen_X", (size_t)std::max<int64_t>(pr.A->nrows, 1) * r, &X));
+        RC(scratch_t(c, "cohen_M", (size_t)std::max<int64_t>(pr.A->ncols, 1) * r, &M));
+        CK(launch_cohen_keys(pr.A->nrows, pr.A->row0, r, seed, X, keys_out, c->stream));
+        CK(launch_cohen_min(pr.A->ncols, pr.A->col_ptr, pr.A->row_idx, 0, X, r, M, nullptr, c->stream));
+    }
     CK(launch_cohen_min(pr.n, pr.B->col_ptr, pr.B->row_idx, pr.cb, M, r, nullptr, est, c->stream));
     return MCL_OK;
 }
@@ -1591,6 +1601,28 @@ int mcl_summa_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, 
             const int64_t c0 = cut(n, P, r), nc = cut(n, P, r + 1) - c0;
             CK(launch_offset_colptr(nc + 1, cps + c0 + r, off[r], fcp + c0, c->stream));
         }
+        // Cohen's first layer (min of the row keys over each column of A) is the
+        // one estimator pass over all of A: each rank computes it for its own column block
+        // and the blocks are broadcast, instead of every rank redoing all of A
+        if (pin->estimator != 1) {
+            const int rk = pin->est_keys;
+            float *X, *Mf;
+            RC(scratch_t(c, "cohen_X", (size_t)std::max<int64_t>(n, 1) * rk, &X));
+            RC(scratch_t(c, "cohen_Mfull", (size_t)std::max<int64_t>(n, 1) * rk, &Mf));
+            CK(launch_cohen_keys(n, 0, rk, pin->seed, X, nullptr, c->stream));
+            const int64_t my0 = cut(n, P, c->rank);
+            CK(launch_cohen_min(A->ncols, A->col_ptr, A->row_idx, 0, X, rk, Mf + my0 * rk, nullptr,
+                                c->stream));
+            NC(ncclGroupStart());
+            for (int r = 0; r < P; r++) {
+                const int64_t c0 = cut(n, P, r), nc = cut(n, P, r + 1) - c0;
+                if (nc) NC(ncclBroadcast(Mf + c0 * rk, Mf + c0 * rk, nc * rk, ncclFloat32, r, c->world,
+                                         c->stream));
+            }
+            NC(ncclGroupEnd());
+            c->cohen_M_pre = Mf;
+            c->cohen_M_r = rk;
+        }
         mcl_csc_t Af;
         zero_csc(&Af);
         Af.nrows = n;
@@ -1600,7 +1632,9 @@ int mcl_summa_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, 
         Af.col_ptr = fcp;
         Af.row_idx = frow;
         Af.val = fval;
-        RC(mcl_iterate_range(c, &Af, A->col0, A->col0 + A->ncols, pin, A_next, st));
+        const int rc_it = mcl_iterate_range(c, &Af, A->col0, A->col0 + A->ncols, pin, A_next, st);
+        c->cohen_M_pre = nullptr;  // consumed by that call (or dropped on its failure)
+        RC(rc_it);
         float chaos = st ? st->chaos : 0.f;
         float *cm;
         RC(scratch_t(c, "chaos_max", 4, &cm));
