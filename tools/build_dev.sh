@@ -2,6 +2,6 @@
 # development: build libmclx.so and the -DMCLX_PROF copy (tools/libmclx_prof.so)
 set -e
 cd "$(dirname "$0")/.."
-MCLX_NVCC_EXTRA=-DMCLX_PROF python -c "from paper_2002_10083_b200 import _build; _build.build(force=True)"
+MCLX_NVCC_EXTRA=-DMCLX_PROF python paper_2002_10083_b200/_build.py
 cp paper_2002_10083_b200/libmclx.so tools/libmclx_prof.so
-python -c "from paper_2002_10083_b200 import _build; _build.build(force=True)"
+python paper_2002_10083_b200/_build.py
