@@ -48,8 +48,20 @@ __device__ unsigned long long g_prof[12];
 #define PROF_ADD(i, v) ((void)0)
 #endif
 
-constexpr int kItems = 4;   // sub-segment chunks whose gathers a warp keeps in flight
+#ifndef MCLX_KITEMS
+#define MCLX_KITEMS 4
+#endif
+constexpr int kItems = MCLX_KITEMS;  // sub-segment chunks whose gathers a warp keeps in flight
 
+
+// Double hashing for the private slices: an odd step from a second hash of the row, so a
+// power-of-two slice is walked in a full cycle and keys that share a home slot part ways
+// after one probe (linear probing's primary clusters make the warp-uniform probe loop wait
+// for the longest run among ~100 lane-items).  Slices are powers of two (CAP / W, or the
+// global bin's 64 W 2^k).
+__device__ __forceinline__ uint32_t probe_step(int row, uint32_t scap) {
+    return (((uint32_t)row * 0x85EBCA6Bu) >> 15 | 1u) & (scap - 1);
+}
 
 // Open addressing with linear probing, four keys per lane at a time.  Phase 1 finds
 // the slot of every (row) -- the first probe of all four is issued back to back, and
@@ -114,7 +126,7 @@ __device__ __forceinline__ int group_size_for(int64_t avg) {
 }
 
 // Insert kItems (row, v) per lane into this warp's private slice (keys, vals)[0, scap):
-// open addressing with linear probing, empty slots claimed with an integer atomicCAS (lanes
+// open addressing with double hashing (probe_step), empty slots claimed with an integer atomicCAS (lanes
 // of the warp may race for one slot), `fill` (warp-uniform) counts claimed slots and
 // passing `limit` (7/8 of the slice) reports overflow so the column is re-run in a bigger
 // bin.  All 32 lanes must call.  (item u: lanes hold distinct rows of one sub-segment;
@@ -160,7 +172,7 @@ __device__ __forceinline__ bool warp_insert_n(int *keys, V *vals, uint32_t scap,
                         need[u] = old != row[u];
                     }
                 } else {
-                    s[u] = (s[u] + 1 == scap) ? 0u : s[u] + 1;
+                    s[u] = (s[u] + probe_step(row[u], scap)) & (scap - 1);
                     k[u] = vk[s[u]];
                     need[u] = k[u] != row[u];
                 }
@@ -431,7 +443,11 @@ __global__ void __launch_bounds__(NT, (bin_min_blocks<CAP, NT, MODE, GLOBAL, ATO
             int rr[kItems];
             float av[kItems], bb[kItems];
             int ml = g < q1 ? fetch(g, eb, c, clo, clen, cdb, rr, av, bb) : 0;
-            while (g < q1 && ok) {
+            // one pipeline step: fetch the next batch into (nr, na, nb), insert the current
+            // one from (cr, ca, cb).  The loop below runs it twice per trip with the two
+            // register sets swapped, so no batch is copied between them.
+            auto step = [&](int (&cr)[kItems], float (&ca)[kItems], float (&cb)[kItems],
+                            int (&nr)[kItems], float (&na)[kItems], float (&nb)[kItems]) {
                 // position of the next batch
                 int neb = eb, nc = c + 32;
                 int64_t ng = g;
@@ -448,16 +464,14 @@ __global__ void __launch_bounds__(NT, (bin_min_blocks<CAP, NT, MODE, GLOBAL, ATO
                         load_desc(ng + 32, nlo, nlen, ndb);
                     }
                 }
-                int nrr[kItems];
-                float nav[kItems], nbb[kItems];
-                const int nml = ng < q1 ? fetch(ng, neb, nc, clo, clen, cdb, nrr, nav, nbb) : 0;
+                const int nml = ng < q1 ? fetch(ng, neb, nc, clo, clen, cdb, nr, na, nb) : 0;
                 // insert the current batch
                 bool vl[kItems];
                 V vv[kItems];
     #pragma unroll
                 for (int u = 0; u < kItems; u++) {
-                    vl[u] = rr[u] >= 0;
-                    vv[u] = GLOBAL ? (V)av[u] * (V)bb[u] : (V)(av[u] * bb[u]);
+                    vl[u] = cr[u] >= 0;
+                    vv[u] = GLOBAL ? (V)ca[u] * (V)cb[u] : (V)(ca[u] * cb[u]);
                 }
 #ifdef MCLX_PROF
     #pragma unroll
@@ -466,19 +480,20 @@ __global__ void __launch_bounds__(NT, (bin_min_blocks<CAP, NT, MODE, GLOBAL, ATO
                     prof_valid += __popc(__ballot_sync(0xffffffffu, vl[u]));
                 }
 #endif
-                if (!warp_insert_n<MODE, V, kItems>(wkeys, wvals, scap, vl, rr, vv, fill, limit,
+                if (!warp_insert_n<MODE, V, kItems>(wkeys, wvals, scap, vl, cr, vv, fill, limit,
                                                     prof_passes))
                     ok = false;
-    #pragma unroll
-                for (int u = 0; u < kItems; u++) {
-                    rr[u] = nrr[u];
-                    av[u] = nav[u];
-                    bb[u] = nbb[u];
-                }
                 g = ng;
                 eb = neb;
                 c = nc;
                 ml = nml;
+            };
+            int rr2[kItems];
+            float av2[kItems], bb2[kItems];
+            while (g < q1 && ok) {
+                step(rr, av, bb, rr2, av2, bb2);
+                if (!(g < q1 && ok)) break;
+                step(rr2, av2, bb2, rr, av, bb);
             }
             fresh = lane == 0 ? fill : 0;
 #ifdef MCLX_PROF
@@ -808,14 +823,24 @@ static cudaError_t launch_of(const BinArgs &a, int grid, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// threads of the private-family bins 3-5 (development overrides: -DMCLX_NT3=... etc.)
+#ifndef MCLX_NT3
+#define MCLX_NT3 128
+#endif
+#ifndef MCLX_NT4
+#define MCLX_NT4 256
+#endif
+#ifndef MCLX_NT5
+#define MCLX_NT5 512
+#endif
 #define MCLX_BIN_SWITCH(MODE, WHAT, ...)                                          \
     switch (bin) {                                                                \
         case 0: return WHAT<512, 32, MODE, false, false>(__VA_ARGS__);            \
         case 1: return WHAT<1024, 32, MODE, false, false>(__VA_ARGS__);           \
         case 2: return WHAT<2048, 64, MODE, false, false>(__VA_ARGS__);           \
-        case 3: return WHAT<4096, 128, MODE, false, false>(__VA_ARGS__);          \
-        case 4: return WHAT<8192, 256, MODE, false, false>(__VA_ARGS__);          \
-        case 5: return WHAT<16384, 512, MODE, false, false>(__VA_ARGS__);         \
+        case 3: return WHAT<4096, MCLX_NT3, MODE, false, false>(__VA_ARGS__);       \
+        case 4: return WHAT<8192, MCLX_NT4, MODE, false, false>(__VA_ARGS__);       \
+        case 5: return WHAT<16384, MCLX_NT5, MODE, false, false>(__VA_ARGS__);       \
         case 6: return WHAT<0, kGlobalThreads, MODE, true, false>(__VA_ARGS__);   \
         case 7: return WHAT<512, 64, MODE, false, true>(__VA_ARGS__);             \
         case 8: return WHAT<1024, 64, MODE, false, true>(__VA_ARGS__);            \
