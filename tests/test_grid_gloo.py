@@ -1,4 +1,4 @@
-"""Multi-process (gloo, world size 2 and 4 on CPU) check of the Sparse-SUMMA schedule of
+"""Multi-process (gloo, world size 2, 4 and 8 on CPU) check of the Sparse-SUMMA schedule of
 paper_2002_10083_b200.grid: every rank holds only its block, owners broadcast the panels
 named by the grid arithmetic, each rank multiplies them (oracle spgemm) and merges the
 stage partials under Alg. 2; the result must equal the oracle's A.A restricted to the
@@ -77,7 +77,7 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("pr,pc", [(1, 2), (2, 1), (2, 2)])
+@pytest.mark.parametrize("pr,pc", [(1, 2), (2, 1), (2, 2), (1, 4), (1, 8), (2, 4)])
 def test_summa_schedule_gloo(pr, pc):
     ctx = mp.get_context("spawn")
     errq = ctx.Queue()
