@@ -342,6 +342,8 @@ def run_gpu(args):
     # this rank's result block (col_ptr, rows, vals) back.  Time: max over ranks; bytes:
     # summed over ranks.
     e2e = None
+    if args.e2e_steps is None:
+        args.e2e_steps = args.steps
     if args.e2e_steps > 0:
         hc = A.colptr.cpu().pin_memory()
         hr = A.rows.cpu().pin_memory()
@@ -520,7 +522,8 @@ def main():
                     help="N>1: the 2D Sparse-SUMMA (default) or column partition + all-gather")
     ap.add_argument("--grid", default=None, help="pr x pc for --mode summa, e.g. 2x2 (default "
                     "1xN: whole columns per rank, stages accumulated in the fused kernel)")
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=None,
+                    help="pipelined end-to-end steps timed (default: --steps; 0 skips e2e)")
     ap.add_argument("--cpu-flops", type=float, default=5e8)
     ap.add_argument("--ref-flops", type=float, default=2e8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
