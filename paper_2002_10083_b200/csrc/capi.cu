@@ -129,9 +129,20 @@ int scratch_t(mcl_ctx *c, const char *name, size_t count, T **out) {
     return scratch(c, name, count * sizeof(T), (void **)out);
 }
 
-// Copy `bytes` from device to the pinned buffer and wait for the stream.
+// Small read-backs are stored by a one-CTA kernel straight into the pinned buffer (mapped
+// under UVA) instead of a D2H memcpy: copy-engine work is served in order, so a memcpy here
+// would wait behind a caller's large D2H on another stream (the e2e bench's result read-back
+// of the previous step) and stall the iteration at each of its host syncs.
+__global__ void k_readback(const unsigned char *__restrict__ src, unsigned char *dst, size_t n) {
+    for (size_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+}
+
+// Copy `bytes` (<= 4096) from device to the pinned buffer and wait for the stream.
 int readback(mcl_ctx *c, const void *dev, size_t bytes, void *host) {
-    CK(cudaMemcpyAsync(c->pin, dev, bytes, cudaMemcpyDeviceToHost, c->stream));
+    if (bytes > 4096) return fail(c, MCL_ERR_INVALID_ARG, "readback: %zu bytes > 4096", bytes);
+    if (bytes == 0) return MCL_OK;
+    k_readback<<<1, 256, 0, c->stream>>>((const unsigned char *)dev, (unsigned char *)c->pin, bytes);
+    CK(cudaGetLastError());
     CK(cudaStreamSynchronize(c->stream));
     memcpy(host, c->pin, bytes);
     return MCL_OK;
