@@ -14,7 +14,8 @@
  *    column-by-column, no transpose).  All pointers inside mcl_csc_t are DEVICE
  *    pointers on the context's device.  col_ptr is int64 [ncols+1] with
  *    col_ptr[0] = 0 and non-decreasing; row_idx is int32 [nnz], strictly
- *    increasing inside each column; val is fp32 [nnz], finite and > 0.
+ *    increasing inside each column; val is fp32 [nnz], finite and > 0 (>= 0 for an
+ *    unpruned product, whose entries may underflow to 0, Q13).
  *  - Inputs are BORROWED: owned by the caller, valid in stream order for the
  *    duration of the call, never modified.
  *  - Outputs (mcl_csc_t *out arguments) are ALLOCATED BY THE LIBRARY through
@@ -48,12 +49,17 @@ enum {
     MCL_OK = 0,
     MCL_ERR_INVALID_ARG = -1,       /* NULL pointer, r <= 1, S < 1, pct outside [0,1], theta < 0, ... */
     MCL_ERR_DIM = -2,               /* A.ncols != B.nrows, non-square where A*A is needed, bad range */
-    MCL_ERR_FORMAT = -3,            /* only with env MCLX_VALIDATE=1: malformed CSC                    */
+    MCL_ERR_FORMAT = -3,            /* only with env MCLX_VALIDATE=1 (checked on the device for every
+                                       input matrix): col_ptr not 0-based / non-decreasing / ending at
+                                       nnz, a row outside [0, nrows) or not strictly increasing in its
+                                       column, a negative or non-finite value          */
     MCL_ERR_OOM = -4,               /* allocator returned NULL                                          */
     MCL_ERR_CUDA = -5,              /* a CUDA runtime error (message in mcl_last_error)                 */
     MCL_ERR_NCCL = -6,              /* an NCCL error                                                    */
     MCL_ERR_UNSUPPORTED_DEVICE = -7,/* device is not sm_100 (B200)                                      */
-    MCL_ERR_NOT_IMPLEMENTED = -8
+    MCL_ERR_NOT_IMPLEMENTED = -8,
+    MCL_ERR_INTERNAL = -9           /* a device consistency check failed, or a hash table overflowed
+                                       even at the exact size bound min(f_j, m) (a library bug)     */
 };
 
 /* A CSC block.  (row0, col0, n_global) place the block in a global matrix for the

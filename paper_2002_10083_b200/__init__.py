@@ -42,7 +42,7 @@ except OSError as e:  # pragma: no cover
 MCL_OK = 0
 ERRORS = {-1: "MCL_ERR_INVALID_ARG", -2: "MCL_ERR_DIM", -3: "MCL_ERR_FORMAT", -4: "MCL_ERR_OOM",
           -5: "MCL_ERR_CUDA", -6: "MCL_ERR_NCCL", -7: "MCL_ERR_UNSUPPORTED_DEVICE",
-          -8: "MCL_ERR_NOT_IMPLEMENTED"}
+          -8: "MCL_ERR_NOT_IMPLEMENTED", -9: "MCL_ERR_INTERNAL"}
 NUM_BINS = 6
 
 

@@ -58,6 +58,7 @@ struct mcl_ctx {
     int64_t fp64_terms = kFp64Terms;          // MCLX_FP64_TERMS (tests)
     int64_t cap_budget = (int64_t)16 << 30;   // unfused products: upper-bound slots up to this
     bool split_private = true;                // MCLX_SPLIT_PRIVATE=0: P <= 4 parts shared-table too
+    bool validate = false;                    // MCLX_VALIDATE=1: check input CSC invariants
 };
 
 namespace {
@@ -133,14 +134,18 @@ int scratch_t(mcl_ctx *c, const char *name, size_t count, T **out) {
 // under UVA) instead of a D2H memcpy: copy-engine work is served in order, so a memcpy here
 // would wait behind a caller's large D2H on another stream (the e2e bench's result read-back
 // of the previous step) and stall the iteration at each of its host syncs.
+constexpr size_t kPinBytes = 65536;  // mapped pinned read-back buffer
+
 __global__ void k_readback(const unsigned char *__restrict__ src, unsigned char *dst, size_t n) {
     for (size_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
 }
 
-// Copy `bytes` (<= 4096) from device to the pinned buffer and wait for the stream.
+// Copy `bytes` (<= kPinBytes) from device to the pinned buffer and wait for the stream.
 int readback(mcl_ctx *c, const void *dev, size_t bytes, void *host) {
-    if (bytes > 4096) return fail(c, MCL_ERR_INVALID_ARG, "readback: %zu bytes > 4096", bytes);
+    if (bytes > kPinBytes) return fail(c, MCL_ERR_INVALID_ARG, "readback: %zu bytes > %zu", bytes, kPinBytes);
     if (bytes == 0) return MCL_OK;
+    if (!dev) return fail(c, MCL_ERR_INVALID_ARG, "readback from a NULL device pointer");
+    ++g_launches;
     k_readback<<<1, 256, 0, c->stream>>>((const unsigned char *)dev, (unsigned char *)c->pin, bytes);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(c->stream));
@@ -151,6 +156,26 @@ int readback(mcl_ctx *c, const void *dev, size_t bytes, void *host) {
 void zero_csc(mcl_csc_t *m) {
     if (m) memset(m, 0, sizeof *m);
 }
+
+void free_csc(mcl_ctx *c, mcl_csc_t *m) {
+    dfree(c, m->col_ptr, 0);
+    dfree(c, m->row_idx, 0);
+    dfree(c, m->val, 0);
+    zero_csc(m);
+}
+
+// Frees an output matrix on every early return unless release()d: the header's "on
+// error, outputs are zeroed and nothing leaks" contract for the entry points.
+struct OutGuard {
+    mcl_ctx *c;
+    mcl_csc_t *m;
+    bool armed = true;
+    OutGuard(mcl_ctx *c_, mcl_csc_t *m_) : c(c_), m(m_) {}
+    ~OutGuard() {
+        if (armed && m) free_csc(c, m);
+    }
+    void release() { armed = false; }
+};
 
 int alloc_rows_vals(mcl_ctx *c, mcl_csc_t *m, int64_t nnz) {
     m->nnz = nnz;
@@ -168,6 +193,21 @@ int check_csc(mcl_ctx *c, const mcl_csc_t *m, const char *what) {
     if (m->nnz > 0 && (!m->row_idx || !m->val))
         return fail(c, MCL_ERR_INVALID_ARG, "%s has nnz > 0 but NULL arrays", what);
     if (m->nrows > 0x7ffffffeLL) return fail(c, MCL_ERR_DIM, "%s: more than 2^31-2 rows", what);
+    if (c->validate) {  // MCLX_VALIDATE=1: the CSC invariants, checked on the device
+        int *flag;
+        RC(scratch_t(c, "validate_flag", 1, &flag));
+        CK(cudaMemsetAsync(flag, 0, sizeof(int), c->stream));
+        CK(launch_validate_csc(m->ncols, m->nrows, m->nnz, m->col_ptr, m->row_idx, m->val, flag,
+                               c->stream));
+        int h = 0;
+        RC(readback(c, flag, sizeof(int), &h));
+        if (h)
+            return fail(c, MCL_ERR_FORMAT, "%s is not a valid CSC:%s%s%s%s", what,
+                        (h & 1) ? " col_ptr not 0-based / non-decreasing / ending at nnz;" : "",
+                        (h & 2) ? " row index out of range;" : "",
+                        (h & 4) ? " rows not strictly increasing in a column;" : "",
+                        (h & 8) ? " a value is negative or not finite;" : "");
+    }
     return MCL_OK;
 }
 
@@ -660,7 +700,7 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
         }
         if (nretry == 0) break;
         if (round == nrounds - 1)
-            return fail(c, MCL_ERR_CUDA, "hash table overflow after exact re-binning");
+            return fail(c, MCL_ERR_INTERNAL, "hash table overflow after exact re-binning");
         if (st) st->retries += nretry;
         CK(cudaMemcpyAsync(retry_in, retry_list, sizeof(int32_t) * nretry, cudaMemcpyDeviceToDevice,
                            c->stream));
@@ -674,7 +714,7 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
     }
     int herr = 0;
     RC(readback(c, err, sizeof(int), &herr));
-    if (herr) return fail(c, MCL_ERR_CUDA, "device consistency check failed (code %d)", herr);
+    if (herr) return fail(c, MCL_ERR_INTERNAL, "device consistency check failed (code %d)", herr);
     return MCL_OK;
 }
 
@@ -976,11 +1016,11 @@ int dist_prune(mcl_ctx *c, const mcl_csc_t *C, ncclComm_t comm, const PruneParam
     // exact global top-K cut of the select columns (same list, same order on every rank)
     CK(launch_dp_sellist(n, mode, selflag, selpos, sel, tmp, c->stream));
     int64_t nsel = 0;
-    {
+    if (n > 0) {
         int64_t last[2];
         RC(readback(c, selpos + n - 1, sizeof(int64_t), &last[0]));
         RC(readback(c, selflag + n - 1, sizeof(int64_t), &last[1]));
-        nsel = n > 0 ? last[0] + last[1] : 0;
+        nsel = last[0] + last[1];
     }
     if (nsel > 0) {
         RC(scratch_t(c, "dp_hist", 256 * (size_t)nsel, &hist));
@@ -1033,13 +1073,6 @@ int dist_prune(mcl_ctx *c, const mcl_csc_t *C, ncclComm_t comm, const PruneParam
     return MCL_OK;
 }
 
-void free_csc(mcl_ctx *c, mcl_csc_t *m) {
-    dfree(c, m->col_ptr, 0);
-    dfree(c, m->row_idx, 0);
-    dfree(c, m->val, 0);
-    zero_csc(m);
-}
-
 }  // namespace
 
 // ====================================================================== public API
@@ -1083,6 +1116,7 @@ int mcl_ctx_create(mcl_ctx_t *out, int device, void *stream, mcl_alloc_fn alloc,
     c->free_fn = free_fn;
     c->state = alloc_state;
     c->sms = prop.multiProcessorCount;
+    g_sms = c->sms;
     if (const char *e = getenv("MCLX_ALPHA")) c->alpha = (float)atof(e);
     if (const char *e = getenv("MCLX_MAX_LOAD")) c->max_load = (float)atof(e);
     if (const char *e = getenv("MCLX_ORDER")) c->order_lists = atoi(e) != 0;
@@ -1095,7 +1129,8 @@ int mcl_ctx_create(mcl_ctx_t *out, int device, void *stream, mcl_alloc_fn alloc,
     if (const char *e = getenv("MCLX_SPLIT_PART_NEED"))
         c->split_part_need = std::max<int64_t>(16, std::min<int64_t>(kPartNeed, atoll(e)));
     if (const char *e = getenv("MCLX_GBIN_BUDGET_MB")) c->gbin_budget = (int64_t)atoll(e) << 20;
-    if (cudaMallocHost(&c->pin, 4096) != cudaSuccess) {
+    if (const char *e = getenv("MCLX_VALIDATE")) c->validate = atoi(e) != 0;
+    if (cudaMallocHost(&c->pin, kPinBytes) != cudaSuccess) {
         delete c;
         return MCL_ERR_CUDA;
     }
@@ -1173,6 +1208,7 @@ int mcl_preprocess(mcl_ctx_t c, const mcl_csc_t *G, int add_loops, mcl_csc_t *A_
     CK(launch_pre_count(n, G->col_ptr, G->row_idx, add_loops, cnt, c->stream));
     mcl_csc_t out;
     zero_csc(&out);
+    OutGuard guard(c, &out);
     out.col_ptr = (int64_t *)dalloc(c, (size_t)(n + 1) * sizeof(int64_t));
     if (!out.col_ptr) return fail(c, MCL_ERR_OOM, "col_ptr");
     CK(launch_scan_i64(cnt, out.col_ptr, n, tmp, c->stream));
@@ -1185,6 +1221,7 @@ int mcl_preprocess(mcl_ctx_t c, const mcl_csc_t *G, int add_loops, mcl_csc_t *A_
     CK(launch_pre_fill(n, G->col_ptr, G->row_idx, G->val, add_loops, out.col_ptr, out.row_idx,
                        out.val, c->stream));
     *A_out = out;
+    guard.release();
     return MCL_OK;
 }
 
@@ -1307,6 +1344,7 @@ int mcl_prune_inflate(mcl_ctx_t c, const mcl_csc_t *C, const mcl_params_t *pin, 
                     chaos_dev ? chaos_dev : chaos, cmax, pp, grid, c->stream));
     CK(cudaEventRecord(c->ev[1], c->stream));
     int64_t nnz = 0;
+    OutGuard guard(c, A_next);
     RC(assemble(c, C->nrows, n, cnt, soff, srow, sval, A_next, &nnz));
     A_next->row0 = C->row0;
     A_next->col0 = C->col0;
@@ -1325,6 +1363,7 @@ int mcl_prune_inflate(mcl_ctx_t c, const mcl_csc_t *C, const mcl_params_t *pin, 
         st->peak_bytes = (int64_t)c->peak;
         st->launches = g_launches - launches0;
     }
+    guard.release();
     return MCL_OK;
 }
 
@@ -1420,6 +1459,7 @@ int mcl_iterate_range(mcl_ctx_t c, const mcl_csc_t *A, int64_t col_begin, int64_
     CK(cudaEventRecord(c->ev[4], c->stream));
     // a8: assemble A_next
     int64_t nnz = 0;
+    OutGuard guard(c, A_next);
     RC(assemble(c, A->nrows, n, cnt, soff, srow, sval, A_next, &nnz));
     A_next->row0 = A->row0;
     A_next->col0 = A->col0 + col_begin;
@@ -1444,6 +1484,7 @@ int mcl_iterate_range(mcl_ctx_t c, const mcl_csc_t *A, int64_t col_begin, int64_
         st->peak_bytes = (int64_t)c->peak;
         st->launches = g_launches - launches0;
     }
+    guard.release();
     return MCL_OK;
 }
 
@@ -1493,6 +1534,7 @@ int mcl_block(mcl_ctx_t c, const mcl_csc_t *A, int64_t r0, int64_t r1, int64_t c
     RC(scratch(c, "scan_tmp", scan_tmp_bytes(nc + 1), &tmp));
     mcl_csc_t o;
     zero_csc(&o);
+    OutGuard guard(c, &o);
     o.col_ptr = (int64_t *)dalloc(c, sizeof(int64_t) * (nc + 1));
     if (!o.col_ptr) return fail(c, MCL_ERR_OOM, "col_ptr");
     CK(launch_rowslice_count(nc, A->col_ptr + c0, A->row_idx, r0, r1, first, cnt, c->stream));
@@ -1508,6 +1550,7 @@ int mcl_block(mcl_ctx_t c, const mcl_csc_t *A, int64_t r0, int64_t r1, int64_t c
     o.col0 = A->col0 + c0;
     o.n_global = A->n_global ? A->n_global : A->nrows;
     *out = o;
+    guard.release();
     return MCL_OK;
 }
 
@@ -1646,6 +1689,7 @@ int mcl_summa_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, 
         const int rc_it = mcl_iterate_range(c, &Af, A->col0, A->col0 + A->ncols, pin, A_next, st);
         c->cohen_M_pre = nullptr;  // consumed by that call (or dropped on its failure)
         RC(rc_it);
+        OutGuard guard(c, A_next);
         float chaos = st ? st->chaos : 0.f;
         float *cm;
         RC(scratch_t(c, "chaos_max", 4, &cm));
@@ -1657,6 +1701,7 @@ int mcl_summa_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, 
             st->comm_bytes = (tot - my) * 8 + (n - A->ncols) * 8;
             st->phases = 1;
         }
+        guard.release();
         return MCL_OK;
     }
     const int s = pr / gcd_i(pr, pc) * pc;  // lcm
@@ -1859,6 +1904,7 @@ int mcl_summa_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, 
     CK(cudaEventRecord(c->sev[1], c->stream));
     mcl_csc_t Cb = stack[0];
     float chaos = 0.f;
+    OutGuard guard(c, A_next);
     rc = dist_prune(c, &Cb, pr > 1 ? c->colc : nullptr, pp, A_next, &chaos);
     const int64_t nnz_unpruned = Cb.nnz;
     free_csc(c, &Cb);
@@ -1909,6 +1955,7 @@ int mcl_summa_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, 
         st->peak_bytes = (int64_t)c->peak;
         st->launches = g_launches - launches0;
     }
+    guard.release();
     return MCL_OK;
 }
 

@@ -26,6 +26,9 @@ enum Mode { kSym = 0, kNum = 1, kFused = 2, kPart = 3 };
 
 // Host-side count of kernel launches issued by this library (reported in mcl_stats_t).
 extern int64_t g_launches;
+// Multiprocessor count of the current context's device (set by mcl_ctx_create); launch
+// helpers size persistent grids as multiples of it.
+extern int g_sms;
 
 struct BinArgs {
     // operands: C = A * B[:, cb : cb + ncols_out)
@@ -113,6 +116,10 @@ cudaError_t launch_rowpart(int64_t ncols, const int64_t *cp, const int32_t *row,
                            int *rowpart, cudaStream_t s, int nparts = 32);
 
 // misc kernels (kernels_misc.cu)
+// CSC invariants of include/mclx.h (MCLX_VALIDATE); *flag |= 1 col_ptr, 2 row range,
+// 4 row order, 8 value (not finite or <= 0)
+cudaError_t launch_validate_csc(int64_t ncols, int64_t nrows, int64_t nnz, const int64_t *cp,
+                                const int32_t *row, const float *val, int *flag, cudaStream_t s);
 cudaError_t launch_flops(int64_t ncols, const int64_t *acp, const int64_t *bcp,
                          const int32_t *brow, int64_t cb, int64_t *f, cudaStream_t s);
 cudaError_t launch_reduce_i64(const int64_t *x, int64_t n, unsigned long long *out, cudaStream_t s);

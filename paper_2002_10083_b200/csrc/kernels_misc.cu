@@ -8,6 +8,7 @@
 namespace mclx {
 
 int64_t g_launches = 0;
+int g_sms = 148;  // SMs of the context's device (mcl_ctx_create sets it); caps grid sizes
 
 // ------------------------------------------------------------------ flops
 // f_j = sum_{k in inds(B_*j)} nnz(A_*k).  One warp per column.
@@ -32,9 +33,49 @@ cudaError_t launch_flops(int64_t ncols, const int64_t *acp, const int64_t *bcp,
                          const int32_t *brow, int64_t cb, int64_t *f, cudaStream_t s) {
     if (ncols <= 0) return cudaSuccess;
     int64_t blocks = (ncols * 32 + 255) / 256;
-    if (blocks > 148 * 64) blocks = 148 * 64;
+    if (blocks > g_sms * 64) blocks = g_sms * 64;
     ++g_launches;
     k_flops<<<(int)blocks, 256, 0, s>>>(ncols, acp, bcp, brow, cb, f);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ CSC validation
+// MCLX_VALIDATE=1 (include/mclx.h MCL_ERR_FORMAT): the CSC invariants of the header --
+// col_ptr[0] = 0, non-decreasing, col_ptr[n] = nnz; rows in [0, nrows) and strictly
+// increasing inside each column; values finite and >= 0 (negative -> rejection,
+// S:70; an unpruned product entry may underflow to 0, Q13).  One warp per
+// column; violations OR bits into *flag (1 col_ptr, 2 row range, 4 row order, 8 value).
+__global__ void k_validate_csc(int64_t ncols, int64_t nrows, int64_t nnz,
+                               const int64_t *__restrict__ cp, const int32_t *__restrict__ row,
+                               const float *__restrict__ val, int *flag) {
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = lane_id();
+    if (w == 0 && lane == 0 && (cp[0] != 0 || cp[ncols] != nnz)) atomicOr(flag, 1);
+    for (int64_t col = w; col < ncols; col += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t q0 = cp[col], q1 = cp[col + 1];
+        int bad = 0;
+        if (q1 < q0 || q0 < 0 || q1 > nnz) {
+            bad = 1;
+        } else {
+            for (int64_t q = q0 + lane; q < q1; q += 32) {
+                const int r = row[q];
+                if (r < 0 || r >= nrows) bad |= 2;
+                if (q > q0 && row[q - 1] >= r) bad |= 4;
+                const float v = val[q];
+                if (!(v >= 0.f) || !isfinite(v)) bad |= 8;  // NaN, inf or negative
+            }
+        }
+        bad = __reduce_or_sync(0xffffffffu, bad);
+        if (lane == 0 && bad) atomicOr(flag, bad);
+    }
+}
+
+cudaError_t launch_validate_csc(int64_t ncols, int64_t nrows, int64_t nnz, const int64_t *cp,
+                                const int32_t *row, const float *val, int *flag, cudaStream_t s) {
+    int64_t blocks = (std::max<int64_t>(ncols, 1) * 32 + 255) / 256;
+    if (blocks > g_sms * 32) blocks = g_sms * 32;
+    ++g_launches;
+    k_validate_csc<<<(int)blocks, 256, 0, s>>>(ncols, nrows, nnz, cp, row, val, flag);
     return cudaGetLastError();
 }
 
@@ -70,7 +111,7 @@ cudaError_t launch_rowpart(int64_t ncols, const int64_t *cp, const int32_t *row,
                            int *rowpart, cudaStream_t s, int nparts) {
     if (ncols <= 0) return cudaSuccess;
     int64_t blocks = (ncols * 32 + 255) / 256;
-    if (blocks > 148 * 32) blocks = 148 * 32;
+    if (blocks > g_sms * 32) blocks = g_sms * 32;
     ++g_launches;
     if (nparts == kFineParts) k_rowpart<kFineParts><<<(int)blocks, 256, 0, s>>>(ncols, cp, row, m, rowpart);
     else k_rowpart<32><<<(int)blocks, 256, 0, s>>>(ncols, cp, row, m, rowpart);
@@ -98,7 +139,7 @@ __global__ void k_reduce_f32(const float *__restrict__ x, int64_t n, double *out
 }
 static int red_grid(int64_t n) {
     int64_t b = (n + 255) / 256;
-    if (b > 148 * 4) b = 148 * 4;
+    if (b > g_sms * 4) b = g_sms * 4;
     return b < 1 ? 1 : (int)b;
 }
 cudaError_t launch_reduce_i64(const int64_t *x, int64_t n, unsigned long long *out, cudaStream_t s) {
@@ -279,7 +320,7 @@ __global__ void k_classify(ClassifyArgs c) {
 cudaError_t launch_classify(const ClassifyArgs &c, cudaStream_t s) {
     if (c.n <= 0) return cudaSuccess;
     int64_t b = (c.n + 255) / 256;
-    if (b > 148 * 16) b = 148 * 16;
+    if (b > g_sms * 16) b = g_sms * 16;
     ++g_launches;
     k_classify<<<(int)b, 256, 0, s>>>(c);
     return cudaGetLastError();
@@ -352,7 +393,7 @@ cudaError_t launch_split_gather(int64_t nitems, const int64_t *stg_cnt, const in
                                 int32_t *crow, float *cval, cudaStream_t s) {
     if (nitems <= 0) return cudaSuccess;
     int64_t b = (nitems + 7) / 8;
-    if (b > 148 * 16) b = 148 * 16;
+    if (b > g_sms * 16) b = g_sms * 16;
     ++g_launches;
     k_split_gather<<<(int)b, 256, 0, s>>>(nitems, stg_cnt, stg_off, stg_row, stg_val, sioff, crow,
                                           cval);
@@ -390,7 +431,7 @@ cudaError_t launch_minhash_key(int64_t n, const int64_t *bcp, const int32_t *bro
                                uint32_t *key, cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
     int64_t b = (n + 7) / 8;
-    if (b > 148 * 16) b = 148 * 16;
+    if (b > g_sms * 16) b = g_sms * 16;
     ++g_launches;
     k_minhash_key<<<(int)b, 256, 0, s>>>(n, bcp, brow, cb, key);
     return cudaGetLastError();
@@ -435,7 +476,7 @@ cudaError_t launch_order_lists(int64_t n, const int32_t *cols, const int32_t *co
     cudaError_t e = cudaMemsetAsync(hist, 0, sizeof(int64_t) * nbk, s);
     if (e != cudaSuccess) return e;
     int64_t b = (n + 255) / 256;
-    if (b > 148 * 16) b = 148 * 16;
+    if (b > g_sms * 16) b = g_sms * 16;
     ++g_launches;
     k_order_hist<<<(int)b, 256, 0, s>>>(n, cols, colbin, key, hist);
     if ((e = launch_scan_i64(hist, offs, nbk, scan_tmp, s)) != cudaSuccess) return e;
@@ -548,7 +589,7 @@ cudaError_t launch_copy_cols(int64_t ncols, const int64_t *cnt, const int64_t *s
                              int32_t *orow, float *oval, cudaStream_t s) {
     if (ncols <= 0) return cudaSuccess;
     int64_t blocks = (ncols * 32 + 255) / 256;
-    if (blocks > 148 * 32) blocks = 148 * 32;
+    if (blocks > g_sms * 32) blocks = g_sms * 32;
     ++g_launches;
     k_copy_cols<<<(int)blocks, 256, 0, s>>>(ncols, cnt, soff, srow, sval, cp, orow, oval);
     return cudaGetLastError();
@@ -627,7 +668,7 @@ cudaError_t launch_cohen_keys(int64_t m, int64_t row0, int r, uint64_t seed, flo
                               float *keys_out, cudaStream_t s) {
     if (m <= 0) return cudaSuccess;
     int64_t b = (m + 255) / 256;
-    if (b > 148 * 16) b = 148 * 16;
+    if (b > g_sms * 16) b = g_sms * 16;
     ++g_launches;
     k_cohen_keys<<<(int)b, 256, 0, s>>>(m, row0, r, seed, X, keys_out);
     return cudaGetLastError();
@@ -669,7 +710,7 @@ cudaError_t launch_cohen_min(int64_t ncols, const int64_t *cp, const int32_t *ro
                              const float *in, int r, float *out, float *est, cudaStream_t s) {
     if (ncols <= 0) return cudaSuccess;
     int64_t blocks = (ncols * 32 + 255) / 256;
-    if (blocks > 148 * 32) blocks = 148 * 32;
+    if (blocks > g_sms * 32) blocks = g_sms * 32;
     ++g_launches;
     k_cohen_min<<<(int)blocks, 256, 0, s>>>(ncols, cp, row, c0, in, r, out, est);
     return cudaGetLastError();
@@ -749,7 +790,7 @@ cudaError_t launch_pre_fill(int64_t n, const int64_t *gcp, const int32_t *grow, 
                             cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
     int64_t blocks = (n * 32 + 255) / 256;
-    if (blocks > 148 * 32) blocks = 148 * 32;
+    if (blocks > g_sms * 32) blocks = g_sms * 32;
     ++g_launches;
     k_pre_fill<<<(int)blocks, 256, 0, s>>>(n, gcp, grow, gw, add_loops, cp, row, val);
     return cudaGetLastError();
@@ -821,7 +862,7 @@ cudaError_t launch_cc(int64_t n, const int64_t *cp, const int32_t *row, int32_t 
     ++g_launches;
     k_cc_init<<<g, 256, 0, s>>>(n, parent);
     int64_t blocks = (n * 32 + 255) / 256;
-    if (blocks > 148 * 32) blocks = 148 * 32;
+    if (blocks > g_sms * 32) blocks = g_sms * 32;
     ++g_launches;
     k_cc_hook<<<(int)blocks, 256, 0, s>>>(n, cp, row, parent);
     ++g_launches;

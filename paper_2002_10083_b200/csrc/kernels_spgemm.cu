@@ -221,6 +221,10 @@ __global__ void __launch_bounds__(NT, (bin_min_blocks<CAP, NT, MODE, GLOBAL, ATO
     __shared__ double swd[4][NT / 32];
     constexpr int W = NT / 32;         // warps = row-range owners
     constexpr int PSTEP = kParts / W;  // rowpart boundaries per warp
+    // the private slices' double-hashing probe walks a full cycle only on a power-of-two
+    // slice, and the warps split the 32 rowparts evenly (MCLX_NT* overrides must keep this)
+    static_assert(ATOMIC || GLOBAL || (((CAP / W) & (CAP / W - 1)) == 0 && kParts % W == 0),
+                  "private-family bins need CAP / W a power of two and W | kParts");
 
     const int tid = threadIdx.x;
     const int lane = lane_id();

@@ -27,7 +27,7 @@ __global__ void k_rebase_colptr(int64_t n1, const int64_t *__restrict__ cp, int6
 cudaError_t launch_rebase_colptr(int64_t n1, const int64_t *cp, int64_t *out, cudaStream_t s) {
     if (n1 <= 0) return cudaSuccess;
     int64_t b = (n1 + 255) / 256;
-    if (b > 148 * 16) b = 148 * 16;
+    if (b > g_sms * 16) b = g_sms * 16;
     ++g_launches;
     k_rebase_colptr<<<(int)b, 256, 0, s>>>(n1, cp, out);
     return cudaGetLastError();
@@ -57,7 +57,7 @@ cudaError_t launch_rowslice_count(int64_t ncols, const int64_t *cp, const int32_
                                   int64_t r1, int64_t *first, int64_t *cnt, cudaStream_t s) {
     if (ncols <= 0) return cudaSuccess;
     int64_t b = (ncols + 255) / 256;
-    if (b > 148 * 16) b = 148 * 16;
+    if (b > g_sms * 16) b = g_sms * 16;
     ++g_launches;
     k_rowslice_count<<<(int)b, 256, 0, s>>>(ncols, cp, rows, r0, r1, first, cnt);
     return cudaGetLastError();
@@ -81,7 +81,7 @@ cudaError_t launch_rowslice_copy(int64_t ncols, const int64_t *first, const int6
                                  float *oval, cudaStream_t s) {
     if (ncols <= 0) return cudaSuccess;
     int64_t b = (ncols * 32 + 255) / 256;
-    if (b > 148 * 32) b = 148 * 32;
+    if (b > g_sms * 32) b = g_sms * 32;
     ++g_launches;
     k_rowslice_copy<<<(int)b, 256, 0, s>>>(ncols, first, ocp, rows, vals, r0, orow, oval);
     return cudaGetLastError();
@@ -98,7 +98,7 @@ __device__ __forceinline__ int64_t dp_warp0() {
 __device__ __forceinline__ int64_t dp_wstride() { return ((int64_t)gridDim.x * blockDim.x) >> 5; }
 static int dp_grid(int64_t ncols) {
     int64_t b = (ncols * 32 + kDP - 1) / kDP;
-    if (b > 148 * 32) b = 148 * 32;
+    if (b > g_sms * 32) b = g_sms * 32;
     return b < 1 ? 1 : (int)b;
 }
 
@@ -167,7 +167,7 @@ cudaError_t launch_dp_branch(int64_t ncols, const int64_t *nnz, const int64_t *m
                              uint32_t *prefix, int32_t *rowcut, cudaStream_t s) {
     if (ncols <= 0) return cudaSuccess;
     int64_t b = (ncols + 255) / 256;
-    if (b > 148 * 16) b = 148 * 16;
+    if (b > g_sms * 16) b = g_sms * 16;
     ++g_launches;
     k_dp_branch<<<(int)b, 256, 0, s>>>(ncols, nnz, m, sm, pp, K, mode, rem, prefix, rowcut);
     return cudaGetLastError();
@@ -277,7 +277,7 @@ cudaError_t launch_dp_digit(int64_t nsel, const int32_t *sel, const unsigned *hi
                             int32_t *rowcut, cudaStream_t s) {
     if (nsel <= 0) return cudaSuccess;
     int64_t b = (nsel * 32 + 255) / 256;
-    if (b > 148 * 32) b = 148 * 32;
+    if (b > g_sms * 32) b = g_sms * 32;
     ++g_launches;
     k_dp_digit<<<(int)b, 256, 0, s>>>(nsel, sel, hist, pass, vprefix, rprefix, rem, done, rowcut);
     return cudaGetLastError();
@@ -299,7 +299,7 @@ cudaError_t launch_dp_sellist(int64_t ncols, const int8_t *mode, int64_t *flag, 
                               int32_t *sel, void *tmp, cudaStream_t s) {
     if (ncols <= 0) return cudaSuccess;
     int64_t b = (ncols + 255) / 256;
-    if (b > 148 * 16) b = 148 * 16;
+    if (b > g_sms * 16) b = g_sms * 16;
     ++g_launches;
     k_dp_selflag<<<(int)b, 256, 0, s>>>(ncols, mode, flag);
     cudaError_t e = launch_scan_i64(flag, pos, ncols, tmp, s);
@@ -322,7 +322,7 @@ cudaError_t launch_dp_undone(int64_t nsel, const int32_t *sel, const int32_t *do
     cudaError_t e = cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), s);
     if (e != cudaSuccess || nsel <= 0) return e;
     ++g_launches;
-    k_dp_undone<<<(int)std::min<int64_t>((nsel + 255) / 256, 148 * 4), 256, 0, s>>>(nsel, sel, done,
+    k_dp_undone<<<(int)std::min<int64_t>((nsel + 255) / 256, g_sms * 4), 256, 0, s>>>(nsel, sel, done,
                                                                                   cnt);
     return cudaGetLastError();
 }
