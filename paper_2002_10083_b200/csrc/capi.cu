@@ -59,6 +59,7 @@ struct mcl_ctx {
     int64_t cap_budget = (int64_t)16 << 30;   // unfused products: upper-bound slots up to this
     bool split_private = true;                // MCLX_SPLIT_PRIVATE=0: P <= 4 parts shared-table too
     bool validate = false;                    // MCLX_VALIDATE=1: check input CSC invariants
+    int family = -1;                          // MCLX_FAMILY=0/1 forces a kernel family (A/B runs)
 };
 
 namespace {
@@ -475,6 +476,11 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
     RC(scratch_t(c, "rowpart", (size_t)std::max<int64_t>(pr.A->ncols, 1) * 33, &rowpart));
     CK(launch_rowpart(pr.A->ncols, pr.A->col_ptr, pr.A->row_idx, pr.A->nrows, rowpart, c->stream));
     base.rowpart = rowpart;
+    // interleaved (row, value) copy of A for the private family's 8-byte gathers
+    int2 *apair;
+    RC(scratch_t(c, "apair", (size_t)std::max<int64_t>(pr.A->nnz, 1), &apair));
+    CK(launch_pack_pairs(pr.A->nnz, pr.A->row_idx, pr.A->val, apair, c->stream));
+    base.apair = apair;
     // locality order of the work lists (MCLX_ORDER=0 turns it off)
     int32_t *colbin = nullptr;
     uint32_t *okey = nullptr;
@@ -529,7 +535,7 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
         ca.force_bin = force_bin < 0 ? -1 : force_bin % kFamily;
         // the private family addresses A with 32-bit offsets
         const bool big_a = pr.A->nnz >= ((int64_t)1 << 32);
-        ca.force_family = force_bin >= 0 ? force_bin / kFamily : (round > 0 || big_a) ? 1 : -1;
+        ca.force_family = force_bin >= 0 ? force_bin / kFamily : (round > 0 || big_a) ? 1 : c->family;
         ca.list_stride = std::max<int64_t>(n, 1);
         ca.bin_count = counts;
         ca.lists = lists;
@@ -1130,6 +1136,7 @@ int mcl_ctx_create(mcl_ctx_t *out, int device, void *stream, mcl_alloc_fn alloc,
         c->split_part_need = std::max<int64_t>(16, std::min<int64_t>(kPartNeed, atoll(e)));
     if (const char *e = getenv("MCLX_GBIN_BUDGET_MB")) c->gbin_budget = (int64_t)atoll(e) << 20;
     if (const char *e = getenv("MCLX_VALIDATE")) c->validate = atoi(e) != 0;
+    if (const char *e = getenv("MCLX_FAMILY")) c->family = atoi(e);
     if (cudaMallocHost(&c->pin, kPinBytes) != cudaSuccess) {
         delete c;
         return MCL_ERR_CUDA;

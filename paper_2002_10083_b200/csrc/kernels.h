@@ -41,6 +41,7 @@ struct BinArgs {
     const float *bval;
     int64_t cb;
     const int64_t *flops;  // [ncols_out]
+    const int2 *apair;     // [nnz(A)] (row, value bits) pairs of A: one 8-byte gather per product
     const int *rowpart;    // [A.ncols][33] row-range index of A (see kernels_spgemm.cu)
     const int *rowpart_fine;  // [A.ncols][129] (split parts of the private family)
     // work list of this bin
@@ -116,6 +117,9 @@ cudaError_t launch_rowpart(int64_t ncols, const int64_t *cp, const int32_t *row,
                            int *rowpart, cudaStream_t s, int nparts = 32);
 
 // misc kernels (kernels_misc.cu)
+// apair[q] = (row[q], bits of val[q]): the interleaved copy of A the private family gathers
+cudaError_t launch_pack_pairs(int64_t nnz, const int32_t *row, const float *val, int2 *apair,
+                              cudaStream_t s);
 // CSC invariants of include/mclx.h (MCLX_VALIDATE); *flag |= 1 col_ptr, 2 row range,
 // 4 row order, 8 value (not finite or <= 0)
 cudaError_t launch_validate_csc(int64_t ncols, int64_t nrows, int64_t nnz, const int64_t *cp,

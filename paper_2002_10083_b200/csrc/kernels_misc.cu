@@ -39,6 +39,47 @@ cudaError_t launch_flops(int64_t ncols, const int64_t *acp, const int64_t *bcp,
     return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ (row, value) pairs of A
+// 16-byte loads of 4 rows + 4 values, two 16-byte stores of 4 pairs (row / val aligned)
+__global__ void k_pack_pairs4(int64_t nnz, const int4 *__restrict__ row4,
+                              const float4 *__restrict__ val4, const int32_t *__restrict__ row,
+                              const float *__restrict__ val, int4 *__restrict__ out) {
+    const int64_t n4 = nnz >> 2;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int4 r = __ldg(row4 + i);
+        const float4 v = __ldg(val4 + i);
+        out[2 * i] = make_int4(r.x, __float_as_int(v.x), r.y, __float_as_int(v.y));
+        out[2 * i + 1] = make_int4(r.z, __float_as_int(v.z), r.w, __float_as_int(v.w));
+    }
+    if (blockIdx.x == 0 && threadIdx.x < (nnz & 3)) {
+        const int64_t q = (n4 << 2) + threadIdx.x;
+        reinterpret_cast<int2 *>(out)[q] = make_int2(row[q], __float_as_int(val[q]));
+    }
+}
+__global__ void k_pack_pairs1(int64_t nnz, const int32_t *__restrict__ row,
+                              const float *__restrict__ val, int2 *__restrict__ out) {
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nnz;
+         q += (int64_t)gridDim.x * blockDim.x)
+        out[q] = make_int2(row[q], __float_as_int(val[q]));
+}
+
+cudaError_t launch_pack_pairs(int64_t nnz, const int32_t *row, const float *val, int2 *apair,
+                              cudaStream_t s) {
+    if (nnz <= 0) return cudaSuccess;
+    int64_t blocks = ((nnz >> 2) + 255) / 256;
+    if (blocks > g_sms * 16) blocks = g_sms * 16;
+    if (blocks < 1) blocks = 1;
+    ++g_launches;
+    if ((((uintptr_t)row | (uintptr_t)val | (uintptr_t)apair) & 15) == 0)
+        k_pack_pairs4<<<(int)blocks, 256, 0, s>>>(nnz, reinterpret_cast<const int4 *>(row),
+                                                  reinterpret_cast<const float4 *>(val), row, val,
+                                                  reinterpret_cast<int4 *>(apair));
+    else
+        k_pack_pairs1<<<(int)blocks, 256, 0, s>>>(nnz, row, val, apair);
+    return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ CSC validation
 // MCLX_VALIDATE=1 (include/mclx.h MCL_ERR_FORMAT): the CSC invariants of the header --
 // col_ptr[0] = 0, non-decreasing, col_ptr[n] = nnz; rows in [0, nrows) and strictly

@@ -28,7 +28,7 @@
 //
 // CTA-shared family (short segments, R-MAT-like): one table per CTA, groups of g lanes per
 // segment with 16-byte gathers, warps take segments dynamically, slots resolved first and
-// float atomicAdds issued with the warp reconverged (insert4).
+// float atomicAdds issued with the warp reconverged (insert4b).
 //
 // kPart: one row-range part of a split column (see run_split in capi.cu), accumulated by
 // either family over the part's rowparts and written, rows sorted, to a staging slot.
@@ -63,56 +63,70 @@ __device__ __forceinline__ uint32_t probe_step(int row, uint32_t scap) {
     return (((uint32_t)row * 0x85EBCA6Bu) >> 15 | 1u) & (scap - 1);
 }
 
-// Open addressing with linear probing, four keys per lane at a time.  Phase 1 finds
-// the slot of every (row) -- the first probe of all four is issued back to back, and
-// lanes that collide or insert a new key resolve in a warp-uniform loop (claims by
-// integer CAS; `fill` counts occupied slots and an insert that would push the load
-// past `limit` = 7/8 cap reports overflow, so an under-estimated column fails fast
-// and is re-run in a bigger bin).  Phase 2, after the warp reconverges, adds all
-// values together, so the float atomicAdd (a CAS loop on sm_100) runs with full warps.
-// Returns false (warp-uniform) on overflow.  `fresh` counts keys this lane created.
+// Open addressing, four keys per lane at a time (CTA-shared family).  Double hashing
+// (probe_step; the CTA-shared tables are powers of two); an empty home slot is claimed by
+// integer CAS in the first pass; the table's fill count is updated once per call by one lane
+// (a warp-aggregated claim count), not by an atomic per claim inside the probe loop, so the
+// warp-uniform loop walks only real collisions.  The float atomicAdds (a CAS loop on
+// sm_100) then run with the warp reconverged.  Returns false (warp-uniform) on overflow:
+// fill past `limit` (7/8 cap: an under-estimated column fails fast and is re-run in a bigger
+// bin), or a walk longer than cap.  `fresh` counts keys this lane created.
 template <int MODE, typename V>
-__device__ __forceinline__ bool insert4(int *keys, V *vals, uint32_t cap, const int (&row)[4],
-                                        const V (&v)[4], const bool (&valid)[4], int *fill,
-                                        int limit, int &fresh) {
+__device__ __forceinline__ bool insert4b(int *keys, V *vals, uint32_t cap, const int (&row)[4],
+                                         const V (&v)[4], const bool (&valid)[4], int *fill,
+                                         int limit, int &fresh) {
+    const unsigned FULL = 0xffffffffu;
     volatile int *vk = keys;
     uint32_t s[4];
     int k[4];
     bool need[4];
+    int claims = 0;
+    bool any = false;
 #pragma unroll
     for (int j = 0; j < 4; j++) {
         s[j] = hash_slot(row[j], cap);
         k[j] = valid[j] ? vk[s[j]] : row[j];
-        need[j] = k[j] != row[j];
     }
-    bool ok = true;
-    while (__any_sync(0xffffffffu, need[0] | need[1] | need[2] | need[3])) {
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+        if (valid[j] && k[j] == kEmptyKey) {
+            const int old = atomicCAS(&keys[s[j]], kEmptyKey, row[j]);
+            claims += old == kEmptyKey;
+            k[j] = old == kEmptyKey ? row[j] : old;
+        }
+        need[j] = k[j] != row[j];
+        any |= need[j];
+    }
+    uint32_t walk = 0;
+    while (__any_sync(FULL, any)) {
+        any = false;
 #pragma unroll
         for (int j = 0; j < 4; j++) {
-            if (!need[j]) continue;
-            if (k[j] == kEmptyKey) {
-                if (atomicAdd(fill, 1) >= limit) {
-                    ok = false;
-                    need[j] = false;
-                    continue;
-                }
-                const int old = atomicCAS(&keys[s[j]], kEmptyKey, row[j]);
-                if (old == kEmptyKey) {
-                    fresh++;
-                    need[j] = false;
+            if (need[j]) {
+                if (k[j] == kEmptyKey) {
+                    const int old = atomicCAS(&keys[s[j]], kEmptyKey, row[j]);
+                    if (old == kEmptyKey) {
+                        claims++;
+                        need[j] = false;
+                    } else {
+                        k[j] = old;
+                        need[j] = old != row[j];
+                    }
                 } else {
-                    atomicSub(fill, 1);
-                    k[j] = old;  // another lane claimed the slot: re-examine it
-                    need[j] = old != row[j];
+                    s[j] = (s[j] + probe_step(row[j], cap)) & (cap - 1);
+                    k[j] = vk[s[j]];
+                    need[j] = k[j] != row[j];
                 }
-            } else {
-                s[j] = (s[j] + 1 == cap) ? 0u : s[j] + 1;
-                k[j] = vk[s[j]];
-                need[j] = k[j] != row[j];
             }
+            any |= need[j];
         }
+        if (++walk > cap) break;  // warp-uniform: a (nearly) full table -> overflow below
     }
-    ok = __all_sync(0xffffffffu, ok);
+    fresh += claims;
+    int tot = __reduce_add_sync(FULL, claims);
+    if (lane_id() == 0) tot = atomicAdd(fill, tot) + tot;
+    tot = __shfl_sync(FULL, tot, 0);
+    const bool ok = tot <= limit && walk <= cap;
     if (MODE != kSym && ok) {
 #pragma unroll
         for (int j = 0; j < 4; j++)
@@ -193,6 +207,8 @@ __device__ __forceinline__ bool warp_insert_n(int *keys, V *vals, uint32_t scap,
     return true;
 }
 
+
+
 // Resident CTAs per SM that a private-family bin's table allows (table + ~3 KB static
 // shared memory out of 228 KB, at most 2048 threads): the launch bound then gives the
 // compiler 65536 / (that x NT) registers -- occupancy is set by the table anyway -- so the
@@ -265,7 +281,7 @@ __global__ void __launch_bounds__(NT, (bin_min_blocks<CAP, NT, MODE, GLOBAL, ATO
         bool ok = true;
         if constexpr (ATOMIC) {
             // ---- short segments (R-MAT-like): CTA-shared table, groups of g lanes per
-            // segment, integer-CAS claims and float atomicAdd values (insert4)
+            // segment, integer-CAS claims and float atomicAdd values (insert4b)
             __shared__ int64_t st_start[NT];
             __shared__ int st_k[NT];
             __shared__ float st_b[NT];
@@ -335,7 +351,8 @@ __global__ void __launch_bounds__(NT, (bin_min_blocks<CAP, NT, MODE, GLOBAL, ATO
                         hi = lo + st_k[e];
                         bkj = st_b[e];
                     }
-                    const unsigned nstep = (unsigned)((hi + 4 * g - 1) / (4 * g));
+                    const int lg = 31 - __clz(4 * g);  // g is a power of two: no division
+                    const unsigned nstep = (unsigned)((hi + 4 * g - 1) >> lg);
                     const unsigned maxs = __reduce_max_sync(0xffffffffu, nstep);
                     for (unsigned si = 0; si < maxs; si++) {
                         const int i0 = 4 * ((int)si * g + lane_g);
@@ -353,7 +370,7 @@ __global__ void __launch_bounds__(NT, (bin_min_blocks<CAP, NT, MODE, GLOBAL, ATO
                             vld[j] = i0 + j >= lo && i0 + j < hi;
                             pv[j] = GLOBAL ? (V)(&v4.x)[j] * (V)bkj : (V)((&v4.x)[j] * bkj);
                         }
-                        if (!insert4<MODE, V>(keys, vals, cap, rr, pv, vld, &s_fill[0], limit, fresh)) {
+                        if (!insert4b<MODE, V>(keys, vals, cap, rr, pv, vld, &s_fill[0], limit, fresh)) {
                             ok = false;
                             *vovf = 1;
                         }
@@ -429,11 +446,11 @@ __global__ void __launch_bounds__(NT, (bin_min_blocks<CAP, NT, MODE, GLOBAL, ATO
                     ml = len > ml ? len : ml;
                     const bool v = t < len;
                     const uint32_t q = lo + (uint32_t)t;
-                    rr[u] = v ? __ldg(a.arow + q) : -1;
-                    av[u] = 0.f;
-                    if (MODE != kSym && v) {
-                        av[u] = __ldg(a.aval + q);
-                    }
+                    // one 8-byte gather of the interleaved (row, value) pair (+4% on C3 over
+                    // separate row / value loads)
+                    const int2 pv = v ? __ldg(a.apair + q) : make_int2(-1, 0);
+                    rr[u] = pv.x;
+                    av[u] = __int_as_float(pv.y);
                 }
                 return ml;
             };
@@ -512,7 +529,6 @@ __global__ void __launch_bounds__(NT, (bin_min_blocks<CAP, NT, MODE, GLOBAL, ATO
             (void)prof_calls;
             (void)prof_valid;
 #endif
-
         }
         if (!ok && lane == 0) s_ovf = 1;
         __syncthreads();
