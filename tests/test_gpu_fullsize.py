@@ -1,0 +1,192 @@
+"""Parity at the configs' stated sizes (VERDICT r1 "Next round" 1).
+
+Expected values come from the ORACLE ONLY: tests/golden/oracle_cache.json and the .npz files
+beside it were written by tools/oracle_cache.py (oracle/ + synth/, column shards over host
+cores, identical to a single-threaded run), and the sampled columns are recomputed here by
+the oracle (oracle/shard.py) on the box's host cores.  The GPU side goes through the C ABI.
+
+  P1  unpruned structure: per-column nnz(A_t A_t) of ALL columns via mcl_symbolic (digest of
+      the int64 array = the oracle's), flops per column (digest), and full row lists of
+      sampled columns via mcl_spgemm(A, A[:, sample]) -- bit-exact;
+  P2  unpruned values of the sampled columns, 1e-5 relative for v64 >= 1e-30;
+  P3  the fused mcl_iterate output on the sampled columns against the oracle's prune /
+      inflate of the same unpruned columns (kept sets up to the 1e-6 band, values 1e-5);
+  P4  full MCL on C3 (n = 500k): canonical labels identical to the oracle's.
+
+Inputs: C2 / C3 / C5 iteration 0 = the fp32 A_0 both sides build from synth; C3 iteration 1
+= the oracle's own fp64 A_1 cast to fp32 (its digest is checked against the cache); C4 =
+R-MAT scale 22 (n = 4,194,304), iteration 0.
+"""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import synth
+from oracle.shard import sharded_mcl_iterates, sharded_spgemm
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+if torch.cuda.is_available():
+    import paper_2002_10083_b200 as M
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+META = json.load(open(os.path.join(GOLD, "oracle_cache.json")))
+PARAMS = {c: (synth.CONFIGS[c]["theta"], synth.CONFIGS[c]["S"], synth.CONFIGS[c]["R"],
+              synth.CONFIGS[c]["pct"]) for c in synth.CONFIGS}
+# sampled columns: (random columns, heaviest-flops columns); C3 it1 and C4 columns are long
+# (1.8e4 / 1e5 unpruned entries on average), so their random samples are smaller
+SAMPLE = {("C2", 0): (20000, 100), ("C3", 0): (20000, 100), ("C3", 1): (5000, 100),
+          ("C5", 0): (20000, 100), ("C4", 0): (1000, 100)}
+
+
+def digest(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def f32(m):
+    return O.Mat(m.nrows, m.ncols, m.colptr, m.rows, m.vals.astype(np.float32).astype(np.float64))
+
+
+def iterate_input(cfg, it):
+    """A_t as both sides see it (fp32 values), checked against the oracle cache's digest."""
+    A = O.preprocess(synth.config_graph(cfg))
+    A = f32(sharded_mcl_iterates(A, PARAMS[cfg], it))
+    meta = META[f"nnz_{cfg}_it{it}"]
+    assert digest(A.rows) + ":" + digest(A.vals) == meta["input_sha256"], "input drifted"
+    return A
+
+
+def host_mat(g):
+    cp, rw, vl = g.to_host()
+    return O.Mat(g.nrows, g.ncols, cp.astype(np.int64), rw.astype(np.int32), vl.astype(np.float64))
+
+
+def col_flops(A):
+    deg = np.diff(A.colptr)
+    f = np.zeros(A.ncols, np.int64)
+    np.add.at(f, np.repeat(np.arange(A.ncols), deg), deg[A.rows])
+    return f
+
+
+def take_cols(A, cols):
+    cnt = np.diff(A.colptr)[cols]
+    cp = np.zeros(len(cols) + 1, np.int64)
+    np.cumsum(cnt, out=cp[1:])
+    idx = np.concatenate([np.arange(A.colptr[c], A.colptr[c + 1]) for c in cols])
+    return O.Mat(A.nrows, len(cols), cp, A.rows[idx], A.vals[idx])
+
+
+CASES = [("C2", 0), ("C3", 0), ("C3", 1), ("C5", 0), ("C4", 0)]
+
+
+def check_p1_all_columns(cfg, it, A):
+    """P1 over every column: nnz(C_*j) from the exact symbolic pass and flops_j equal the
+    oracle's arrays (sha256 of the int64 arrays), and the totals agree."""
+    meta = META[f"nnz_{cfg}_it{it}"]
+    Ad = M.CSC.from_host(A)
+    nnz, tot = M.symbolic(Ad)
+    fl, ftot = M.flops(Ad)
+    g = nnz.cpu().numpy().astype(np.int64)
+    assert ftot == meta["flops"] and digest(fl.cpu().numpy().astype(np.int64)) == meta["flops_sha256"]
+    assert tot == meta["nnz_unpruned"], (tot, meta["nnz_unpruned"])
+    if digest(g) != meta["nnz_sha256"]:
+        p = os.path.join(GOLD, f"nnz_{cfg}_it{it}.npz")
+        where = ""
+        if os.path.exists(p):
+            ref = np.load(p)["nnz"].astype(np.int64)
+            bad = np.nonzero(ref != g)[0]
+            where = f" first mismatching columns {bad[:10].tolist()}"
+        pytest.fail(f"per-column nnz differs from the oracle's{where}")
+
+
+def assert_unpruned(G, R, rtol=1e-5):
+    assert np.array_equal(G.colptr, R.colptr), "P1 col_ptr"
+    assert np.array_equal(G.rows, R.rows), "P1 row_idx"
+    big = R.vals >= 1e-30
+    rel = np.abs(G.vals[big] - R.vals[big]) / R.vals[big]
+    assert rel.size == 0 or rel.max() <= rtol, f"P2 max rel err {rel.max()}"
+    return float(rel.max()) if rel.size else 0.0
+
+
+def kept_parity_cols(Ag, cols, Cr, params, band=1e-6, rtol=1e-5):
+    """P3 for the fused output Ag (full GPU iterate) on `cols` against the oracle's prune /
+    inflate of the unpruned columns Cr (same order as cols)."""
+    theta, S, R, pct = params
+    Ao, info = O.prune_inflate(Cr, theta, S, R, pct, 2.0)
+    flips = excluded = 0
+    for i, j in enumerate(cols):
+        gr = Ag.rows[Ag.colptr[j]:Ag.colptr[j + 1]]
+        gv = Ag.vals[Ag.colptr[j]:Ag.colptr[j + 1]]
+        orow = Ao.rows[Ao.colptr[i]:Ao.colptr[i + 1]]
+        assert np.all(np.diff(gr) > 0)
+        if np.array_equal(gr, orow):
+            ov = Ao.vals[Ao.colptr[i]:Ao.colptr[i + 1]]
+            assert np.max(np.abs(gv - ov) / ov, initial=0.0) <= rtol, (j, "P3 values")
+            continue
+        cr = Cr.rows[Cr.colptr[i]:Cr.colptr[i + 1]]
+        cv = Cr.vals[Cr.colptr[i]:Cr.colptr[i + 1]]
+        diff = np.setxor1d(gr, orow)
+        vals = cv[np.searchsorted(cr, diff)]
+        assert np.all(np.abs(vals - info.tau[i]) <= band), (j, "P3 kept set outside the band")
+        flips += 1
+        excluded += len(diff)
+        w = cv[np.searchsorted(cr, gr)]
+        w = w / w.sum()
+        ref = w * w / (w * w).sum()
+        assert np.max(np.abs(gv - ref) / ref) <= rtol
+    return flips, excluded
+
+
+@pytest.mark.parametrize("cfg,it", CASES)
+def test_fullsize_parity(cfg, it):
+    """P1 on all columns (check_p1_all_columns), then P1 rows + P2 values of sampled
+    unpruned columns (mcl_spgemm on the gathered columns: the expansion kernels) and P3 of
+    the fused mcl_iterate output on the same columns."""
+    A = iterate_input(cfg, it)
+    check_p1_all_columns(cfg, it, A)
+    nrand, nheavy = SAMPLE[(cfg, it)]
+    rng = np.random.default_rng(1234 + it)
+    fl = col_flops(A)
+    cols = np.unique(np.concatenate([rng.choice(A.ncols, min(nrand, A.ncols), replace=False),
+                                     np.argsort(fl, kind="stable")[-nheavy:]]))
+    B = take_cols(A, cols)
+    Cr, flr = sharded_spgemm(A, B)
+    assert np.array_equal(flr, fl[cols])
+    Ad = M.CSC.from_host(A)
+    Cg, st = M.spgemm(Ad, M.CSC.from_host(B))
+    assert st["flops"] == int(fl[cols].sum())
+    assert_unpruned(host_mat(Cg), Cr)
+    del Cg
+    Ag, st = M.iterate(Ad, M.Params(prune_threshold=PARAMS[cfg][0], select_k=PARAMS[cfg][1],
+                                    recover_k=PARAMS[cfg][2], recover_pct=PARAMS[cfg][3]))
+    assert st["flops"] == int(fl.sum())
+    G = host_mat(Ag)
+    del Ag
+    flips, _ = kept_parity_cols(G, cols, Cr, PARAMS[cfg])
+    assert flips <= max(2, len(cols) // 1000)
+    # whole-matrix invariants of the fused output at full size
+    nz = np.diff(G.colptr) > 0
+    sums = np.add.reduceat(G.vals, np.minimum(G.colptr[:-1], max(G.vals.size - 1, 0)))[nz]
+    np.testing.assert_allclose(sums, 1.0, atol=1e-5)
+    assert np.diff(G.colptr).max() <= max(PARAMS[cfg][1], PARAMS[cfg][2])
+
+
+def test_p4_c3_full_mcl_clusters():
+    """P4: full MCL on C3 (n = 500,000) to convergence on the GPU gives the oracle's clusters
+    (canonical labels, tests/golden/c3_mcl.npz), iteration counts within one."""
+    meta = META["c3_mcl"]
+    ref = np.load(os.path.join(GOLD, "c3_mcl.npz"))["labels"]
+    assert digest(ref) == meta["labels_sha256"]
+    theta, S, R, pct = PARAMS["C3"]
+    labels, k, hist, _ = M.run(M.CSC.from_host(synth.config_graph("C3")),
+                               M.Params(prune_threshold=theta, select_k=S, recover_k=R,
+                                        recover_pct=pct))
+    lab = labels.cpu().numpy()
+    assert k == meta["nclusters"], (k, meta["nclusters"])
+    assert np.array_equal(lab, ref), f"{int((lab != ref).sum())} vertices labelled differently"
+    assert abs(len(hist) - meta["iterations"]) <= 1

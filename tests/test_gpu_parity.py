@@ -417,83 +417,3 @@ def test_full_mcl_clusters_equal_small_c3_c4_shapes(shape):
     assert k == ref.nclusters
     assert np.array_equal(labels.cpu().numpy(), ref.labels)
     assert abs(len(hist) - ref.iterations) <= 1
-
-
-# ---------------------------------------------------------------- C3 at full size, sampled
-def _sampled_parity(A32, Ag, params, n_random=200, n_heavy=20, seed=0):
-    """Compare sampled columns of the GPU iterate with the oracle, column by column
-    (O.expand on one column, then O.prune_inflate), plus whole-matrix invariants."""
-    theta, S, R, pct = params
-    G_ = host_mat(Ag)
-    rng = np.random.default_rng(seed)
-    fl_all, _ = M.flops(dev(A32))
-    heavy = np.argsort(fl_all.cpu().numpy())[-n_heavy:]
-    cols = np.unique(np.concatenate([rng.choice(A32.ncols, n_random, replace=False), heavy]))
-    for j in cols:
-        Cj, _ = O.expand(A32, int(j), int(j) + 1)
-        _, info = O.prune_inflate(Cj, theta, S, R, pct, 2.0)
-        sub = O.Mat(G_.nrows, 1, np.array([0, G_.colptr[j + 1] - G_.colptr[j]], np.int64),
-                    G_.rows[G_.colptr[j]:G_.colptr[j + 1]], G_.vals[G_.colptr[j]:G_.colptr[j + 1]])
-        kept_parity(sub, Cj, info, params)
-    nz = np.diff(G_.colptr) > 0
-    sums = np.add.reduceat(G_.vals.astype(np.float64), G_.colptr[:-1])[nz]
-    np.testing.assert_allclose(sums, 1.0, atol=1e-5)
-    assert np.diff(G_.colptr).max() <= max(S, R)
-
-
-@pytest.mark.slow
-def test_c4_scale20_sampled_columns():
-    """R-MAT scale 20 (C4 shape at 1/4 size): half the columns exceed one CTA's table and
-    run as split row-range parts (hashed and dense row tiles) -- sampled columns vs the
-    oracle, at the size and launch configuration `bench.py --config C4 --scale 0.25` times."""
-    A32 = f32(O.preprocess(synth.config_graph("C4", 0.25)))
-    params = (1e-4, 1100, 1400, 0.9)
-    Ag, st = M.iterate(dev(A32), M.Params())
-    assert st["split_cols"] > 0 and st["split_vcols"][2] > 0  # dense tiles exercised
-    _sampled_parity(A32, Ag, params, n_random=100, n_heavy=10)
-
-
-@pytest.mark.slow
-def test_c5_full_size_sampled_columns():
-    A32 = f32(O.preprocess(synth.config_graph("C5")))
-    Ag, st = M.iterate(dev(A32), M.Params())
-    _sampled_parity(A32, Ag, (1e-4, 1100, 1400, 0.9))
-
-
-@pytest.mark.slow
-def test_c3_iteration1_sampled_columns():
-    """C3's heaviest iteration (it1, ~1e11 flops): the input A_1 is the oracle's own
-    iterate (fp64 expand + prune/inflate of A_0, cast to fp32), so the GPU and the oracle
-    square the same matrix; 2/3 of its columns run through the split path."""
-    A0 = O.preprocess(synth.config_graph("C3"))
-    C0, _ = O.expand(A0)
-    A1, _ = O.prune_inflate(C0, 1e-4, 1100, 1400, 0.9, 2.0)
-    del C0
-    A32 = f32(A1)
-    Ag, st = M.iterate(dev(A32), M.Params())
-    assert st["split_cols"] > 0
-    _sampled_parity(A32, Ag, (1e-4, 1100, 1400, 0.9))
-
-
-@pytest.mark.slow
-def test_c3_full_size_sampled_columns():
-    G = synth.config_graph("C3")
-    A = O.preprocess(G)
-    A32 = f32(A)
-    Ad = dev(A32)
-    Ag, st = M.iterate(Ad, M.Params())
-    G_ = host_mat(Ag)
-    rng = np.random.default_rng(0)
-    fl_all, _ = M.flops(Ad)
-    heavy = np.argsort(fl_all.cpu().numpy())[-20:]
-    cols = np.unique(np.concatenate([rng.choice(A.ncols, 200, replace=False), heavy]))
-    for j in cols:
-        Cj, _ = O.expand(A32, int(j), int(j) + 1)
-        _, info = O.prune_inflate(Cj, 1e-4, 1100, 1400, 0.9, 2.0)
-        sub = O.Mat(G_.nrows, 1, np.array([0, G_.colptr[j + 1] - G_.colptr[j]], np.int64),
-                    G_.rows[G_.colptr[j]:G_.colptr[j + 1]], G_.vals[G_.colptr[j]:G_.colptr[j + 1]])
-        kept_parity(sub, Cj, info, (1e-4, 1100, 1400, 0.9))
-    # whole-matrix invariants at full size: columns sum to 1, |kept| <= max(S,R)
-    sums = np.add.reduceat(G_.vals.astype(np.float64), G_.colptr[:-1])
-    np.testing.assert_allclose(sums, 1.0, atol=1e-5)
-    assert np.diff(G_.colptr).max() <= 1400

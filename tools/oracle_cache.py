@@ -20,7 +20,6 @@ from __future__ import annotations
 
 import hashlib
 import json
-import multiprocessing as mp
 import os
 import sys
 import time
@@ -32,92 +31,15 @@ sys.path.insert(0, ROOT)
 
 import oracle as O  # noqa: E402
 import synth  # noqa: E402
+from oracle.shard import sharded_nnz, sharded_step  # noqa: E402
 
 GOLD = os.path.join(ROOT, "tests", "golden")
 PARAMS = {c: (synth.CONFIGS[c]["theta"], synth.CONFIGS[c]["S"], synth.CONFIGS[c]["R"],
               synth.CONFIGS[c]["pct"]) for c in synth.CONFIGS}
 
-_A = None       # the iterate the workers read (inherited through fork, never written)
-_PRM = None
-
 
 def log(*a):
     print(time.strftime("%H:%M:%S"), *a, file=sys.stderr, flush=True)
-
-
-def _ranges(n: int, flops: np.ndarray, pieces: int):
-    """Column ranges of near-equal oracle work (flops + nnz proxy)."""
-    w = flops.astype(np.float64) + 1.0
-    cum = np.cumsum(w)
-    cuts = np.searchsorted(cum, np.linspace(0, cum[-1], pieces + 1)[1:-1])
-    b = np.unique(np.concatenate([[0], cuts, [n]]))
-    return [(int(b[i]), int(b[i + 1])) for i in range(len(b) - 1) if b[i + 1] > b[i]]
-
-
-def _flops(A) -> np.ndarray:
-    """flops_j = sum_{k in A_*j} nnz(A_*k): integer counting, no method arithmetic
-    beyond the definition (used only to balance the shards)."""
-    deg = np.diff(A.colptr)
-    return np.add.reduceat(np.concatenate([deg[A.rows].astype(np.int64), [0]]),
-                           np.minimum(A.colptr[:-1], A.rows.size)) * (deg > 0)
-
-
-def _w_step(rng):
-    b, e = rng
-    C, fl = O.expand(_A, b, e)
-    An, info = O.prune_inflate(C, *_PRM, 2.0)
-    return b, np.diff(An.colptr), An.rows, An.vals, float(info.chaos.max()) if info.chaos.size else 0.0
-
-
-def _w_nnz(rng):
-    b, e = rng
-    out = []
-    fl = []
-    step = max(1, min(e - b, 4096))
-    for s in range(b, e, step):
-        C, f = O.expand(_A, s, min(e, s + step))
-        out.append(np.diff(C.colptr))
-        fl.append(f)
-        del C
-    return b, np.concatenate(out), np.concatenate(fl)
-
-
-def _pool(nproc):
-    return mp.get_context("fork").Pool(nproc)
-
-
-def sharded_step(A, prm, nproc):
-    """One MCL iteration (expand + prune/inflate) of the oracle, sharded by columns."""
-    global _A, _PRM
-    _A, _PRM = A, prm
-    rng = _ranges(A.ncols, _flops(A), nproc * 24)
-    parts = {}
-    with _pool(nproc) as p:
-        for b, cnt, rows, vals, ch in p.imap_unordered(_w_step, rng):
-            parts[b] = (cnt, rows, vals, ch)
-    keys = sorted(parts)
-    cnt = np.concatenate([parts[k][0] for k in keys])
-    cp = np.zeros(A.ncols + 1, np.int64)
-    np.cumsum(cnt, out=cp[1:])
-    rows = np.concatenate([parts[k][1] for k in keys])
-    vals = np.concatenate([parts[k][2] for k in keys])
-    chaos = max(parts[k][3] for k in keys) if keys else 0.0
-    _A = None
-    return O.Mat(A.nrows, A.ncols, cp, rows, vals), chaos
-
-
-def sharded_nnz(A, nproc):
-    global _A
-    _A = A
-    rng = _ranges(A.ncols, _flops(A), nproc * 32)
-    parts = {}
-    with _pool(nproc) as p:
-        for b, cnt, fl in p.imap_unordered(_w_nnz, rng):
-            parts[b] = (cnt, fl)
-    keys = sorted(parts)
-    _A = None
-    return (np.concatenate([parts[k][0] for k in keys]).astype(np.int64),
-            np.concatenate([parts[k][1] for k in keys]).astype(np.int64))
 
 
 def digest(a: np.ndarray) -> str:
