@@ -59,6 +59,7 @@ struct mcl_ctx {
     int64_t cap_budget = (int64_t)16 << 30;   // unfused products: upper-bound slots up to this
     bool split_private = true;                // MCLX_SPLIT_PRIVATE=0: P <= 4 parts shared-table too
     bool validate = false;                    // MCLX_VALIDATE=1: check input CSC invariants
+    bool split_cand = true;                   // MCLX_SPLIT_CAND=0: split parts stage every entry
     int family = -1;                          // MCLX_FAMILY=0/1 forces a kernel family (A/B runs)
 };
 
@@ -299,8 +300,9 @@ int run_split(mcl_ctx *c, const Prod &pr, int nsplit, int32_t *split_list,
     CK(cudaStreamSynchronize(c->stream));
     // variant by the virtual part count P (parts sized for T = split_part_need distinct
     // rows): <= 32 parts of kPartCap slots; 64: 32 parts of 2 kPartCap slots; more
-    // (outputs dense in a sizable share of the rows, or long fp64 sums): 32 dense fp64
-    // row tiles (kernels_dense.cu), staging capacity min(part rows, 2 P T / 32 + 256)
+    // (outputs dense in a sizable share of the rows, or long fp64 sums): kDenseParts row
+    // ranges swept by dense fp32 / fp64 tiles (kernels_dense.cu), staging capacity
+    // min(part rows, 2 P T / kDenseParts + 256)
     // variants: 4 (P <= 16: private row-range slices, 8 warps over the part's >= 8 rowparts
     // of the 128-way index), 0 (P = 32, or MCLX_SPLIT_PRIVATE=0: CTA-shared tables), 1, 2, 3
     // (the private family addresses A with 32-bit offsets; its 128-way row index costs a
@@ -323,21 +325,29 @@ int run_split(mcl_ctx *c, const Prod &pr, int nsplit, int32_t *split_list,
         std::stable_partition(hl.begin(), hl.end(),
                               [&](int32_t col) { return variant_of(hP[col]) == vorder[o]; });
     const int64_t cap_of[2] = {kPartCap, 2 * kPartCap};
+    // candidates: each part stages only its top max(S, R) entries plus the statistics of all
+    // of them (exact: the column's kept set lies in the union of its parts' top-max(S, R)
+    // for every branch of Alg. 1 l.4, readings Q5-Q8), so the stitched columns k_prune reads
+    // are short; MCLX_SPLIT_CAND=0 stages every entry instead
+    const int cand_k = (c->split_cand && a.pp.kmax <= kCandMax) ? a.pp.kmax : 0;
     std::vector<int64_t> hoff((size_t)nsplit + 1, 0);   // first item of each column
     std::vector<int64_t> hstg;                          // staging offset of each item
     hstg.reserve((size_t)nsplit * 4 + 1);
     int64_t stg = 0;
     for (int s2 = 0; s2 < nsplit; s2++) {
         const int v = variant_of(hP[hl[s2]]), P = hP[hl[s2]] & ~(kSplitFp64 | kSplitShared);
-        const int parts = P < 32 ? P : 32;
+        const int parts = split_parts(hP[hl[s2]]);
         hoff[s2 + 1] = hoff[s2] + parts;
-        const int64_t prow = (pr.A->nrows + kParts - 1) / kParts + 1;
-        const int64_t dcap = std::min<int64_t>(prow, (int64_t)P * c->split_part_need / 16 + 256);
+        // a dense part's slot: its rows, or twice its share of the column's size bound
+        const int64_t prow = (pr.A->nrows + kDenseParts - 1) / kDenseParts + 1;
+        const int64_t dcap =
+            std::min<int64_t>(prow, (int64_t)P * c->split_part_need * 2 / kDenseParts + 256);
         for (int q = 0; q < parts; q++) {
             hstg.push_back(stg);
             // the 7/8 fill limit bounds a hashed part's entries
             const int64_t tc = v == 1 ? cap_of[1] : cap_of[0];
-            stg += (v == 2 || v == 3) ? dcap : tc - tc / 8;
+            const int64_t slot = (v == 2 || v == 3) ? dcap : tc - tc / 8;
+            stg += cand_k > 0 ? std::min<int64_t>(slot, cand_k) : slot;
         }
     }
     hstg.push_back(stg);
@@ -380,6 +390,16 @@ int run_split(mcl_ctx *c, const Prod &pr, int nsplit, int32_t *split_list,
     RC(scratch_t(c, "split_cval", (size_t)chunk_stg, &cval));
     RC(scratch_t(c, "split_ccp", (size_t)nsplit + 1, &ccp));
     RC(scratch_t(c, "split_colmap", (size_t)nsplit, &colmap));
+    int64_t *stg_nnz = nullptr, *stg_m = nullptr, *fnnz = nullptr, *fm = nullptr;
+    double *stg_s = nullptr, *fs = nullptr;
+    if (cand_k > 0) {
+        RC(scratch_t(c, "split_stg_nnz", (size_t)chunk_items, &stg_nnz));
+        RC(scratch_t(c, "split_stg_m", (size_t)chunk_items, &stg_m));
+        RC(scratch_t(c, "split_stg_s", (size_t)chunk_items, &stg_s));
+        RC(scratch_t(c, "split_fnnz", (size_t)nsplit, &fnnz));
+        RC(scratch_t(c, "split_fm", (size_t)nsplit, &fm));
+        RC(scratch_t(c, "split_fs", (size_t)nsplit, &fs));
+    }
     RC(scratch(c, "split_scan_tmp", scan_tmp_bytes(chunk_items + 1), &tmp));
     std::vector<int> hcnt((size_t)2 * nchunks, 0);
     for (int q = 0; q < nchunks; q++) hcnt[q] = (int)(hoff[cuts[q + 1]] - hoff[cuts[q]]);
@@ -437,16 +457,20 @@ int run_split(mcl_ctx *c, const Prod &pr, int nsplit, int32_t *split_list,
         ap.stg_row = stg_row - hstg[item0];
         ap.stg_val = stg_val - hstg[item0];
         ap.stg_cnt = stg_cnt;
+        ap.cand_k = cand_k;
+        ap.stg_nnz = stg_nnz;
+        ap.stg_m = stg_m;
+        ap.stg_s = stg_s;
         const int grid = (int)std::min<int64_t>(nit, (int64_t)occ[v] * c->sms);
         if (v == 2 || v == 3) CK(launch_dense_part(v == 3, ap, grid, c->stream));
         else CK(launch_part(v, ap, grid, c->stream));
         CK(launch_scan_i64(stg_cnt, sioff, nit, tmp, c->stream));
         CK(launch_split_stitch(nc, ioff + s0, item0, item_col + item0, sioff, a.col_flag, ccp, colmap,
-                               c->stream));
+                               stg_nnz, stg_m, stg_s, fnnz, fm, fs, c->stream));
         CK(launch_split_gather(nit, stg_cnt, stg_off + item0, stg_row - hstg[item0],
                                stg_val - hstg[item0], sioff, crow, cval, c->stream));
         CK(launch_prune(nc, ccp, crow, cval, a.soff, a.s_row, a.s_val, a.s_cnt, a.chaos,
-                        a.chaos_max, a.pp, pgrid, c->stream, colmap, out_count));
+                        a.chaos_max, a.pp, pgrid, c->stream, colmap, out_count, fnnz, fm, fs));
     }
     return MCL_OK;
 }
@@ -498,7 +522,9 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
 
 
     // split columns (kFused only): big columns as row-range parts, see run_split
-    const bool use_split = c->split && mode == kFused && pr.A->ncols > 0;
+    // (the row-range parts address A with 32-bit positions)
+    const bool use_split = c->split && mode == kFused && pr.A->ncols > 0 &&
+                           pr.A->nnz < ((int64_t)1 << 32);
     int32_t *split_list = nullptr, *split_P = nullptr;
     int *split_count = nullptr, *col_flag = nullptr;
     if (use_split) {
@@ -1137,6 +1163,7 @@ int mcl_ctx_create(mcl_ctx_t *out, int device, void *stream, mcl_alloc_fn alloc,
     if (const char *e = getenv("MCLX_GBIN_BUDGET_MB")) c->gbin_budget = (int64_t)atoll(e) << 20;
     if (const char *e = getenv("MCLX_VALIDATE")) c->validate = atoi(e) != 0;
     if (const char *e = getenv("MCLX_FAMILY")) c->family = atoi(e);
+    if (const char *e = getenv("MCLX_SPLIT_CAND")) c->split_cand = atoi(e) != 0;
     if (cudaMallocHost(&c->pin, kPinBytes) != cudaSuccess) {
         delete c;
         return MCL_ERR_CUDA;

@@ -77,20 +77,40 @@ struct BinArgs {
     float *stg_val;
     int64_t *stg_cnt;
     int *col_flag;                                      // [ncols_out] overflowed split columns
+    // kPart with cand_k > 0: a part stages only its top-cand_k entries (value desc, row asc;
+    // cand_k = max(S, R), so the column's kept set is among them for every branch of
+    // Alg. 1 l.4) and reports the statistics of ALL its entries for the branch decision
+    int cand_k;
+    int64_t *stg_nnz;  // [items] entries of the part
+    int64_t *stg_m;    // [items] entries >= theta
+    double *stg_s;     // [items] their mass (fp64)
 };
+// largest cand_k the dense sweep's candidate buffer holds (kCandBuf - 1024 free slots per
+// tile chunk of 1024 entries)
+constexpr int kCandBuf = 2560;
+constexpr int kCandMax = kCandBuf - 1024;
 // the shared-table bin that runs the parts of split columns (table slots, threads)
 constexpr int kPartCap = 8192;
 constexpr int kPartThreads = 512;
 constexpr int kPartNeed = kPartCap / 2;  // distinct rows a part is sized for (load 1/2)
 constexpr int kParts = 32;  // row ranges of the rowpart index (k_rowpart)
 constexpr int kFineParts = 128;  // the finer index used by private-slice split parts
-// dense bin (kernels_dense.cu): 32 row-tile parts per column, fp64 tiles in shared memory
+// dense bin (kernels_dense.cu): kDenseParts row-range parts per column, each swept tile by
+// tile with per-segment cursors (tile + kSweepSeg descriptors in shared memory)
 constexpr int kDenseThreads = 1024;
-constexpr int kDenseTileBytes = 196608;  // a dense part's tile per pass (192 KB)
+constexpr int kDenseParts = 8;             // parts of a dense column (32 / 8 = 4 rowparts each)
+constexpr int kSweepTileBytes = 163840;    // dense tile: 40960 fp32 / 20480 fp64 rows
+constexpr int kSweepSeg = 3072;            // segment descriptors (cursor, end, b) per chunk
 // split_P flag: the column needs fp64 accumulation (more than kFp64Terms segments)
 constexpr int kSplitFp64 = 1 << 30;
 // split_P flag: short sub-segments, run the parts in the CTA-shared-table family
 constexpr int kSplitShared = 1 << 29;
+// work items (row-range parts) of a split column from its split_P entry: the dense variants
+// (more than 64 virtual parts, or fp64) sweep kDenseParts ranges, hashed parts min(P, 32)
+__host__ __device__ inline int split_parts(int Pf) {
+    const int P = Pf & ~(kSplitFp64 | kSplitShared);
+    return ((Pf & kSplitFp64) || P > 64) ? kDenseParts : (P < 32 ? P : 32);
+}
 cudaError_t launch_dense_part(bool fp64, const BinArgs &a, int grid, cudaStream_t s);
 int dense_part_occupancy(bool fp64);
 // part variants: 0 kPartCap-slot shared table, 1 2*kPartCap-slot shared table
@@ -168,9 +188,12 @@ cudaError_t launch_split_items(int nsplit, const int32_t *split_list, const int3
 // stitch the parts of split columns [s0, s0 + nc) (items from ioff[s0]) into an unpruned
 // CSC: ccp from the scanned part counts sioff; colmap = product column, or -1 when a part
 // overflowed (the column is re-run in a later round)
+// with stg_nnz (candidates) also the column sums of the parts' statistics -> fnnz, fm, fs
 cudaError_t launch_split_stitch(int nc, const int64_t *ioff, int64_t item0, const int32_t *item_col,
                                 const int64_t *sioff, const int *col_flag, int64_t *ccp,
-                                int32_t *colmap, cudaStream_t s);
+                                int32_t *colmap, const int64_t *stg_nnz, const int64_t *stg_m,
+                                const double *stg_s, int64_t *fnnz, int64_t *fm, double *fs,
+                                cudaStream_t s);
 cudaError_t launch_split_gather(int64_t nitems, const int64_t *stg_cnt, const int64_t *stg_off,
                                 const int32_t *stg_row, const float *stg_val, const int64_t *sioff,
                                 int32_t *crow, float *cval, cudaStream_t s);
@@ -201,7 +224,8 @@ cudaError_t launch_prune(int64_t ncols, const int64_t *ccp, const int32_t *crow,
                          const int64_t *soff, int32_t *srow, float *sval, int64_t *scnt,
                          float *chaos, float *chaos_max, const PruneParams &pp, int grid,
                          cudaStream_t s, const int32_t *colmap = nullptr,
-                         unsigned long long *out_count = nullptr);
+                         unsigned long long *out_count = nullptr, const int64_t *fnnz = nullptr,
+                         const int64_t *fm = nullptr, const double *fs = nullptr);
 cudaError_t launch_cohen_keys(int64_t m, int64_t row0, int r, uint64_t seed, float *X,
                               float *keys_out, cudaStream_t s);
 cudaError_t launch_cohen_min(int64_t ncols, const int64_t *cp, const int32_t *row, int64_t c0,

@@ -1,25 +1,32 @@
 // kernels_dense.cu -- the dense bin of the expansion step (SURVEY §8(a) a4 "dense": the
 // R-MAT hub columns of C4, whose product covers a sizable share of the row space).
 //
-// Such a column is run as 32 row-range parts (rowparts of A, as the split path), each a
-// (column, row tile) work item of one CTA: rows [ceil(p0 m/32), ceil(p1 m/32)) accumulate
-// into a dense tile in shared memory (kDenseTileBytes: 24576 fp64 or 49152 fp32 rows per
-// pass; wider parts sweep several passes, re-reading their sub-segments and skipping
-// rows outside the pass).  No hashing: the slot is the row.  A touched row is one with a
-// value > 0 -- fp64 products of positive fp32 values never underflow; an fp32 product
-// that underflows to 0 marks its row with -0.0 instead (Q13: the entry stays in the
-// structure) -- so compacting a tile emits its rows in ascending order, no sort.  Values
-// are added with shared-memory atomics (groups of lanes share a segment; a CAS loop on
-// sm_100).  fp64 tiles for columns with more than kFp64Terms segments (T), fp32 otherwise
-// (as the hashed bins).  Entries go to the item's
-// staging slot, which the split path stitches and prunes (k_prune); more entries than
-// the slot holds flag the column for the next round.
+// Such a column runs as kDenseParts row-range parts (part p = rowparts [p 32/D, (p+1) 32/D)
+// of A's 32-way row index), each a work item of one CTA that SWEEPS its row range tile by
+// tile: a tile of kSweepTileBytes (40960 fp32 / 20480 fp64 rows) is a dense accumulator in
+// shared memory -- no hashing, the slot is the row -- and every segment A_*k of the column
+// keeps a cursor (its next position, in shared memory beside the tile) that advances as the
+// tiles pass, so each product is gathered exactly once and each segment descriptor is read
+// once per part ("per-k cursors kept ... when one CTA sweeps the tiles in
+// order").  Columns with more than kSweepSeg segments take them in chunks whose cursors are
+// re-found by binary search at every tile.  A touched row is one with a value > 0 -- fp64
+// products of positive fp32 values never underflow; an fp32 product that underflows to 0
+// marks its row with -0.0 instead (Q13: the entry stays in the structure) -- so compacting
+// a tile emits its rows in ascending order, no sort.  Values are added with shared-memory
+// atomics (lanes of a group walk one segment; other groups may hit the same row).  fp64
+// tiles for columns with more than kFp64Terms segments (T), fp32 otherwise.  Entries go to
+// the item's staging slot, which the split path stitches and prunes (k_prune); more entries
+// than the slot holds flag the column for the next round.  With candidates (cand_k =
+// max(S, R) > 0) a part stages only its top-cand_k entries, kept by a streaming selection in
+// a shared-memory buffer (append what beats the buffer's cut, radix-select back to cand_k
+// when it fills), plus the count / mass statistics of all its entries (see run_split).
 //
-// Tried and dropped (kept here as a note): one L2-resident fp64 array of m rows per
-// column, products added by RED.ADD.F64 from CTAs splitting the column by segments
-// (~210 G atomics/s into L2-resident arrays, tools/ubench_red.cu).  The L2 budget admits
-// only a few columns in flight, and each column's compaction + prune then runs in one
-// CTA on the critical path: 10x slower than the tiles on R-MAT scale 20.
+// History: the first dense kernel gave every (column, 1/32 row range) part several passes
+// over a 192 KB tile, re-reading each sub-segment's prefix and all segment descriptors at
+// every pass: 112 s of C4's (R-MAT scale 22) 130 s iteration.  An L2-resident variant (one
+// fp64 array of m rows per column, RED.ADD.F64) was 10x slower than tiles at scale 20.
+#include <climits>
+
 #include "kernels.h"
 
 namespace mclx {
@@ -38,21 +45,40 @@ __device__ __forceinline__ void atomic_mark_zero(float *p) {
 __device__ __forceinline__ void atomic_mark_zero(double *) {}  // fp64 products never underflow
 
 __device__ __forceinline__ int dense_group_size(int64_t avg) {
-    return avg >= 24 ? 32 : avg >= 12 ? 16 : avg >= 6 ? 8 : avg >= 3 ? 4 : avg >= 2 ? 2 : 1;
+    return avg >= 48 ? 32 : avg >= 24 ? 16 : avg >= 12 ? 8 : avg >= 6 ? 4 : avg >= 3 ? 2 : 1;
+}
+
+// first position q in [lo, hi) of A with row >= r (rows of a segment ascend)
+__device__ __forceinline__ uint32_t lower_row(const int2 *__restrict__ ap, uint32_t lo, uint32_t hi,
+                                              int64_t r) {
+    while (lo < hi) {
+        const uint32_t mid = lo + ((hi - lo) >> 1);
+        if ((int64_t)__ldg(&ap[mid].x) < r) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
 }
 
 template <typename V>
-__global__ void __launch_bounds__(kDenseThreads, 1) k_dense_part(BinArgs a) {
+__global__ void __launch_bounds__(kDenseThreads, 1) k_dense_sweep(BinArgs a) {
     constexpr int NT = kDenseThreads;
-    constexpr int TILE = kDenseTileBytes / (int)sizeof(V);
+    constexpr int TILE = kSweepTileBytes / (int)sizeof(V);
     extern __shared__ __align__(16) unsigned char dsm[];
     V *acc = reinterpret_cast<V *>(dsm);
-    __shared__ int64_t st_start[NT];
-    __shared__ int st_k[NT];
-    __shared__ float st_b[NT];
+    uint32_t *cur = reinterpret_cast<uint32_t *>(dsm + kSweepTileBytes);  // segment cursors
+    uint32_t *end = cur + kSweepSeg;                                        // segment ends
+    float *bkj = reinterpret_cast<float *>(end + kSweepSeg);               // b_kj
+    int *crow = reinterpret_cast<int *>(bkj + kSweepSeg);                   // candidates (rows)
+    float *cval = reinterpret_cast<float *>(crow + kCandBuf);              // candidates (values)
     __shared__ int sscan[NT / 32];
-    __shared__ int s_col, s_idx, s_pr, s_next;
-    const int tid = threadIdx.x;
+    __shared__ double sred[NT / 32];
+    __shared__ unsigned hist[256];
+    __shared__ int sint[4];
+    __shared__ int s_col, s_idx, s_pr, s_next, s_ncand, s_reduced;
+    __shared__ uint32_t s_thr;
+    const bool cand = a.cand_k > 0;
+    const double theta = a.pp.theta;
+    const int tid = threadIdx.x, lane = tid & 31;
     const int count = *a.count;
     for (;;) {
         if (tid == 0) {
@@ -60,7 +86,9 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_dense_part(BinArgs a) {
             s_idx = idx;
             s_col = idx < count ? a.list[idx] : -1;
             s_pr = idx < count ? a.item_pr[idx] : 0;
-            s_next = 0;
+            s_ncand = 0;
+            s_reduced = 0;
+            s_thr = 0u;
         }
         __syncthreads();
         const int col = s_col, idx = s_idx, pr = s_pr;
@@ -72,67 +100,160 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_dense_part(BinArgs a) {
         const int64_t q0 = a.bcp[bj], q1 = a.bcp[bj + 1];
         const int64_t nb = q1 - q0;
         const int64_t dst0 = a.stg_off[idx], cap = a.stg_off[idx + 1] - dst0;
+        const int64_t ntiles = (r_hi - r_lo + TILE - 1) / TILE;
+        // lanes per segment from the expected products of one segment in one tile
         const int64_t fpart = a.flops[col] * (p1 - p0) / kParts;
-        const int g = dense_group_size(nb > 0 ? fpart / nb : 0);
-        const int lane_g = tid & (g - 1);
+        const int g = dense_group_size(nb > 0 && ntiles > 0 ? fpart / (nb * ntiles) : 0);
+        const int lane_g = lane & (g - 1);
+        const bool chunked = nb > kSweepSeg;
         int64_t written = 0;
+        int nloc = 0, mloc = 0;  // candidates: statistics of all the part's entries
+        double sloc = 0.0;
+        // keep the top cand_k of the candidate buffer (value desc, row asc; order-preserving,
+        // so the buffer stays sorted by row); later entries must beat its cut strictly
+        auto reduce_cands = [&]() {
+            uint32_t t = 0;
+            int rowcut = 0;
+            const int nc = s_ncand;
+            radix_select_topk<NT, float>(crow, cval, nc, a.cand_k, t, rowcut, hist, sint);
+            const int kept = compact_inplace<NT, float>(
+                crow, cval, nc,
+                [=](int k, float v) {
+                    const uint32_t b = val_bits(v);
+                    return b > t || (b == t && k <= rowcut);
+                },
+                sscan);
+            if (tid == 0) {
+                s_ncand = kept;
+                s_thr = t;
+                s_reduced = 1;
+            }
+            __syncthreads();
+        };
         for (int64_t t0 = r_lo; t0 < r_hi; t0 += TILE) {
             const int tw = (int)((r_hi - t0) < TILE ? (r_hi - t0) : TILE);
+            const int64_t t_end = t0 + tw;
             for (int i = tid; i < tw; i += NT) acc[i] = V(0);
-            __syncthreads();
-            for (int64_t c0 = q0; c0 < q1; c0 += NT) {
-                const int cnt = (int)((q1 - c0) < NT ? (q1 - c0) : NT);
-                if (tid < cnt) {
-                    const int k = __ldg(a.brow + c0 + tid);
-                    const int *pk = a.rowpart + (int64_t)k * (kParts + 1);
-                    const int e0 = __ldg(pk + p0), e1 = __ldg(pk + p1);
-                    st_start[tid] = __ldg(a.acp + k) + e0;
-                    st_k[tid] = e1 - e0;
-                    st_b[tid] = __ldg(a.bval + c0 + tid);
-                }
-                __syncthreads();
-                // segments handed to warps dynamically (32/g at a time), so warps that drew
-                // short segments take more instead of idling at the batch barrier; the row
-                // and value of an entry are loaded together (one round trip, not two)
-                for (;;) {
-                    int e0 = 0;
-                    if ((tid & 31) == 0) e0 = atomicAdd(&s_next, 32 / g);
-                    e0 = __shfl_sync(0xffffffffu, e0, 0);
-                    if (e0 >= cnt) break;
-                    const int e = e0 + (tid & 31) / g;
-                    if (e >= cnt) continue;
-                    const int64_t s0 = st_start[e];
-                    const int len = st_k[e];
-                    const V b = (V)st_b[e];
-                    for (int i = lane_g; i < len; i += g) {
-                        const int r = __ldg(a.arow + s0 + i);
-                        const float av = __ldg(a.aval + s0 + i);
-                        if (r >= t0 + tw) break;  // rows ascend: the rest is past this pass
-                        if (r < t0) continue;
-                        const V prod = (V)av * b;
-                        if (prod > V(0)) atomicAdd(&acc[r - t0], prod);
-                        else atomic_mark_zero(&acc[r - t0]);  // fp32 underflow: keep the entry
+            for (int64_t c0 = q0; c0 < q1; c0 += kSweepSeg) {
+                const int cnt = (int)((q1 - c0) < kSweepSeg ? (q1 - c0) : kSweepSeg);
+                if (t0 == r_lo || chunked) {
+                    // the part's sub-segment of every A_*k (rowpart index), and for later
+                    // tiles of a chunked column the cursor re-found at the tile's first row
+                    for (int i = tid; i < cnt; i += NT) {
+                        const int k = __ldg(a.brow + c0 + i);
+                        const int *pk = a.rowpart + (int64_t)k * (kParts + 1);
+                        const uint32_t base = (uint32_t)__ldg(a.acp + k);
+                        uint32_t s = base + (uint32_t)__ldg(pk + p0);
+                        const uint32_t e = base + (uint32_t)__ldg(pk + p1);
+                        if (t0 > r_lo) s = lower_row(a.apair, s, e, t0);
+                        cur[i] = s;
+                        end[i] = e;
+                        bkj[i] = __ldg(a.bval + c0 + i);
                     }
                 }
-                __syncthreads();
                 if (tid == 0) s_next = 0;
+                __syncthreads();
+                // groups of g lanes take segments dynamically and walk each from its cursor
+                // while the rows stay inside the tile, 4 gathers in flight per lane
+                for (;;) {
+                    int e0 = 0;
+                    if (lane == 0) e0 = atomicAdd(&s_next, 32 / g);
+                    e0 = __shfl_sync(0xffffffffu, e0, 0);
+                    if (e0 >= cnt) break;
+                    const int e = e0 + lane / g;
+                    const bool has = e < cnt;
+                    const uint32_t pos = has ? cur[e] : 0u, fin = has ? end[e] : 0u;
+                    const V b = has ? (V)bkj[e] : V(0);
+                    uint32_t stop = fin;
+                    for (uint32_t i = pos + (uint32_t)lane_g;; i += 4u * (uint32_t)g) {
+                        int2 pv[4];
+#pragma unroll
+                        for (int u = 0; u < 4; u++) {
+                            const uint32_t q = i + (uint32_t)(u * g);
+                            pv[u] = q < fin ? __ldg(a.apair + q) : make_int2(INT_MAX, 0);
+                        }
+                        bool done = false;
+#pragma unroll
+                        for (int u = 0; u < 4; u++) {
+                            if (done) continue;
+                            if ((int64_t)pv[u].x >= t_end) {
+                                const uint32_t q = i + (uint32_t)(u * g);
+                                stop = q < fin ? q : fin;
+                                done = true;
+                            } else {
+                                const V prod = (V)__int_as_float(pv[u].y) * b;
+                                V *slot = &acc[pv[u].x - t0];
+                                if (prod > V(0)) atomicAdd(slot, prod);
+                                else atomic_mark_zero(slot);  // fp32 underflow: keep the entry
+                            }
+                        }
+                        if (done) break;
+                    }
+                    // the segment's new cursor: the first position the group did not take
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1)
+                        if (o < g) {
+                            const uint32_t t = __shfl_xor_sync(0xffffffffu, stop, o);
+                            stop = t < stop ? t : stop;
+                        }
+                    if (has && lane_g == 0 && !chunked) cur[e] = stop;
+                }
+                __syncthreads();
             }
-            // the pass's touched rows, in row order
+            // the tile's touched rows, in row order: to the item's staging slot, or (with
+            // candidates) to the candidate buffer when they can still be in the part's top
             for (int i0 = 0; i0 < tw; i0 += NT) {
                 const int i = i0 + tid;
                 const V v = i < tw ? acc[i] : V(0);
-                // fp64: value > 0 is the structure; fp32 products can underflow to 0, so
-                // a touched-but-zero entry is marked by the sign bit (see the add below)
                 const int f = dense_touched(v);
+                const float vf = fabsf((float)v);
                 int tot;
-                const int pos = block_excl_scan<NT>(f, sscan, tot);
-                if (f && written + pos < cap) {
-                    a.stg_row[dst0 + written + pos] = (int32_t)(t0 + i);
-                    a.stg_val[dst0 + written + pos] = fabsf((float)v);
+                if (cand) {
+                    if (s_ncand > kCandBuf - NT) reduce_cands();  // CTA-uniform
+                    if (f) {
+                        nloc++;
+                        if ((double)vf >= theta) {
+                            mloc++;
+                            sloc += (double)vf;
+                        }
+                    }
+                    const int acc_c = f && (!s_reduced || val_bits(vf) > s_thr);
+                    const int pos = block_excl_scan<NT>(acc_c, sscan, tot);
+                    const int base = s_ncand;
+                    if (acc_c) {
+                        crow[base + pos] = (int32_t)(t0 + i);
+                        cval[base + pos] = vf;
+                    }
+                    __syncthreads();
+                    if (tid == 0) s_ncand = base + tot;
+                    __syncthreads();
+                } else {
+                    const int pos = block_excl_scan<NT>(f, sscan, tot);
+                    if (f && written + pos < cap) {
+                        a.stg_row[dst0 + written + pos] = (int32_t)(t0 + i);
+                        a.stg_val[dst0 + written + pos] = vf;
+                    }
+                    written += tot;
                 }
-                written += tot;
             }
             __syncthreads();
+        }
+        if (cand) {
+            if (s_ncand > a.cand_k) reduce_cands();
+            const int nc = s_ncand;
+            for (int i = tid; i < nc; i += NT) {
+                a.stg_row[dst0 + i] = crow[i];
+                a.stg_val[dst0 + i] = cval[i];
+            }
+            written = nc;
+            const int n_all = block_sum<NT, int>(nloc, sscan);
+            const int m_all = block_sum<NT, int>(mloc, sscan);
+            const double s_all = block_sum<NT, double>(sloc, sred);
+            if (tid == 0) {
+                a.stg_nnz[idx] = n_all;
+                a.stg_m[idx] = m_all;
+                a.stg_s[idx] = s_all;
+            }
         }
         if (tid == 0) {
             if (written > cap) {
@@ -146,18 +267,20 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_dense_part(BinArgs a) {
     }
 }
 
+constexpr size_t kSweepSmem = kSweepTileBytes + (size_t)kSweepSeg * 12 + (size_t)kCandBuf * 8;
+
 cudaError_t launch_dense_part(bool fp64, const BinArgs &a, int grid, cudaStream_t s) {
     ++g_launches;
-    if (fp64) k_dense_part<double><<<grid, kDenseThreads, kDenseTileBytes, s>>>(a);
-    else k_dense_part<float><<<grid, kDenseThreads, kDenseTileBytes, s>>>(a);
+    if (fp64) k_dense_sweep<double><<<grid, kDenseThreads, kSweepSmem, s>>>(a);
+    else k_dense_sweep<float><<<grid, kDenseThreads, kSweepSmem, s>>>(a);
     return cudaGetLastError();
 }
 
 int dense_part_occupancy(bool fp64) {
-    auto fn = fp64 ? k_dense_part<double> : k_dense_part<float>;
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kDenseTileBytes);
+    auto fn = fp64 ? k_dense_sweep<double> : k_dense_sweep<float>;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepSmem);
     int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kDenseThreads, kDenseTileBytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kDenseThreads, kSweepSmem);
     return nb;
 }
 

@@ -372,8 +372,7 @@ __global__ void k_split_items(int nsplit, const int32_t *split_list, const int32
                               const int64_t *ioff, int32_t *item_col, int32_t *item_pr) {
     for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < nsplit; s += gridDim.x * blockDim.x) {
         const int32_t col = split_list[s];
-        const int Pv = split_P[col] & ~(kSplitFp64 | kSplitShared);
-        const int P = Pv < 32 ? Pv : 32;
+        const int P = split_parts(split_P[col]);
         const int step = 32 / P;
         const int64_t i0 = ioff[s];
         for (int p = 0; p < P; p++) {
@@ -394,22 +393,38 @@ cudaError_t launch_split_items(int nsplit, const int32_t *split_list, const int3
 
 __global__ void k_split_stitch(int nc, const int64_t *ioff, int64_t item0, const int32_t *item_col,
                                const int64_t *sioff, const int *col_flag, int64_t *ccp,
-                               int32_t *colmap) {
+                               int32_t *colmap, const int64_t *stg_nnz, const int64_t *stg_m,
+                               const double *stg_s, int64_t *fnnz, int64_t *fm, double *fs) {
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c <= nc; c += gridDim.x * blockDim.x) {
         const int64_t i = ioff[c] - item0;  // first item of chunk column c (or the end)
         ccp[c] = sioff[i];
         if (c < nc) {
             const int32_t col = item_col[i];
             colmap[c] = col_flag[col] ? -1 : col;
+            if (stg_nnz) {  // candidates: the column's statistics are the sums over its parts
+                const int64_t i1 = ioff[c + 1] - item0;
+                int64_t n = 0, m = 0;
+                double sm = 0.0;
+                for (int64_t q = i; q < i1; q++) {
+                    n += stg_nnz[q];
+                    m += stg_m[q];
+                    sm += stg_s[q];
+                }
+                fnnz[c] = n;
+                fm[c] = m;
+                fs[c] = sm;
+            }
         }
     }
 }
 cudaError_t launch_split_stitch(int nc, const int64_t *ioff, int64_t item0, const int32_t *item_col,
                                 const int64_t *sioff, const int *col_flag, int64_t *ccp,
-                                int32_t *colmap, cudaStream_t s) {
+                                int32_t *colmap, const int64_t *stg_nnz, const int64_t *stg_m,
+                                const double *stg_s, int64_t *fnnz, int64_t *fm, double *fs,
+                                cudaStream_t s) {
     ++g_launches;
     k_split_stitch<<<(nc + 256) / 256, 256, 0, s>>>(nc, ioff, item0, item_col, sioff, col_flag, ccp,
-                                                   colmap);
+                                                   colmap, stg_nnz, stg_m, stg_s, fnnz, fm, fs);
     return cudaGetLastError();
 }
 
@@ -647,7 +662,9 @@ __global__ void __launch_bounds__(kPruneNT)
             const float *__restrict__ cval, const int64_t *__restrict__ soff,
             int32_t *__restrict__ srow, float *__restrict__ sval, int64_t *__restrict__ scnt,
             float *__restrict__ chaos_out, float *chaos_max, PruneParams pp,
-            const int32_t *__restrict__ colmap, unsigned long long *out_count) {
+            const int32_t *__restrict__ colmap, unsigned long long *out_count,
+            const int64_t *__restrict__ fnnz, const int64_t *__restrict__ fm,
+            const double *__restrict__ fs) {
     __shared__ unsigned hist[256];
     __shared__ int sint[4];
     __shared__ double sred[kPruneNT / 32];
@@ -658,19 +675,25 @@ __global__ void __launch_bounds__(kPruneNT)
         if (col < 0) continue;
         const int64_t base = ccp[ci];
         const int nnz = (int)(ccp[ci + 1] - base);
-        prune_column<kPruneNT>(crow + base, cval + base, nnz, col, soff, srow, sval, scnt, chaos_out,
-                               chaos_max, out_count, pp, hist, sint, sred, sscan);
+        if (fnnz)  // candidates of split parts + the whole column's statistics
+            prune_column<kPruneNT>(crow + base, cval + base, nnz, col, soff, srow, sval, scnt,
+                                   chaos_out, chaos_max, out_count, pp, hist, sint, sred, sscan,
+                                   fnnz[ci], fm[ci], fs[ci]);
+        else
+            prune_column<kPruneNT>(crow + base, cval + base, nnz, col, soff, srow, sval, scnt,
+                                   chaos_out, chaos_max, out_count, pp, hist, sint, sred, sscan);
     }
 }
 
 cudaError_t launch_prune(int64_t ncols, const int64_t *ccp, const int32_t *crow, const float *cval,
                          const int64_t *soff, int32_t *srow, float *sval, int64_t *scnt,
                          float *chaos, float *chaos_max, const PruneParams &pp, int grid,
-                         cudaStream_t s, const int32_t *colmap, unsigned long long *out_count) {
+                         cudaStream_t s, const int32_t *colmap, unsigned long long *out_count,
+                         const int64_t *fnnz, const int64_t *fm, const double *fs) {
     if (ncols <= 0) return cudaSuccess;
     ++g_launches;
     k_prune<<<grid, kPruneNT, 0, s>>>(ncols, ccp, crow, cval, soff, srow, sval, scnt, chaos,
-                                      chaos_max, pp, colmap, out_count);
+                                      chaos_max, pp, colmap, out_count, fnnz, fm, fs);
     return cudaGetLastError();
 }
 

@@ -565,12 +565,56 @@ __global__ void __launch_bounds__(NT, (bin_min_blocks<CAP, NT, MODE, GLOBAL, ATO
             const uint32_t scap = cap / W;
             int *wk = keys + (size_t)warp * scap;
             V *wv = vals + (size_t)warp * scap;
-            const int cnt_w = warp_compact<V>(wk, wv, (int)scap,
-                                              [](int k, V) { return k != kEmptyKey; });
+            int cnt_w = warp_compact<V>(wk, wv, (int)scap,
+                                        [](int k, V) { return k != kEmptyKey; });
 #ifdef MCLX_PROF
             if (tid == 0) PROF_ADD(6, clock64() - prof_e0);  // compaction of the slices
             const long long prof_e1 = clock64();
 #endif
+            if (MODE == kPart && a.cand_k > 0) {
+                // candidates: statistics of all the part's entries, then each warp keeps its
+                // slice's share of the part's top-cand_k (segmented radix select)
+                const double theta = a.pp.theta;
+                int mloc = 0;
+                double sloc = 0.0;
+                for (int i = lane; i < cnt_w; i += 32) {
+                    const double v = (double)(float)wv[i];
+                    if (v >= theta) {
+                        mloc++;
+                        sloc += v;
+                    }
+                }
+                mloc = warp_sum(mloc);
+                sloc = warp_sum(sloc);
+                if (lane == 0) {
+                    swi[0][warp] = cnt_w;
+                    swi[1][warp] = mloc;
+                    swd[0][warp] = sloc;
+                }
+                __syncthreads();
+                int nnz = 0, m = 0;
+                double sm = 0.0;
+                for (int w2 = 0; w2 < W; w2++) {
+                    nnz += swi[0][w2];
+                    m += swi[1][w2];
+                    sm += swd[0][w2];
+                }
+                if (tid == 0) {
+                    a.stg_nnz[idx] = nnz;
+                    a.stg_m[idx] = m;
+                    a.stg_s[idx] = sm;
+                }
+                if (nnz > a.cand_k) {
+                    uint32_t t = 0;
+                    int rowcut = 0;
+                    radix_select_topk_seg<NT, V>(wk, wv, cnt_w, a.cand_k, t, rowcut, hist, sint);
+                    cnt_w = warp_compact<V>(wk, wv, cnt_w, [=](int k, V v) {
+                        const uint32_t b = val_bits(v);
+                        return b > t || (b == t && k <= rowcut);
+                    });
+                }
+                __syncthreads();  // swi reuse below
+            }
             if (MODE == kNum || MODE == kPart) {
                 if (lane == 0) swi[0][warp] = cnt_w;
                 __syncthreads();
@@ -721,11 +765,44 @@ __global__ void __launch_bounds__(NT, (bin_min_blocks<CAP, NT, MODE, GLOBAL, ATO
                 continue;
             }
             if (MODE == kPart) {
-                // nnz <= the 7/8 fill limit <= stg_cap
+                // nnz <= the 7/8 fill limit <= stg_cap.  With candidates: statistics of all
+                // entries, then only the part's top-cand_k are sorted and staged.
+                int keep = nnz;
+                if (a.cand_k > 0) {
+                    const double theta = a.pp.theta;
+                    int mloc = 0;
+                    double sloc = 0.0;
+                    for (int i = tid; i < nnz; i += NT) {
+                        const double v = (double)(float)vals[i];
+                        if (v >= theta) {
+                            mloc++;
+                            sloc += v;
+                        }
+                    }
+                    const int m = block_sum<NT, int>(mloc, sscan);
+                    const double sm = block_sum<NT, double>(sloc, sred);
+                    if (tid == 0) {
+                        a.stg_nnz[idx] = nnz;
+                        a.stg_m[idx] = m;
+                        a.stg_s[idx] = sm;
+                    }
+                    if (nnz > a.cand_k) {
+                        uint32_t t = 0;
+                        int rowcut = 0;
+                        radix_select_topk<NT, V>(keys, vals, nnz, a.cand_k, t, rowcut, hist, sint);
+                        keep = compact_inplace<NT, V>(
+                            keys, vals, nnz,
+                            [=](int k, V v) {
+                                const uint32_t b = val_bits(v);
+                                return b > t || (b == t && k <= rowcut);
+                            },
+                            sscan);
+                    }
+                }
                 const int64_t dst = a.stg_off[idx];
-                sort_write<NT, V>(keys, vals, nnz, (int)cap, a.stg_row + dst, a.stg_val + dst,
+                sort_write<NT, V>(keys, vals, keep, (int)cap, a.stg_row + dst, a.stg_val + dst,
                                   [](V v) { return (float)v; }, sscan);
-                if (tid == 0) a.stg_cnt[idx] = nnz;
+                if (tid == 0) a.stg_cnt[idx] = keep;
                 continue;
             }
 

@@ -652,26 +652,37 @@ __device__ __forceinline__ void atomic_max_nonneg_float(float *addr, float v) {
 // entries are extracted in row order with a block scan, so the output stays sorted.
 // Writes srow/sval at soff[col], scnt[col], chaos_out[col] (if given) and folds the
 // chaos into *chaos_max and the kept count into *out_count (if given).  All NT threads call.
+// With fnnz >= 0 the entries given are only CANDIDATES of the column (the top max(S, R) of
+// every row-range part, run_split) and (fnnz, fm, fs) are the statistics of the whole
+// unpruned column: the branch is decided on those, the selection runs on the candidates.
 template <int NT>
 __device__ void prune_column(const int32_t *rows, const float *vals, int nnz, int64_t col,
                              const int64_t *soff, int32_t *srow, float *sval, int64_t *scnt,
                              float *chaos_out, float *chaos_max, unsigned long long *out_count,
                              const PruneParams &pp, unsigned *hist, int *sint, double *sred,
-                             int *sscan) {
+                             int *sscan, int64_t fnnz = -1, int64_t fm = 0, double fs = 0.0) {
     const int tid = threadIdx.x;
-    int mloc = 0;
-    double sloc = 0.0;
-    for (int i = tid; i < nnz; i += NT) {
-        double v = (double)vals[i];
-        if (v >= pp.theta) {
-            mloc++;
-            sloc += v;
+    int64_t nnz_b = nnz, m;
+    double s;
+    if (fnnz >= 0) {
+        nnz_b = fnnz;
+        m = fm;
+        s = fs;
+    } else {
+        int mloc = 0;
+        double sloc = 0.0;
+        for (int i = tid; i < nnz; i += NT) {
+            double v = (double)vals[i];
+            if (v >= pp.theta) {
+                mloc++;
+                sloc += v;
+            }
         }
+        m = block_sum<NT, int>(mloc, sscan);
+        s = block_sum<NT, double>(sloc, sred);
     }
-    const int m = block_sum<NT, int>(mloc, sscan);
-    const double s = block_sum<NT, double>(sloc, sred);
     int64_t K;
-    const int br = prune_branch(pp, nnz, m, s, K);
+    const int br = prune_branch(pp, nnz_b, m, s, K);
     uint32_t t = 0;
     int rowcut = 0, sel;
     if (br == 0) {

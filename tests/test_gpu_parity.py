@@ -417,3 +417,24 @@ def test_full_mcl_clusters_equal_small_c3_c4_shapes(shape):
     assert k == ref.nclusters
     assert np.array_equal(labels.cpu().numpy(), ref.labels)
     assert abs(len(hist) - ref.iterations) <= 1
+
+
+@pytest.mark.parametrize("graph", ["rmat14", "C1it1"])
+def test_iterate_split_columns_all_entries(monkeypatch, graph):
+    """Split parts that stage every entry (MCLX_SPLIT_CAND=0) instead of their top max(S, R)
+    candidates plus statistics: the same kept sets as the oracle."""
+    monkeypatch.setenv("MCLX_SPLIT_CAND", "0")
+    monkeypatch.setenv("MCLX_SPLIT_MIN_NEED", "100")
+    monkeypatch.setenv("MCLX_SPLIT_PART_NEED", "16")
+    if graph == "rmat14":
+        A = f32(O.preprocess(synth.rmat(scale=14, seed=4)))
+    else:
+        A0 = O.preprocess(synth.planted_partition())
+        A, _ = O.prune_inflate(O.expand(A0)[0], 1e-4, 1100, 1400, 0.9, 2.0)
+        A = f32(A)
+    ctx = M.Context()
+    Ag, st = ctx.iterate(dev(A), M.Params())
+    Cr, fl = O.expand(A)
+    _, info = O.prune_inflate(Cr, 1e-4, 1100, 1400, 0.9, 2.0)
+    kept_parity(host_mat(Ag), Cr, info, (1e-4, 1100, 1400, 0.9))
+    assert st["split_cols"] > 0

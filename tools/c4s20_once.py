@@ -1,0 +1,9 @@
+"""One fused iteration of C4 at R-MAT scale 20 (for launch lists under ncu)."""
+import sys
+sys.path.insert(0, ".")
+import torch, synth
+import paper_2002_10083_b200 as M
+A = M.preprocess(M.CSC.from_host(synth.config_graph("C4", 0.25)))
+An, st = M.iterate(A, M.Params())
+torch.cuda.synchronize()
+print({k: st[k] for k in ("flops", "split_cols", "split_vcols", "split_vms", "bin_ms")})
