@@ -31,6 +31,8 @@
 
 namespace mclx {
 
+constexpr int kLongPerTile = 16;  // expected rows per tile above which a warp walks a segment
+
 __device__ __forceinline__ int dense_touched(double v) { return v > 0.0 ? 1 : 0; }
 // fp32 tiles start at +0 and every add is >= 0, so a touched entry is > 0 -- unless its
 // products underflowed to 0.  Those are flagged by storing -0.0 (sign bit) at the first
@@ -44,9 +46,6 @@ __device__ __forceinline__ void atomic_mark_zero(float *p) {
 }
 __device__ __forceinline__ void atomic_mark_zero(double *) {}  // fp64 products never underflow
 
-__device__ __forceinline__ int dense_group_size(int64_t avg) {
-    return avg >= 48 ? 32 : avg >= 24 ? 16 : avg >= 12 ? 8 : avg >= 6 ? 4 : avg >= 3 ? 2 : 1;
-}
 
 // first position q in [lo, hi) of A with row >= r (rows of a segment ascend)
 __device__ __forceinline__ uint32_t lower_row(const int2 *__restrict__ ap, uint32_t lo, uint32_t hi,
@@ -57,6 +56,49 @@ __device__ __forceinline__ uint32_t lower_row(const int2 *__restrict__ ap, uint3
         else hi = mid;
     }
     return lo;
+}
+
+// One group of G lanes walks segment e (its cursor .. end) while the rows stay below t_end,
+// adding b_kj * a_ik into the tile (4 gathers in flight per lane), then stores the segment's
+// new cursor: the first position the group did not take (rows ascend in a segment).
+template <int G, typename V>
+__device__ __forceinline__ void sweep_walk(const int2 *__restrict__ ap, V *acc, int64_t t0,
+                                           int64_t t_end, uint32_t *cur, const uint32_t *end,
+                                           const float *bkj, int e, bool has, bool save) {
+    const int lane_g = (int)(threadIdx.x & 31) & (G - 1);
+    const uint32_t pos = has ? cur[e] : 0u, fin = has ? end[e] : 0u;
+    const V b = has ? (V)bkj[e] : V(0);
+    uint32_t stop = fin;
+    for (uint32_t i = pos + (uint32_t)lane_g;; i += 4u * G) {
+        int2 pv[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const uint32_t q = i + (uint32_t)(u * G);
+            pv[u] = q < fin ? __ldg(ap + q) : make_int2(INT_MAX, 0);
+        }
+        bool done = false;
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            if (done) continue;
+            if ((int64_t)pv[u].x >= t_end) {
+                const uint32_t q = i + (uint32_t)(u * G);
+                stop = q < fin ? q : fin;
+                done = true;
+            } else {
+                const V prod = (V)__int_as_float(pv[u].y) * b;
+                V *slot = &acc[pv[u].x - t0];
+                if (prod > V(0)) atomicAdd(slot, prod);
+                else atomic_mark_zero(slot);  // fp32 underflow: keep the entry
+            }
+        }
+        if (done) break;
+    }
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) {
+        const uint32_t t = __shfl_xor_sync(0xffffffffu, stop, o);
+        stop = t < stop ? t : stop;
+    }
+    if (has && lane_g == 0 && save) cur[e] = stop;
 }
 
 template <typename V>
@@ -71,10 +113,11 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_dense_sweep(BinArgs a) {
     int *crow = reinterpret_cast<int *>(bkj + kSweepSeg);                   // candidates (rows)
     float *cval = reinterpret_cast<float *>(crow + kCandBuf);              // candidates (values)
     __shared__ int sscan[NT / 32];
+    __shared__ int s_wcnt[32];
     __shared__ double sred[NT / 32];
     __shared__ unsigned hist[256];
     __shared__ int sint[4];
-    __shared__ int s_col, s_idx, s_pr, s_next, s_ncand, s_reduced;
+    __shared__ int s_col, s_idx, s_pr, s_nextL, s_nextS, s_nL, s_nS, s_ncand, s_reduced;
     __shared__ uint32_t s_thr;
     const bool cand = a.cand_k > 0;
     const double theta = a.pp.theta;
@@ -101,11 +144,10 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_dense_sweep(BinArgs a) {
         const int64_t nb = q1 - q0;
         const int64_t dst0 = a.stg_off[idx], cap = a.stg_off[idx + 1] - dst0;
         const int64_t ntiles = (r_hi - r_lo + TILE - 1) / TILE;
-        // lanes per segment from the expected products of one segment in one tile
-        const int64_t fpart = a.flops[col] * (p1 - p0) / kParts;
-        const int g = dense_group_size(nb > 0 && ntiles > 0 ? fpart / (nb * ntiles) : 0);
-        const int lane_g = lane & (g - 1);
         const bool chunked = nb > kSweepSeg;
+        // a sub-segment expecting >= kLongPerTile rows per tile is walked by a whole warp,
+        // shorter ones by one lane each (R-MAT columns mix hub segments with 1-3 row ones)
+        const uint32_t long_len = (uint32_t)(kLongPerTile * ntiles);
         int64_t written = 0;
         int nloc = 0, mloc = 0;  // candidates: statistics of all the part's entries
         double sloc = 0.0;
@@ -138,7 +180,14 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_dense_sweep(BinArgs a) {
                 const int cnt = (int)((q1 - c0) < kSweepSeg ? (q1 - c0) : kSweepSeg);
                 if (t0 == r_lo || chunked) {
                     // the part's sub-segment of every A_*k (rowpart index), and for later
-                    // tiles of a chunked column the cursor re-found at the tile's first row
+                    // tiles of a chunked column the cursor re-found at the tile's first row;
+                    // empty ones are dropped, long ones listed from the front, short ones
+                    // from the back
+                    if (tid == 0) {
+                        s_nL = 0;
+                        s_nS = 0;
+                    }
+                    __syncthreads();
                     for (int i = tid; i < cnt; i += NT) {
                         const int k = __ldg(a.brow + c0 + i);
                         const int *pk = a.rowpart + (int64_t)k * (kParts + 1);
@@ -146,70 +195,56 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_dense_sweep(BinArgs a) {
                         uint32_t s = base + (uint32_t)__ldg(pk + p0);
                         const uint32_t e = base + (uint32_t)__ldg(pk + p1);
                         if (t0 > r_lo) s = lower_row(a.apair, s, e, t0);
-                        cur[i] = s;
-                        end[i] = e;
-                        bkj[i] = __ldg(a.bval + c0 + i);
+                        if (e > s) {
+                            const int slot = (e - s >= long_len) ? atomicAdd(&s_nL, 1)
+                                                                  : kSweepSeg - 1 - atomicAdd(&s_nS, 1);
+                            cur[slot] = s;
+                            end[slot] = e;
+                            bkj[slot] = __ldg(a.bval + c0 + i);
+                        }
                     }
                 }
-                if (tid == 0) s_next = 0;
+                if (tid == 0) {
+                    s_nextL = 0;
+                    s_nextS = 0;
+                }
                 __syncthreads();
-                // groups of g lanes take segments dynamically and walk each from its cursor
-                // while the rows stay inside the tile, 4 gathers in flight per lane
+                // warps take long segments one at a time, then short ones 32 at a time
+                const int nL = s_nL, nS = s_nS;
                 for (;;) {
                     int e0 = 0;
-                    if (lane == 0) e0 = atomicAdd(&s_next, 32 / g);
+                    if (lane == 0) e0 = atomicAdd(&s_nextL, 1);
                     e0 = __shfl_sync(0xffffffffu, e0, 0);
-                    if (e0 >= cnt) break;
-                    const int e = e0 + lane / g;
-                    const bool has = e < cnt;
-                    const uint32_t pos = has ? cur[e] : 0u, fin = has ? end[e] : 0u;
-                    const V b = has ? (V)bkj[e] : V(0);
-                    uint32_t stop = fin;
-                    for (uint32_t i = pos + (uint32_t)lane_g;; i += 4u * (uint32_t)g) {
-                        int2 pv[4];
-#pragma unroll
-                        for (int u = 0; u < 4; u++) {
-                            const uint32_t q = i + (uint32_t)(u * g);
-                            pv[u] = q < fin ? __ldg(a.apair + q) : make_int2(INT_MAX, 0);
-                        }
-                        bool done = false;
-#pragma unroll
-                        for (int u = 0; u < 4; u++) {
-                            if (done) continue;
-                            if ((int64_t)pv[u].x >= t_end) {
-                                const uint32_t q = i + (uint32_t)(u * g);
-                                stop = q < fin ? q : fin;
-                                done = true;
-                            } else {
-                                const V prod = (V)__int_as_float(pv[u].y) * b;
-                                V *slot = &acc[pv[u].x - t0];
-                                if (prod > V(0)) atomicAdd(slot, prod);
-                                else atomic_mark_zero(slot);  // fp32 underflow: keep the entry
-                            }
-                        }
-                        if (done) break;
-                    }
-                    // the segment's new cursor: the first position the group did not take
-#pragma unroll
-                    for (int o = 1; o < 32; o <<= 1)
-                        if (o < g) {
-                            const uint32_t t = __shfl_xor_sync(0xffffffffu, stop, o);
-                            stop = t < stop ? t : stop;
-                        }
-                    if (has && lane_g == 0 && !chunked) cur[e] = stop;
+                    if (e0 >= nL) break;
+                    sweep_walk<32, V>(a.apair, acc, t0, t_end, cur, end, bkj, e0, true, !chunked);
+                }
+                for (;;) {
+                    int e0 = 0;
+                    if (lane == 0) e0 = atomicAdd(&s_nextS, 32);
+                    e0 = __shfl_sync(0xffffffffu, e0, 0);
+                    if (e0 >= nS) break;
+                    const int e = e0 + lane;
+                    sweep_walk<1, V>(a.apair, acc, t0, t_end, cur, end, bkj, kSweepSeg - 1 - e,
+                                     e < nS, !chunked);
                 }
                 __syncthreads();
             }
-            // the tile's touched rows, in row order: to the item's staging slot, or (with
-            // candidates) to the candidate buffer when they can still be in the part's top
-            for (int i0 = 0; i0 < tw; i0 += NT) {
-                const int i = i0 + tid;
-                const V v = i < tw ? acc[i] : V(0);
-                const int f = dense_touched(v);
-                const float vf = fabsf((float)v);
-                int tot;
-                if (cand) {
-                    if (s_ncand > kCandBuf - NT) reduce_cands();  // CTA-uniform
+            // the tile's touched rows.  Warp w owns the contiguous rows [w RW, (w+1) RW) of the
+            // tile, so the compaction needs warp ballots, not CTA-wide scans (which cost ~5 warp
+            // instructions per row of the whole row space swept by every dense column).
+            constexpr int RW = TILE / 32;
+            const int w = tid >> 5;
+            const unsigned lt = (1u << lane) - 1u;
+            if (cand) {
+                // candidates: rounds of 32 rows per warp (<= NT appends per round, in any
+                // order -- the final set is sorted by row below); the buffer is reduced
+                // (CTA-uniform decision) before a round that could overflow it
+                for (int r0 = 0; r0 < RW; r0 += 32) {
+                    if (s_ncand > kCandBuf - NT) reduce_cands();
+                    const int i = w * RW + r0 + lane;
+                    const V v = i < tw ? acc[i] : V(0);
+                    const int f = dense_touched(v);
+                    const float vf = fabsf((float)v);
                     if (f) {
                         nloc++;
                         if ((double)vf >= theta) {
@@ -217,30 +252,62 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_dense_sweep(BinArgs a) {
                             sloc += (double)vf;
                         }
                     }
-                    const int acc_c = f && (!s_reduced || val_bits(vf) > s_thr);
-                    const int pos = block_excl_scan<NT>(acc_c, sscan, tot);
-                    const int base = s_ncand;
-                    if (acc_c) {
-                        crow[base + pos] = (int32_t)(t0 + i);
-                        cval[base + pos] = vf;
+                    const bool acc_c = f && (!s_reduced || val_bits(vf) > s_thr);
+                    const unsigned bal = __ballot_sync(0xffffffffu, acc_c);
+                    if (bal) {
+                        int base = 0;
+                        if (lane == 0) base = atomicAdd(&s_ncand, __popc(bal));
+                        base = __shfl_sync(0xffffffffu, base, 0);
+                        if (acc_c) {
+                            crow[base + __popc(bal & lt)] = (int32_t)(t0 + i);
+                            cval[base + __popc(bal & lt)] = vf;
+                        }
                     }
                     __syncthreads();
-                    if (tid == 0) s_ncand = base + tot;
-                    __syncthreads();
-                } else {
-                    const int pos = block_excl_scan<NT>(f, sscan, tot);
-                    if (f && written + pos < cap) {
-                        a.stg_row[dst0 + written + pos] = (int32_t)(t0 + i);
-                        a.stg_val[dst0 + written + pos] = vf;
-                    }
-                    written += tot;
                 }
+            } else {
+                // every entry, in row order: per-warp counts, their scan, then the writes
+                int cntw = 0;
+                for (int r0 = 0; r0 < RW; r0 += 32) {
+                    const int i = w * RW + r0 + lane;
+                    cntw += __popc(__ballot_sync(0xffffffffu, i < tw && dense_touched(acc[i])));
+                }
+                if (lane == 0) s_wcnt[w] = cntw;
+                __syncthreads();
+                const int wc = s_wcnt[lane];
+                int inc = wc;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, inc, o);
+                    if (lane >= o) inc += y;
+                }
+                int64_t off = written + __shfl_sync(0xffffffffu, inc - wc, w);
+                const int total = __shfl_sync(0xffffffffu, inc, 31);
+                for (int r0 = 0; r0 < RW; r0 += 32) {
+                    const int i = w * RW + r0 + lane;
+                    const V v = i < tw ? acc[i] : V(0);
+                    const int f = dense_touched(v);
+                    const unsigned bal = __ballot_sync(0xffffffffu, f);
+                    const int64_t at = off + __popc(bal & lt);
+                    if (f && at < cap) {
+                        a.stg_row[dst0 + at] = (int32_t)(t0 + i);
+                        a.stg_val[dst0 + at] = fabsf((float)v);
+                    }
+                    off += __popc(bal);
+                }
+                written += total;
             }
             __syncthreads();
         }
         if (cand) {
             if (s_ncand > a.cand_k) reduce_cands();
+            // the part's candidates, sorted by row for the stitch (parts are row ranges)
             const int nc = s_ncand;
+            int P = 1;
+            while (P < nc) P <<= 1;
+            for (int i = nc + tid; i < P; i += NT) crow[i] = kPadKey;
+            __syncthreads();
+            bitonic_sort<NT, float>(crow, cval, P);
             for (int i = tid; i < nc; i += NT) {
                 a.stg_row[dst0 + i] = crow[i];
                 a.stg_val[dst0 + i] = cval[i];
