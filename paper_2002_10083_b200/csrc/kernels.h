@@ -85,10 +85,11 @@ struct BinArgs {
     int64_t *stg_m;    // [items] entries >= theta
     double *stg_s;     // [items] their mass (fp64)
 };
-// largest cand_k the dense sweep's candidate buffer holds (kCandBuf - 1024 free slots per
-// tile chunk of 1024 entries)
-constexpr int kCandBuf = 2560;
-constexpr int kCandMax = kCandBuf - 1024;
+// the dense sweep's candidate buffer: a round of the tile compaction appends <= 1024 entries,
+// and the buffer is cut back to cand_k (a radix select) when it could overflow, so the
+// slack kCandBuf - 1024 - cand_k sets how often that happens (~every slack accepted entries)
+constexpr int kCandBuf = 4096;
+constexpr int kCandMax = 2048;
 // the shared-table bin that runs the parts of split columns (table slots, threads)
 constexpr int kPartCap = 8192;
 constexpr int kPartThreads = 512;
@@ -100,7 +101,7 @@ constexpr int kFineParts = 128;  // the finer index used by private-slice split 
 constexpr int kDenseThreads = 1024;
 constexpr int kDenseParts = 8;             // parts of a dense column (32 / 8 = 4 rowparts each)
 constexpr int kSweepTileBytes = 163840;    // dense tile: 40960 fp32 / 20480 fp64 rows
-constexpr int kSweepSeg = 3072;            // segment descriptors (cursor, end, b) per chunk
+constexpr int kSweepSeg = 2048;            // segment descriptors (cursor, end, b) per chunk
 // split_P flag: the column needs fp64 accumulation (more than kFp64Terms segments)
 constexpr int kSplitFp64 = 1 << 30;
 // split_P flag: short sub-segments, run the parts in the CTA-shared-table family
