@@ -104,7 +104,9 @@ typedef struct {
     double est_nnz;          /* Cohen estimate of nnz(A*A) (sum over columns), -1 if not run    */
     double cf;               /* flops / nnz_unpruned (or / est_nnz)                             */
     float chaos;             /* max_j chaos_j of the pruned, renormalised columns (Q9)          */
-    int32_t phases;          /* column batches used                                             */
+    int32_t phases;          /* column batches ("phases") the call ran: the planner cuts
+                                the output columns into batches of near-equal estimated bytes
+                                within mem_safety x free HBM (env MCLX_PHASES=h forces h)       */
     int32_t retries;         /* columns re-run after a hash-table overflow                      */
     int32_t estimator_used;  /* 1 exact symbolic, 2 Cohen, 3 Cohen-binned numeric into upper-bound
                                 slots min(f_j, m) + compaction (unfused products, no symbolic) */
@@ -126,6 +128,7 @@ typedef struct {
     int64_t split_vcols[3];  /* split columns per part variant: 8192-slot shared tables,
                                 16384-slot shared tables, fp64 global tables                    */
     float split_vms[3];      /* device time per part variant (parts + stitch + prune)           */
+    int32_t stages;          /* SUMMA inner panels (stage products per phase), 0 if none        */
 } mcl_stats_t;
 
 /* Allocator callbacks: device memory, stream-ordered.  NULL callbacks select the

@@ -71,7 +71,8 @@ class StatsT(C.Structure):
                 ("bin_out", C.c_int64 * (NUM_BINS + 1)), ("comm_bytes", C.c_int64),
                 ("peak_partial", C.c_int64), ("split_cols", C.c_int64),
                 ("split_items", C.c_int64), ("split_ms", C.c_float),
-                ("split_vcols", C.c_int64 * 3), ("split_vms", C.c_float * 3)]
+                ("split_vcols", C.c_int64 * 3), ("split_vms", C.c_float * 3),
+                ("stages", C.c_int32)]
 
     def as_dict(self) -> dict:
         d = {k: getattr(self, k) for k, _ in self._fields_}

@@ -60,6 +60,9 @@ struct mcl_ctx {
     bool split_private = true;                // MCLX_SPLIT_PRIVATE=0: P <= 4 parts shared-table too
     bool validate = false;                    // MCLX_VALIDATE=1: check input CSC invariants
     bool split_cand = true;                   // MCLX_SPLIT_CAND=0: split parts stage every entry
+    int force_phases = 0;                     // MCLX_PHASES=h forces h column batches (tests)
+    int64_t phase_budget = -1;                // MCLX_PHASE_BUDGET_MB: bytes per batch (else
+                                              // mem_safety x free HBM)
     int family = -1;                          // MCLX_FAMILY=0/1 forces a kernel family (A/B runs)
 };
 
@@ -920,6 +923,125 @@ int assemble(mcl_ctx *c, int64_t nrows, int64_t n, const int64_t *cnt, const int
     return MCL_OK;
 }
 
+// Phase planner (§II: HipMCL forms the product "in phases" of column batches;
+// P:575-579 / P:594-595 §V: the estimate sizes them; reading Q15): cut the columns [0, n)
+// into h batches of near-equal estimated bytes (bytes_dev: int64 [n], device) so that one
+// batch fits `budget` bytes; h = ceil(total / budget), or c->force_phases.  bounds receives
+// h + 1 column boundaries.  Two small read-backs (the total, the h - 1 cuts).
+int plan_phases(mcl_ctx *c, const int64_t *bytes_dev, int64_t n, double budget,
+                std::vector<int64_t> &bounds, int64_t *total_out) {
+    bounds.assign(1, 0);
+    if (n <= 0) {
+        bounds.push_back(0);
+        if (total_out) *total_out = 0;
+        return MCL_OK;
+    }
+    int64_t *prefix, *cut;
+    void *tmp;
+    RC(scratch_t(c, "phase_prefix", (size_t)n + 1, &prefix));
+    RC(scratch(c, "phase_scan_tmp", scan_tmp_bytes(n + 1), &tmp));
+    CK(launch_scan_i64(bytes_dev, prefix, n, tmp, c->stream));
+    int64_t total = 0;
+    RC(readback(c, prefix + n, sizeof(int64_t), &total));
+    if (total_out) *total_out = total;
+    int64_t h = c->force_phases > 0 ? c->force_phases
+                                     : std::max<int64_t>(1, (int64_t)std::ceil((double)total / budget));
+    h = std::min<int64_t>(h, std::min<int64_t>(n, 4096));
+    if (h > 1) {
+        RC(scratch_t(c, "phase_cut", (size_t)h, &cut));
+        CK(launch_phase_cuts(prefix, n, (int)h, cut, c->stream));
+        std::vector<int64_t> hc((size_t)h - 1);
+        RC(readback(c, cut, sizeof(int64_t) * (h - 1), hc.data()));
+        for (int64_t v : hc)
+            if (v > bounds.back() && v < n) bounds.push_back(v);
+    }
+    bounds.push_back(n);
+    return MCL_OK;
+}
+
+// bytes a phase may use: MCLX_PHASE_BUDGET_MB, else mem_safety x the device's free memory
+double phase_budget(mcl_ctx *c, double mem_safety) {
+    if (c->phase_budget > 0) return (double)c->phase_budget;
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
+        cudaGetLastError();
+        return 1e18;
+    }
+    return std::max(1.0, mem_safety * (double)fr);
+}
+
+// out = [pieces[0] | pieces[1] | ...] (column concatenation of the phase outputs; the
+// pieces share nrows / row0 / n_global).  Pieces are not freed here.
+int concat_cols(mcl_ctx *c, const std::vector<mcl_csc_t> &pieces, mcl_csc_t *out) {
+    zero_csc(out);
+    int64_t n = 0, nnz = 0;
+    for (auto &q : pieces) {
+        n += q.ncols;
+        nnz += q.nnz;
+    }
+    out->col_ptr = (int64_t *)dalloc(c, (size_t)(n + 1) * sizeof(int64_t));
+    if (!out->col_ptr) return fail(c, MCL_ERR_OOM, "cannot allocate col_ptr");
+    int rc = alloc_rows_vals(c, out, nnz);
+    if (rc != MCL_OK) {
+        free_csc(c, out);
+        return rc;
+    }
+    int64_t coff = 0, off = 0;
+    for (auto &q : pieces) {
+        cudaError_t e = launch_offset_colptr(q.ncols + 1, q.col_ptr, off, out->col_ptr + coff, c->stream);
+        if (e == cudaSuccess && q.nnz) {
+            e = cudaMemcpyAsync(out->row_idx + off, q.row_idx, sizeof(int32_t) * q.nnz,
+                                cudaMemcpyDeviceToDevice, c->stream);
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(out->val + off, q.val, sizeof(float) * q.nnz,
+                                    cudaMemcpyDeviceToDevice, c->stream);
+        }
+        if (e != cudaSuccess) {
+            free_csc(c, out);
+            return fail(c, MCL_ERR_CUDA, "concat: %s", cudaGetErrorString(e));
+        }
+        coff += q.ncols;
+        off += q.nnz;
+    }
+    if (!pieces.empty()) {
+        out->nrows = pieces[0].nrows;
+        out->row0 = pieces[0].row0;
+        out->col0 = pieces[0].col0;
+        out->n_global = pieces[0].n_global;
+    }
+    out->ncols = n;
+    out->nnz = nnz;
+    return MCL_OK;
+}
+
+// accumulate the statistics of one phase into the call's
+void add_stats(mcl_stats_t *st, const mcl_stats_t &q) {
+    st->flops += q.flops;
+    st->nnz_out += q.nnz_out;
+    st->retries += q.retries;
+    st->chaos = std::max(st->chaos, q.chaos);
+    if (q.est_nnz >= 0) st->est_nnz = (st->est_nnz < 0 ? 0 : st->est_nnz) + q.est_nnz;
+    for (int b = 0; b <= kNumBins; b++) {
+        st->bin_cols[b] += q.bin_cols[b];
+        st->bin_flops[b] += q.bin_flops[b];
+        st->bin_ms[b] += q.bin_ms[b];
+        st->bin_nnzb[b] += q.bin_nnzb[b];
+        st->bin_out[b] += q.bin_out[b];
+    }
+    for (int i = 0; i < 8; i++)
+        if (q.ms[i] >= 0) st->ms[i] = (st->ms[i] < 0 ? 0.f : st->ms[i]) + q.ms[i];
+    st->split_cols += q.split_cols;
+    st->split_items += q.split_items;
+    st->split_ms += q.split_ms;
+    for (int v = 0; v < 3; v++) {
+        st->split_vcols[v] += q.split_vcols[v];
+        st->split_vms[v] += q.split_vms[v];
+    }
+    st->peak_bytes = std::max(st->peak_bytes, q.peak_bytes);
+    st->launches += q.launches;
+    st->estimator_used = q.estimator_used;
+}
+
 int merge_impl(mcl_ctx_t c, int32_t L, const mcl_csc_t *lists, mcl_csc_t *out) {
     const int64_t m = lists[0].nrows, n = lists[0].ncols;
     int64_t tot = 0;
@@ -1164,6 +1286,8 @@ int mcl_ctx_create(mcl_ctx_t *out, int device, void *stream, mcl_alloc_fn alloc,
     if (const char *e = getenv("MCLX_VALIDATE")) c->validate = atoi(e) != 0;
     if (const char *e = getenv("MCLX_FAMILY")) c->family = atoi(e);
     if (const char *e = getenv("MCLX_SPLIT_CAND")) c->split_cand = atoi(e) != 0;
+    if (const char *e = getenv("MCLX_PHASES")) c->force_phases = atoi(e);
+    if (const char *e = getenv("MCLX_PHASE_BUDGET_MB")) c->phase_budget = (int64_t)atoll(e) << 20;
     if (cudaMallocHost(&c->pin, kPinBytes) != cudaSuccess) {
         delete c;
         return MCL_ERR_CUDA;
@@ -1408,8 +1532,9 @@ int mcl_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, mcl_cs
     return mcl_iterate_range(c, A, 0, A->ncols, pin, A_next, st);
 }
 
-int mcl_iterate_range(mcl_ctx_t c, const mcl_csc_t *A, int64_t col_begin, int64_t col_end,
-                      const mcl_params_t *pin, mcl_csc_t *A_next, mcl_stats_t *st) {
+// one phase of mcl_iterate_range: the fused iteration on output columns [col_begin, col_end)
+static int iterate_range_impl(mcl_ctx_t c, const mcl_csc_t *A, int64_t col_begin, int64_t col_end,
+                              const mcl_params_t *pin, mcl_csc_t *A_next, mcl_stats_t *st) {
     if (!c) return MCL_ERR_INVALID_ARG;
     if (!A_next || !pin) return fail(c, MCL_ERR_INVALID_ARG, "NULL argument");
     zero_csc(A_next);
@@ -1519,6 +1644,64 @@ int mcl_iterate_range(mcl_ctx_t c, const mcl_csc_t *A, int64_t col_begin, int64_
         st->launches = g_launches - launches0;
     }
     guard.release();
+    return MCL_OK;
+}
+
+int mcl_iterate_range(mcl_ctx_t c, const mcl_csc_t *A, int64_t col_begin, int64_t col_end,
+                      const mcl_params_t *pin, mcl_csc_t *A_next, mcl_stats_t *st) {
+    if (!c) return MCL_ERR_INVALID_ARG;
+    if (!A_next || !pin) return fail(c, MCL_ERR_INVALID_ARG, "NULL argument");
+    zero_csc(A_next);
+    cudaSetDevice(c->device);
+    RC(check_params(c, pin));
+    RC(check_csc(c, A, "A"));
+    if (A->nrows != A->ncols) return fail(c, MCL_ERR_DIM, "mcl_iterate needs a square A");
+    if (col_begin < 0 || col_end > A->ncols || col_begin > col_end)
+        return fail(c, MCL_ERR_DIM, "bad column range [%lld,%lld)", (long long)col_begin,
+                    (long long)col_end);
+    // Phases (Q15).  The fused iteration never holds the unpruned product; what
+    // grows with the columns is the staging of the pruned columns and A_next: 16 B x
+    // min(max(S, R), f_j, m) per column (+ its col_ptr).  Columns are cut into batches of
+    // near-equal bytes within mem_safety x free HBM, each batch runs as one fused iteration
+    // and the batches' outputs are concatenated.
+    const int64_t n = col_end - col_begin;
+    const PruneParams pp = prune_params(pin);
+    int64_t *f, *bytes;
+    RC(scratch_t(c, "phase_flops", (size_t)std::max<int64_t>(n, 1), &f));
+    RC(scratch_t(c, "phase_bytes", (size_t)std::max<int64_t>(n, 1), &bytes));
+    CK(launch_flops(n, A->col_ptr, A->col_ptr, A->row_idx, col_begin, f, c->stream));
+    CK(launch_kcap(n, f, A->nrows, pp.kmax, bytes, c->stream));
+    CK(launch_affine_i64(n, bytes, 16, 16, bytes, false, c->stream));
+    std::vector<int64_t> bounds;
+    RC(plan_phases(c, bytes, n, phase_budget(c, pin->mem_safety), bounds, nullptr));
+    const int h = (int)bounds.size() - 1;
+    if (h <= 1) {
+        const int rc = iterate_range_impl(c, A, col_begin, col_end, pin, A_next, st);
+        if (rc == MCL_OK && st) st->phases = 1;
+        return rc;
+    }
+    init_stats(st);
+    std::vector<mcl_csc_t> pieces;
+    int rc = MCL_OK;
+    for (int q = 0; q < h && rc == MCL_OK; q++) {
+        mcl_csc_t piece;
+        mcl_stats_t sq;
+        rc = iterate_range_impl(c, A, col_begin + bounds[q], col_begin + bounds[q + 1], pin, &piece,
+                                st ? &sq : nullptr);
+        if (rc == MCL_OK) {
+            pieces.push_back(piece);
+            if (st) add_stats(st, sq);
+        }
+    }
+    if (rc == MCL_OK) rc = concat_cols(c, pieces, A_next);
+    for (auto &q : pieces) free_csc(c, &q);
+    if (rc != MCL_OK) return rc;
+    if (st) {
+        st->nnz_in = A->nnz;
+        st->nnz_out = A_next->nnz;
+        st->phases = h;
+        st->peak_bytes = (int64_t)c->peak;
+    }
     return MCL_OK;
 }
 
@@ -1738,7 +1921,12 @@ int mcl_summa_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, 
         guard.release();
         return MCL_OK;
     }
-    const int s = pr / gcd_i(pr, pc) * pc;  // lcm
+    // inner panels: s = lcm(pr, pc) (Q17), times MCLX_SUMMA_STAGES (a multiplier that keeps
+    // every panel inside one row and one column stripe; tests use it to run Alg. 2's merges
+    // on a 1 x 1 grid)
+    int smul = 1;
+    if (const char *e = getenv("MCLX_SUMMA_STAGES")) smul = std::max(1, atoi(e));
+    const int s = pr / gcd_i(pr, pc) * pc * smul;
     const int64_t nj = A->ncols, mi = A->nrows;
     const PruneParams pp = prune_params(pin);
     CK(cudaEventRecord(c->sev[0], c->stream));
@@ -1752,7 +1940,7 @@ int mcl_summa_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, 
     RC(scratch(c, "scan_tmp", scan_tmp_bytes(nj + 1), &tmp));
     int64_t *bcp_own;
     RC(scratch_t(c, "summa_bcp_own", (size_t)s * (nj + 1), &bcp_own));
-    std::vector<int64_t> mine(2 * s, 0);
+    std::vector<int64_t> mine(2 * s, 0), a0s((size_t)s, 0);
     for (int q = 0; q < s; q++) {
         const int64_t k0 = cut(n, s, q), k1 = cut(n, s, q + 1);
         if ((int64_t)q * pc / s == gj) {  // A-panel owner: columns K_q of my block
@@ -1760,6 +1948,7 @@ int mcl_summa_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, 
             RC(readback(c, A->col_ptr + (k0 - A->col0), sizeof(int64_t), &ab[0]));
             RC(readback(c, A->col_ptr + (k1 - A->col0), sizeof(int64_t), &ab[1]));
             mine[2 * q] = ab[1] - ab[0];
+            a0s[q] = ab[0];
         }
         if ((int64_t)q * pr / s == gi) {  // B-panel owner: rows K_q of my block
             CK(launch_rowslice_count(nj, A->col_ptr, A->row_idx, k0 - A->row0, k1 - A->row0, first,
@@ -1772,200 +1961,249 @@ int mcl_summa_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, 
                        cudaMemcpyHostToDevice, c->stream));
     NC(ncclAllGather(hdr + (int64_t)2 * s * c->rank, hdr, 2 * s, ncclInt64, c->world, c->stream));
     std::vector<int64_t> table((size_t)2 * s * pr * pc);
-    CK(cudaMemcpyAsync(table.data(), hdr, sizeof(int64_t) * table.size(), cudaMemcpyDeviceToHost,
-                       c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    RC(readback(c, hdr, sizeof(int64_t) * table.size(), table.data()));
 
-    // ---- stages: broadcast panels, local product, Alg. 2 binary merge.
-    // Pipelined: the panels of stage q+1 are prepared and broadcast on the comm stream
-    // (double-buffered) while stage q's product runs on the compute stream.
-    std::vector<int64_t> a0s((size_t)s, 0);  // A-panel offsets in my block (owner stages)
-    for (int q = 0; q < s; q++) {
-        const int64_t k0 = cut(n, s, q);
-        if ((int64_t)q * pc / s == gj) RC(readback(c, A->col_ptr + (k0 - A->col0), sizeof(int64_t), &a0s[q]));
-    }
+    // ---- every stage's panels, broadcast once on the comm stream and kept resident.  Rank
+    // (i, j) then holds A[rows_i, :] and A[:, cols_j] (nnz(A) (1/pr + 1/pc) entries), all the
+    // operands of every phase, so a phase re-runs its stage products without re-broadcasting
+    // (P:317-319 notes that cost for HipMCL's phases).  The compute stream waits for stage q's
+    // panels only when it first needs them, so the broadcasts overlap the estimation and the
+    // first phase's products.
     struct Panels {
         int64_t *acp, *bcp, *first, *cnt;
         int32_t *arow, *brow;
         float *aval, *bval;
-    } buf[2];
-    int64_t max_a = 1, max_b = 1, max_k = 1;
+        int64_t nnzA, nnzB, k0, kq;
+    };
+    std::vector<Panels> pan((size_t)s);
+    std::vector<cudaEvent_t> ready((size_t)s, nullptr);
+    struct EvGuard {
+        std::vector<cudaEvent_t> &v;
+        ~EvGuard() {
+            for (auto e : v)
+                if (e) cudaEventDestroy(e);
+        }
+    } evg{ready};
     for (int q = 0; q < s; q++) {
+        Panels &P = pan[q];
         const int ca = (int)((int64_t)q * pc / s), rb = (int)((int64_t)q * pr / s);
-        max_a = std::max(max_a, table[(size_t)2 * s * (gi * pc + ca) + 2 * q]);
-        max_b = std::max(max_b, table[(size_t)2 * s * (rb * pc + gj) + 2 * q + 1]);
-        max_k = std::max(max_k, cut(n, s, q + 1) - cut(n, s, q));
-    }
-    for (int i = 0; i < 2; i++) {
-        const std::string t = std::to_string(i);
-        RC(scratch_t(c, ("pa_cp" + t).c_str(), (size_t)max_k + 1, &buf[i].acp));
-        RC(scratch_t(c, ("pa_row" + t).c_str(), (size_t)max_a, &buf[i].arow));
-        RC(scratch_t(c, ("pa_val" + t).c_str(), (size_t)max_a, &buf[i].aval));
-        RC(scratch_t(c, ("pb_cp" + t).c_str(), (size_t)nj + 1, &buf[i].bcp));
-        RC(scratch_t(c, ("pb_row" + t).c_str(), (size_t)max_b, &buf[i].brow));
-        RC(scratch_t(c, ("pb_val" + t).c_str(), (size_t)max_b, &buf[i].bval));
-        RC(scratch_t(c, ("pb_first" + t).c_str(), (size_t)std::max<int64_t>(nj, 1), &buf[i].first));
-        RC(scratch_t(c, ("pb_cnt" + t).c_str(), (size_t)std::max<int64_t>(nj, 1), &buf[i].cnt));
+        P.k0 = cut(n, s, q);
+        P.kq = cut(n, s, q + 1) - P.k0;
+        P.nnzA = table[(size_t)2 * s * (gi * pc + ca) + 2 * q];
+        P.nnzB = table[(size_t)2 * s * (rb * pc + gj) + 2 * q + 1];
+        const std::string t = std::to_string(q);
+        RC(scratch_t(c, ("pa_cp" + t).c_str(), (size_t)P.kq + 1, &P.acp));
+        RC(scratch_t(c, ("pa_row" + t).c_str(), (size_t)std::max<int64_t>(P.nnzA, 1), &P.arow));
+        RC(scratch_t(c, ("pa_val" + t).c_str(), (size_t)std::max<int64_t>(P.nnzA, 1), &P.aval));
+        RC(scratch_t(c, ("pb_cp" + t).c_str(), (size_t)nj + 1, &P.bcp));
+        RC(scratch_t(c, ("pb_row" + t).c_str(), (size_t)std::max<int64_t>(P.nnzB, 1), &P.brow));
+        RC(scratch_t(c, ("pb_val" + t).c_str(), (size_t)std::max<int64_t>(P.nnzB, 1), &P.bval));
+        RC(scratch_t(c, ("pb_first" + t).c_str(), (size_t)std::max<int64_t>(nj, 1), &P.first));
+        RC(scratch_t(c, ("pb_cnt" + t).c_str(), (size_t)std::max<int64_t>(nj, 1), &P.cnt));
+        CK(cudaEventCreateWithFlags(&ready[q], cudaEventDisableTiming));
     }
     cudaStream_t cs = c->cstream;
     CK(cudaEventRecord(c->qev[4], c->stream));  // A, bcp_own ready
     CK(cudaStreamWaitEvent(cs, c->qev[4], 0));
-    auto issue_comm = [&](int q) -> int {
-        const int64_t k0 = cut(n, s, q), k1 = cut(n, s, q + 1), kq = k1 - k0;
+    int64_t comm_bytes = 0;
+    for (int q = 0; q < s; q++) {
+        Panels &P = pan[q];
         const int ca = (int)((int64_t)q * pc / s), rb = (int)((int64_t)q * pr / s);
-        const int64_t nnzA = table[(size_t)2 * s * (gi * pc + ca) + 2 * q];
-        const int64_t nnzB = table[(size_t)2 * s * (rb * pc + gj) + 2 * q + 1];
-        Panels &P = buf[q & 1];
-        if (q >= 2) CK(cudaStreamWaitEvent(cs, c->qev[2 + (q & 1)], 0));  // product q-2 done
         if (ca == gj) {
-            CK(launch_rebase_colptr(kq + 1, A->col_ptr + (k0 - A->col0), P.acp, cs));
-            if (nnzA) {
-                CK(cudaMemcpyAsync(P.arow, A->row_idx + a0s[q], sizeof(int32_t) * nnzA,
+            CK(launch_rebase_colptr(P.kq + 1, A->col_ptr + (P.k0 - A->col0), P.acp, cs));
+            if (P.nnzA) {
+                CK(cudaMemcpyAsync(P.arow, A->row_idx + a0s[q], sizeof(int32_t) * P.nnzA,
                                    cudaMemcpyDeviceToDevice, cs));
-                CK(cudaMemcpyAsync(P.aval, A->val + a0s[q], sizeof(float) * nnzA,
+                CK(cudaMemcpyAsync(P.aval, A->val + a0s[q], sizeof(float) * P.nnzA,
                                    cudaMemcpyDeviceToDevice, cs));
             }
+        } else {
+            comm_bytes += (P.kq + 1) * 8 + P.nnzA * 8;
         }
         if (rb == gi) {
             const int64_t *ocp = bcp_own + (int64_t)q * (nj + 1);
-            CK(launch_rowslice_count(nj, A->col_ptr, A->row_idx, k0 - A->row0, k1 - A->row0, P.first,
-                                     P.cnt, cs));
+            CK(launch_rowslice_count(nj, A->col_ptr, A->row_idx, P.k0 - A->row0, P.k0 + P.kq - A->row0,
+                                     P.first, P.cnt, cs));
             CK(cudaMemcpyAsync(P.bcp, ocp, sizeof(int64_t) * (nj + 1), cudaMemcpyDeviceToDevice, cs));
-            CK(launch_rowslice_copy(nj, P.first, P.bcp, A->row_idx, A->val, k0 - A->row0, P.brow,
+            CK(launch_rowslice_copy(nj, P.first, P.bcp, A->row_idx, A->val, P.k0 - A->row0, P.brow,
                                     P.bval, cs));
+        } else {
+            comm_bytes += (nj + 1) * 8 + P.nnzB * 8;
         }
         NC(ncclGroupStart());
-        NC(ncclBroadcast(P.acp, P.acp, kq + 1, ncclInt64, ca, c->rowc, cs));
-        if (nnzA) {
-            NC(ncclBroadcast(P.arow, P.arow, nnzA, ncclInt32, ca, c->rowc, cs));
-            NC(ncclBroadcast(P.aval, P.aval, nnzA, ncclFloat32, ca, c->rowc, cs));
+        NC(ncclBroadcast(P.acp, P.acp, P.kq + 1, ncclInt64, ca, c->rowc, cs));
+        if (P.nnzA) {
+            NC(ncclBroadcast(P.arow, P.arow, P.nnzA, ncclInt32, ca, c->rowc, cs));
+            NC(ncclBroadcast(P.aval, P.aval, P.nnzA, ncclFloat32, ca, c->rowc, cs));
         }
         NC(ncclBroadcast(P.bcp, P.bcp, nj + 1, ncclInt64, rb, c->colc, cs));
-        if (nnzB) {
-            NC(ncclBroadcast(P.brow, P.brow, nnzB, ncclInt32, rb, c->colc, cs));
-            NC(ncclBroadcast(P.bval, P.bval, nnzB, ncclFloat32, rb, c->colc, cs));
+        if (P.nnzB) {
+            NC(ncclBroadcast(P.brow, P.brow, P.nnzB, ncclInt32, rb, c->colc, cs));
+            NC(ncclBroadcast(P.bval, P.bval, P.nnzB, ncclFloat32, rb, c->colc, cs));
         }
         NC(ncclGroupEnd());
-        CK(cudaEventRecord(c->qev[q & 1], cs));  // panels of stage q ready
-        return MCL_OK;
+        CK(cudaEventRecord(ready[q], cs));
+    }
+    auto panel_a = [&](int q) {
+        mcl_csc_t Pa;
+        zero_csc(&Pa);
+        Pa.nrows = mi;
+        Pa.ncols = pan[q].kq;
+        Pa.nnz = pan[q].nnzA;
+        Pa.row0 = A->row0;
+        Pa.col0 = pan[q].k0;
+        Pa.n_global = n;
+        Pa.col_ptr = pan[q].acp;
+        Pa.row_idx = pan[q].arow;
+        Pa.val = pan[q].aval;
+        return Pa;
     };
+    auto panel_b = [&](int q) {
+        mcl_csc_t Pb;
+        zero_csc(&Pb);
+        Pb.nrows = pan[q].kq;
+        Pb.ncols = nj;
+        Pb.nnz = pan[q].nnzB;
+        Pb.row0 = pan[q].k0;
+        Pb.col0 = A->col0;
+        Pb.n_global = n;
+        Pb.col_ptr = pan[q].bcp;
+        Pb.row_idx = pan[q].brow;
+        Pb.val = pan[q].bval;
+        return Pb;
+    };
+
+    // ---- phases (Q15): the partials Alg. 2 holds for a column are
+    // estimated from Cohen's estimate of every stage product (on the resident
+    // panels), 8 B x 1.3 x sum_q est_q(j) x 2 (partials + the merge's copy) + 16 B; the
+    // estimates are all-reduced (max) over the column communicator, whose ranks split the
+    // same columns and must run the same batches for the distributed prune
+    int64_t *pbytes;
+    float *pest;
+    RC(scratch_t(c, "summa_phase_bytes", (size_t)std::max<int64_t>(nj, 1), &pbytes));
+    RC(scratch_t(c, "summa_phase_est", (size_t)std::max<int64_t>(nj, 1), &pest));
+    CK(cudaMemsetAsync(pbytes, 0, sizeof(int64_t) * std::max<int64_t>(nj, 1), c->stream));
+    for (int q = 0; q < s; q++) {
+        CK(cudaStreamWaitEvent(c->stream, ready[q], 0));
+        mcl_csc_t Pa = panel_a(q), Pb = panel_b(q);
+        RC(cohen(c, Prod{&Pa, &Pb, 0, nj}, pin->est_keys, pin->seed, pest, nullptr));
+        CK(launch_affine_est(nj, pest, 8.0 * 1.3 * 2.0, q == 0 ? 16 : 0, pbytes, c->stream));
+    }
+    if (pr > 1 && nj > 0) NC(ncclAllReduce(pbytes, pbytes, nj, ncclInt64, ncclMax, c->colc, c->stream));
+    std::vector<int64_t> bounds;
+    int64_t est_bytes = 0;
+    RC(plan_phases(c, pbytes, nj, phase_budget(c, pin->mem_safety), bounds, &est_bytes));
+    const int h = (int)bounds.size() - 1;
+
+    // ---- per phase: stage products on the phase's columns, Alg. 2 binary merge
+    // (P:509-529), distributed prune / inflate
+    std::vector<mcl_csc_t> pieces;
     std::vector<mcl_csc_t> stack;
-    int64_t comm_bytes = 0, peak_partial = 0, live_partial = 0, flops = 0;
+    int64_t peak_partial = 0, flops = 0, nnz_unpruned = 0;
+    float chaos = 0.f;
     float bin_ms[kNumBins + 1] = {};
     int64_t bin_flops[kNumBins + 1] = {}, bin_cols[kNumBins + 1] = {}, bin_nnzb[kNumBins + 1] = {},
             bin_out[kNumBins + 1] = {};
-    int rc = issue_comm(0);
-    for (int q = 0; q < s && rc == MCL_OK; q++) {
-        if (q + 1 < s && (rc = issue_comm(q + 1)) != MCL_OK) break;
-        const int64_t k0 = cut(n, s, q), k1 = cut(n, s, q + 1), kq = k1 - k0;
-        const int ca = (int)((int64_t)q * pc / s), rb = (int)((int64_t)q * pr / s);
-        const int64_t nnzA = table[(size_t)2 * s * (gi * pc + ca) + 2 * q];
-        const int64_t nnzB = table[(size_t)2 * s * (rb * pc + gj) + 2 * q + 1];
-        Panels &PB = buf[q & 1];
-        CK(cudaStreamWaitEvent(c->stream, c->qev[q & 1], 0));
-        if (ca != gj) comm_bytes += (kq + 1) * 8 + nnzA * 8;
-        if (rb != gi) comm_bytes += (nj + 1) * 8 + nnzB * 8;
-        mcl_csc_t Pa, Pb, Pq;
-        zero_csc(&Pa);
-        zero_csc(&Pb);
-        Pa.nrows = mi;
-        Pa.ncols = kq;
-        Pa.nnz = nnzA;
-        Pa.row0 = A->row0;
-        Pa.col0 = k0;
-        Pa.n_global = n;
-        Pa.col_ptr = PB.acp;
-        Pa.row_idx = PB.arow;
-        Pa.val = PB.aval;
-        Pb.nrows = kq;
-        Pb.ncols = nj;
-        Pb.nnz = nnzB;
-        Pb.row0 = k0;
-        Pb.col0 = A->col0;
-        Pb.n_global = n;
-        Pb.col_ptr = PB.bcp;
-        Pb.row_idx = PB.brow;
-        Pb.val = PB.bval;
-        mcl_stats_t sst;
-        if ((rc = spgemm_impl(c, &Pa, &Pb, 0, nj, pin, &Pq, &sst)) != MCL_OK) break;
-        CK(cudaEventRecord(c->qev[2 + (q & 1)], c->stream));  // buffer q&1 free again
-        flops += sst.flops;
-        for (int b = 0; b <= kNumBins; b++) {
-            bin_ms[b] += sst.bin_ms[b];
-            bin_flops[b] += sst.bin_flops[b];
-            bin_cols[b] += sst.bin_cols[b];
-            bin_nnzb[b] += sst.bin_nnzb[b];
-            bin_out[b] += sst.bin_out[b];
-        }
-        Pq.row0 = A->row0;
-        Pq.col0 = A->col0;
-        Pq.n_global = n;
-        stack.push_back(Pq);
-        live_partial += Pq.nnz;
-        peak_partial = std::max(peak_partial, live_partial);
-        // Alg. 2 lines 5-14: merge nmerges+1 lists when the stage count is even
-        int jj = q + 1, nmerges = 0;
-        while (jj % 2 == 0 && jj != 0) {
-            nmerges++;
-            jj /= 2;
-        }
-        if (nmerges > 0) {
-            std::vector<mcl_csc_t> L(stack.end() - (nmerges + 1), stack.end());
-            mcl_csc_t merged;
-            if ((rc = merge_impl(c, (int32_t)L.size(), L.data(), &merged)) != MCL_OK) break;
-            for (auto &x : L) {
-                live_partial -= x.nnz;
-                free_csc(c, &x);
+    int rc = MCL_OK;
+    auto drop = [&](std::vector<mcl_csc_t> &v) {
+        for (auto &x : v) free_csc(c, &x);
+        v.clear();
+    };
+    for (int ph = 0; ph < h && rc == MCL_OK; ph++) {
+        const int64_t c0 = bounds[ph], c1 = bounds[ph + 1];
+        int64_t live_partial = 0;
+        for (int q = 0; q < s && rc == MCL_OK; q++) {
+            mcl_csc_t Pa = panel_a(q), Pb = panel_b(q), Pq;
+            mcl_stats_t sst;
+            if ((rc = spgemm_impl(c, &Pa, &Pb, c0, c1, pin, &Pq, &sst)) != MCL_OK) break;
+            flops += sst.flops;
+            for (int b = 0; b <= kNumBins; b++) {
+                bin_ms[b] += sst.bin_ms[b];
+                bin_flops[b] += sst.bin_flops[b];
+                bin_cols[b] += sst.bin_cols[b];
+                bin_nnzb[b] += sst.bin_nnzb[b];
+                bin_out[b] += sst.bin_out[b];
             }
-            stack.resize(stack.size() - L.size());
-            stack.push_back(merged);
-            live_partial += merged.nnz;
+            Pq.row0 = A->row0;
+            Pq.col0 = A->col0 + c0;
+            Pq.n_global = n;
+            stack.push_back(Pq);
+            live_partial += Pq.nnz;
             peak_partial = std::max(peak_partial, live_partial);
+            // Alg. 2 lines 5-14: merge nmerges+1 lists when the stage count is even
+            int jj = q + 1, nmerges = 0;
+            while (jj % 2 == 0 && jj != 0) {
+                nmerges++;
+                jj /= 2;
+            }
+            if (nmerges > 0) {
+                std::vector<mcl_csc_t> L(stack.end() - (nmerges + 1), stack.end());
+                mcl_csc_t merged;
+                if ((rc = merge_impl(c, (int32_t)L.size(), L.data(), &merged)) != MCL_OK) break;
+                for (auto &x : L) {
+                    live_partial -= x.nnz;
+                    free_csc(c, &x);
+                }
+                stack.resize(stack.size() - L.size());
+                stack.push_back(merged);
+                live_partial += merged.nnz;
+                peak_partial = std::max(peak_partial, live_partial);
+            }
         }
-    }
-    if (rc == MCL_OK && stack.size() > 1) {  // Q16: stage counts that are not powers of two
-        mcl_csc_t merged;
-        rc = merge_impl(c, (int32_t)stack.size(), stack.data(), &merged);
-        if (rc == MCL_OK) {
-            for (auto &x : stack) free_csc(c, &x);
-            stack.assign(1, merged);
+        if (rc == MCL_OK && stack.size() > 1) {  // Q16: stage counts that are not powers of two
+            mcl_csc_t merged;
+            rc = merge_impl(c, (int32_t)stack.size(), stack.data(), &merged);
+            if (rc == MCL_OK) {
+                drop(stack);
+                stack.push_back(merged);
+            }
         }
+        if (rc != MCL_OK) break;
+        mcl_csc_t Cb = stack[0], piece;
+        stack.clear();
+        float ch = 0.f;
+        rc = dist_prune(c, &Cb, pr > 1 ? c->colc : nullptr, pp, &piece, &ch);
+        nnz_unpruned += Cb.nnz;
+        free_csc(c, &Cb);
+        if (rc != MCL_OK) break;
+        pieces.push_back(piece);
+        chaos = std::max(chaos, ch);
     }
     if (rc != MCL_OK) {
-        for (auto &x : stack) free_csc(c, &x);
+        drop(stack);
+        drop(pieces);
         return rc;
     }
-    CK(cudaEventRecord(c->sev[1], c->stream));
-    mcl_csc_t Cb = stack[0];
-    float chaos = 0.f;
     OutGuard guard(c, A_next);
-    rc = dist_prune(c, &Cb, pr > 1 ? c->colc : nullptr, pp, A_next, &chaos);
-    const int64_t nnz_unpruned = Cb.nnz;
-    free_csc(c, &Cb);
-    if (rc != MCL_OK) return rc;
+    if (h == 1) {
+        *A_next = pieces[0];
+        pieces.clear();
+    } else {
+        rc = concat_cols(c, pieces, A_next);
+        drop(pieces);
+        if (rc != MCL_OK) return rc;
+    }
+    CK(cudaEventRecord(c->sev[2], c->stream));
     float *cm;
     RC(scratch_t(c, "chaos_max", 4, &cm));
     CK(cudaMemcpyAsync(cm, &chaos, sizeof(float), cudaMemcpyHostToDevice, c->stream));
     NC(ncclAllReduce(cm, cm, 1, ncclFloat32, ncclMax, c->world, c->stream));
     RC(readback(c, cm, sizeof(float), &chaos));
-    CK(cudaEventRecord(c->sev[2], c->stream));
     if (st) {
         st->nnz_in = A->nnz;
         st->nnz_unpruned = nnz_unpruned;
         st->nnz_out = A_next->nnz;
         st->chaos = chaos;
-        st->phases = 1;
+        st->phases = h;
+        st->stages = s;
+        st->est_nnz = (double)est_bytes / (8.0 * 1.3 * 2.0);
         st->estimator_used = 1;
-        float sm3 = -1.f, sm4 = -1.f;
+        float tot = -1.f;
         cudaEventSynchronize(c->sev[2]);
-        cudaEventElapsedTime(&sm3, c->sev[0], c->sev[1]);
-        cudaEventElapsedTime(&sm4, c->sev[1], c->sev[2]);
-        cudaGetLastError();
-        st->ms[3] = sm3;  // stages: broadcasts + products + Alg. 2 merges
-        st->ms[4] = sm4;  // distributed prune + inflate
-        st->ms[6] = sm3 + sm4;
+        if (cudaEventElapsedTime(&tot, c->sev[0], c->sev[2]) != cudaSuccess) cudaGetLastError();
+        st->ms[6] = tot;
         float pm[4];
-        for (int q = 0; q < 4; q++) {
+        for (int q = 0; q < 4; q++) {  // the last phase's distributed prune
             pm[q] = 0.f;
             if (cudaEventElapsedTime(&pm[q], c->pev[q], c->pev[q + 1]) != cudaSuccess) {
                 cudaGetLastError();

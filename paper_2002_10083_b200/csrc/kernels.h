@@ -138,6 +138,12 @@ cudaError_t launch_rowpart(int64_t ncols, const int64_t *cp, const int32_t *row,
                            int *rowpart, cudaStream_t s, int nparts = 32);
 
 // misc kernels (kernels_misc.cu)
+// phase planner (capi.cu plan_phases): per-column byte estimates and the batch cuts
+cudaError_t launch_affine_i64(int64_t n, const int64_t *x, int64_t a, int64_t b, int64_t *bytes,
+                              bool accumulate, cudaStream_t s);
+cudaError_t launch_affine_est(int64_t n, const float *est, double a, int64_t b, int64_t *bytes,
+                              cudaStream_t s);
+cudaError_t launch_phase_cuts(const int64_t *prefix, int64_t n, int h, int64_t *cut, cudaStream_t s);
 // apair[q] = (row[q], bits of val[q]): the interleaved copy of A the private family gathers
 cudaError_t launch_pack_pairs(int64_t nnz, const int32_t *row, const float *val, int2 *apair,
                               cudaStream_t s);

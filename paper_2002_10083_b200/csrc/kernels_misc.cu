@@ -80,6 +80,61 @@ cudaError_t launch_pack_pairs(int64_t nnz, const int32_t *row, const float *val,
     return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ phase planner helpers
+// bytes[j] (+)= a * x[j] + b for an int64 x (accumulate = add to bytes, else overwrite)
+__global__ void k_affine_i64(int64_t n, const int64_t *x, int64_t a, int64_t b, int64_t *bytes,
+                             int accumulate) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+         j += (int64_t)gridDim.x * blockDim.x)
+        bytes[j] = (accumulate ? bytes[j] : 0) + a * x[j] + b;
+}
+// bytes[j] += ceil(a * est[j]) + b for a Cohen estimate est (fp32)
+__global__ void k_affine_est(int64_t n, const float *est, double a, int64_t b, int64_t *bytes) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+         j += (int64_t)gridDim.x * blockDim.x)
+        bytes[j] += (int64_t)ceil(a * (double)est[j]) + b;
+}
+// cut[k-1] = first j with prefix[j] >= k * total / h, k = 1 .. h-1 (prefix: exclusive scan,
+// [n+1]); the batches [cut[k-1], cut[k]) then hold near-equal shares of the bytes
+__global__ void k_phase_cuts(const int64_t *prefix, int64_t n, int h, int64_t *cut) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x + 1;
+    if (k >= h) return;
+    const int64_t total = prefix[n];
+    const int64_t want = (int64_t)((__int128)total * k / h);
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (prefix[mid] < want) lo = mid + 1;
+        else hi = mid;
+    }
+    cut[k - 1] = lo;
+}
+
+cudaError_t launch_affine_i64(int64_t n, const int64_t *x, int64_t a, int64_t b, int64_t *bytes,
+                              bool accumulate, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > g_sms * 16) blocks = g_sms * 16;
+    ++g_launches;
+    k_affine_i64<<<(int)blocks, 256, 0, s>>>(n, x, a, b, bytes, accumulate ? 1 : 0);
+    return cudaGetLastError();
+}
+cudaError_t launch_affine_est(int64_t n, const float *est, double a, int64_t b, int64_t *bytes,
+                              cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > g_sms * 16) blocks = g_sms * 16;
+    ++g_launches;
+    k_affine_est<<<(int)blocks, 256, 0, s>>>(n, est, a, b, bytes);
+    return cudaGetLastError();
+}
+cudaError_t launch_phase_cuts(const int64_t *prefix, int64_t n, int h, int64_t *cut, cudaStream_t s) {
+    if (h <= 1) return cudaSuccess;
+    ++g_launches;
+    k_phase_cuts<<<(h + 255) / 256, 256, 0, s>>>(prefix, n, h, cut);
+    return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ CSC validation
 // MCLX_VALIDATE=1 (include/mclx.h MCL_ERR_FORMAT): the CSC invariants of the header --
 // col_ptr[0] = 0, non-decreasing, col_ptr[n] = nnz; rows in [0, nrows) and strictly
