@@ -252,6 +252,32 @@ int mcl_ctx_set_grid(mcl_ctx_t ctx, int pr, int pc, int rank, const unsigned cha
 int mcl_summa_iterate(mcl_ctx_t ctx, const mcl_csc_t *A, const mcl_params_t *p, mcl_csc_t *A_next,
                       mcl_stats_t *st);
 
+/* ------------------------------------------------------------------ I/O around the kernel
+ * Host-side (no CUDA) ingestion of a weighted graph and the cluster output file (SURVEY §8(f)
+ * row 4; SPEC S:547-559 load_graph / run).  All arrays are HOST memory owned by the struct. */
+typedef struct {
+    int64_t n, nnz;
+    int64_t *col_ptr;  /* host [n+1]                                                       */
+    int32_t *row_idx;  /* host [nnz], strictly increasing inside each column               */
+    float *val;        /* host [nnz], > 0                                                   */
+    char **labels;     /* host [n] vertex labels of a TSV input, NULL for MatrixMarket     */
+} mcl_graph_t;
+
+/* Read a graph: MatrixMarket coordinate (real / integer / pattern -> 1.0, general /
+ * symmetric, 1-based) or a labelled edge list "src dst [weight]" (TSV or spaces; labels get
+ * dense ids in order of first appearance; column = src, row = dst).  Duplicates are summed,
+ * exact zeros dropped; symmetrize != 0 returns max(A, A^T).  On error g is zeroed, err
+ * (optional, errlen bytes) names the file and line: MCL_ERR_FORMAT (malformed line, negative
+ * weight, symmetric-marker violation, entry count), MCL_ERR_DIM (non-square), MCL_ERR_OOM,
+ * MCL_ERR_INVALID_ARG (unreadable file). */
+int mcl_graph_read(const char *path, int symmetrize, mcl_graph_t *g, char *err, size_t errlen);
+void mcl_graph_free(mcl_graph_t *g);
+/* Write the clusters of `labels` (host int32 [n], cluster ids 0..k-1 as mcl_clusters numbers
+ * them, i.e. by smallest member): one line per cluster, its members in ascending vertex order
+ * separated by single spaces -- the graph's labels, or 1-based vertex ids (g NULL or without
+ * labels). */
+int mcl_clusters_write(const char *path, const int32_t *labels, int64_t n, const mcl_graph_t *g);
+
 #ifdef __cplusplus
 }
 #endif

@@ -82,6 +82,12 @@ class StatsT(C.Structure):
         return d
 
 
+class GraphT(C.Structure):
+    _fields_ = [("n", C.c_int64), ("nnz", C.c_int64), ("col_ptr", C.POINTER(C.c_int64)),
+                ("row_idx", C.POINTER(C.c_int32)), ("val", C.POINTER(C.c_float)),
+                ("labels", C.POINTER(C.c_char_p))]
+
+
 ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
 FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
 
@@ -118,6 +124,9 @@ _sig = {
     "mcl_ctx_set_grid": ([_P, C.c_int, C.c_int, C.c_int, C.c_char * 128], C.c_int),
     "mcl_summa_iterate": ([_P, C.POINTER(CscT), C.POINTER(ParamsT), C.POINTER(CscT),
                            C.POINTER(StatsT)], C.c_int),
+    "mcl_graph_read": ([C.c_char_p, C.c_int, C.POINTER(GraphT), C.c_char_p, C.c_size_t], C.c_int),
+    "mcl_graph_free": ([C.POINTER(GraphT)], None),
+    "mcl_clusters_write": ([C.c_char_p, _P, _i64, C.POINTER(GraphT)], C.c_int),
 }
 for _name, (_args, _res) in _sig.items():
     _f = getattr(_lib, _name)
@@ -468,3 +477,55 @@ def nccl_unique_id() -> bytes:
 
 def run(G, params=None, max_iter=100, callback=None):
     return context().run(G, params, max_iter, callback)
+
+
+@dataclass
+class HostGraph:
+    """A graph read by mcl_graph_read: host CSC arrays (numpy) and optional vertex labels."""
+    nrows: int
+    ncols: int
+    colptr: np.ndarray
+    rows: np.ndarray
+    vals: np.ndarray
+    labels: list | None = None
+
+    @property
+    def nnz(self) -> int:
+        return int(self.rows.size)
+
+
+def read_graph(path: str, symmetrize: bool = True) -> HostGraph:
+    """MatrixMarket coordinate or a labelled 'src dst [weight]' edge list -> HostGraph
+    (host-side native parser in libmclx.so; no GPU needed).  Raises MclError on bad input."""
+    g = GraphT()
+    err = C.create_string_buffer(512)
+    rc = _lib.mcl_graph_read(os.fsencode(path), int(symmetrize), C.byref(g), err, 512)
+    if rc != MCL_OK:
+        raise MclError(rc, err.value.decode())
+    try:
+        n, nnz = int(g.n), int(g.nnz)
+        cp = np.ctypeslib.as_array(g.col_ptr, shape=(n + 1,)).copy()
+        rows = np.ctypeslib.as_array(g.row_idx, shape=(max(nnz, 1),))[:nnz].copy()
+        vals = np.ctypeslib.as_array(g.val, shape=(max(nnz, 1),))[:nnz].copy()
+        labels = [g.labels[i].decode() for i in range(n)] if g.labels else None
+    finally:
+        _lib.mcl_graph_free(C.byref(g))
+    return HostGraph(n, n, cp, rows, vals, labels)
+
+
+def write_clusters(path: str, labels, graph: HostGraph | None = None) -> None:
+    """One line per cluster (members by ascending vertex, space-separated graph labels or
+    1-based ids), clusters in label order (mcl_clusters numbers them by smallest member)."""
+    lab = labels.cpu().numpy() if isinstance(labels, torch.Tensor) else np.asarray(labels)
+    lab = np.ascontiguousarray(lab, np.int32)
+    g = None
+    keep = None
+    if graph is not None and graph.labels is not None:
+        g = GraphT()
+        g.n = len(graph.labels)
+        keep = (C.c_char_p * len(graph.labels))(*[x.encode() for x in graph.labels])
+        g.labels = C.cast(keep, C.POINTER(C.c_char_p))
+    rc = _lib.mcl_clusters_write(os.fsencode(path), lab.ctypes.data_as(C.c_void_p), lab.size,
+                                 C.byref(g) if g is not None else None)
+    if rc != MCL_OK:
+        raise MclError(rc, f"cannot write clusters to {path}")

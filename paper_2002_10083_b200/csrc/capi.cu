@@ -34,7 +34,11 @@ struct mcl_ctx {
     std::unordered_map<std::string, Buf> scratch;
     size_t cur = 0, peak = 0;
     int occ[3][kAllBins] = {};
-    void *pin = nullptr;  // pinned host staging for small read-backs
+    void *pin = nullptr;     // mapped pinned read-back buffer (readback)
+    size_t pin_bytes = 0;
+    void *pin_up = nullptr;  // mapped pinned upload buffer (upload)
+    size_t pin_up_bytes = 0;
+    cudaEvent_t up_ev = nullptr;
     cudaEvent_t ev[8] = {};
     cudaEvent_t bev[2 * kAllBins] = {};
     cudaEvent_t pev[6] = {};  // phases of the distributed prune
@@ -135,26 +139,70 @@ int scratch_t(mcl_ctx *c, const char *name, size_t count, T **out) {
     return scratch(c, name, count * sizeof(T), (void **)out);
 }
 
-// Small read-backs are stored by a one-CTA kernel straight into the pinned buffer (mapped
-// under UVA) instead of a D2H memcpy: copy-engine work is served in order, so a memcpy here
-// would wait behind a caller's large D2H on another stream (the e2e bench's result read-back
-// of the previous step) and stall the iteration at each of its host syncs.
-constexpr size_t kPinBytes = 65536;  // mapped pinned read-back buffer
+// Host <-> device transfers of the orchestration (sizes, work lists, plans) go through
+// mapped pinned buffers copied by KERNELS, not cudaMemcpy: copy-engine work is served in
+// order, so a memcpy here would queue behind a caller's large transfer on another stream (the
+// e2e bench's result read-back of the previous step / input upload of the next) and stall the
+// iteration at each of its host syncs.  The buffers grow on demand.
+constexpr size_t kPinBytes = 65536;  // initial size of each mapped pinned buffer
 
-__global__ void k_readback(const unsigned char *__restrict__ src, unsigned char *dst, size_t n) {
-    for (size_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+__global__ void k_copy_bytes(const unsigned char *__restrict__ src, unsigned char *__restrict__ dst,
+                             size_t n) {
+    const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (size_t)gridDim.x * blockDim.x;
+    if ((((uintptr_t)src | (uintptr_t)dst) & 15) == 0) {
+        const size_t n16 = n >> 4;
+        for (size_t i = t; i < n16; i += nt)
+            reinterpret_cast<uint4 *>(dst)[i] = reinterpret_cast<const uint4 *>(src)[i];
+        for (size_t i = (n16 << 4) + t; i < n; i += nt) dst[i] = src[i];
+    } else {
+        for (size_t i = t; i < n; i += nt) dst[i] = src[i];
+    }
 }
 
-// Copy `bytes` (<= kPinBytes) from device to the pinned buffer and wait for the stream.
+void launch_copy_bytes(const void *src, void *dst, size_t n, cudaStream_t s) {
+    const size_t blocks = std::min<size_t>(std::max<size_t>((n + 4095) / 4096, 1), 256);
+    ++g_launches;
+    k_copy_bytes<<<(unsigned)blocks, 256, 0, s>>>((const unsigned char *)src, (unsigned char *)dst, n);
+}
+
+// grow a mapped pinned buffer to >= bytes (its contents are not kept)
+int ensure_pin(mcl_ctx *c, void **buf, size_t *cap, size_t bytes) {
+    if (*cap >= bytes) return MCL_OK;
+    if (*buf) cudaFreeHost(*buf);
+    *buf = nullptr;
+    *cap = 0;
+    const size_t nb = std::max(bytes + bytes / 2, kPinBytes);
+    if (cudaHostAlloc(buf, nb, cudaHostAllocMapped) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(c, MCL_ERR_OOM, "cannot allocate %zu bytes of pinned host memory", nb);
+    }
+    *cap = nb;
+    return MCL_OK;
+}
+
+// Copy `bytes` from device to host through the mapped read-back buffer; waits for the stream.
 int readback(mcl_ctx *c, const void *dev, size_t bytes, void *host) {
-    if (bytes > kPinBytes) return fail(c, MCL_ERR_INVALID_ARG, "readback: %zu bytes > %zu", bytes, kPinBytes);
     if (bytes == 0) return MCL_OK;
     if (!dev) return fail(c, MCL_ERR_INVALID_ARG, "readback from a NULL device pointer");
-    ++g_launches;
-    k_readback<<<1, 256, 0, c->stream>>>((const unsigned char *)dev, (unsigned char *)c->pin, bytes);
+    RC(ensure_pin(c, &c->pin, &c->pin_bytes, bytes));
+    launch_copy_bytes(dev, c->pin, bytes, c->stream);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(c->stream));
     memcpy(host, c->pin, bytes);
+    return MCL_OK;
+}
+
+// Copy `bytes` from host to device through the mapped upload buffer, stream-ordered (the
+// host buffer may be reused at return; the upload buffer is reused after its copy ran).
+int upload(mcl_ctx *c, const void *host, size_t bytes, void *dev) {
+    if (bytes == 0) return MCL_OK;
+    if (!dev) return fail(c, MCL_ERR_INVALID_ARG, "upload to a NULL device pointer");
+    CK(cudaEventSynchronize(c->up_ev));  // the previous upload's copy has read the buffer
+    RC(ensure_pin(c, &c->pin_up, &c->pin_up_bytes, bytes));
+    memcpy(c->pin_up, host, bytes);
+    launch_copy_bytes(c->pin_up, dev, bytes, c->stream);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(c->up_ev, c->stream));
     return MCL_OK;
 }
 
@@ -295,12 +343,18 @@ int cohen(mcl_ctx *c, const Prod &pr, int r, uint64_t seed, float *est, float *k
 int run_split(mcl_ctx *c, const Prod &pr, int nsplit, int32_t *split_list,
               const int32_t *split_P, BinArgs a, unsigned long long *out_count,
               int64_t *nitems_out, mcl_stats_t *st) {
-    std::vector<int32_t> hl((size_t)nsplit), hP((size_t)pr.n);
-    CK(cudaMemcpyAsync(hl.data(), split_list, sizeof(int32_t) * nsplit, cudaMemcpyDeviceToHost,
-                       c->stream));
-    CK(cudaMemcpyAsync(hP.data(), split_P, sizeof(int32_t) * pr.n, cudaMemcpyDeviceToHost,
-                       c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    // the split columns and their part counts (gathered on the device: nsplit entries, not n)
+    std::vector<int32_t> hl((size_t)nsplit), hPl((size_t)nsplit);
+    {
+        int32_t *pl;
+        RC(scratch_t(c, "split_Pl", (size_t)nsplit, &pl));
+        CK(launch_gather_i32(nsplit, split_list, split_P, pl, c->stream));
+        RC(readback(c, split_list, sizeof(int32_t) * nsplit, hl.data()));
+        RC(readback(c, pl, sizeof(int32_t) * nsplit, hPl.data()));
+    }
+    std::unordered_map<int32_t, int32_t> hP;
+    hP.reserve((size_t)nsplit * 2);
+    for (int s2 = 0; s2 < nsplit; s2++) hP[hl[s2]] = hPl[s2];
     // variant by the virtual part count P (parts sized for T = split_part_need distinct
     // rows): <= 32 parts of kPartCap slots; 64: 32 parts of 2 kPartCap slots; more
     // (outputs dense in a sizable share of the rows, or long fp64 sums): kDenseParts row
@@ -406,14 +460,10 @@ int run_split(mcl_ctx *c, const Prod &pr, int nsplit, int32_t *split_list,
     RC(scratch(c, "split_scan_tmp", scan_tmp_bytes(chunk_items + 1), &tmp));
     std::vector<int> hcnt((size_t)2 * nchunks, 0);
     for (int q = 0; q < nchunks; q++) hcnt[q] = (int)(hoff[cuts[q + 1]] - hoff[cuts[q]]);
-    CK(cudaMemcpyAsync(split_list, hl.data(), sizeof(int32_t) * nsplit, cudaMemcpyHostToDevice,
-                       c->stream));
-    CK(cudaMemcpyAsync(ioff, hoff.data(), sizeof(int64_t) * (nsplit + 1), cudaMemcpyHostToDevice,
-                       c->stream));
-    CK(cudaMemcpyAsync(stg_off, hstg.data(), sizeof(int64_t) * (nitems + 1), cudaMemcpyHostToDevice,
-                       c->stream));
-    CK(cudaMemcpyAsync(ccount, hcnt.data(), sizeof(int) * 2 * nchunks, cudaMemcpyHostToDevice,
-                       c->stream));
+    RC(upload(c, hl.data(), sizeof(int32_t) * nsplit, split_list));
+    RC(upload(c, hoff.data(), sizeof(int64_t) * (nsplit + 1), ioff));
+    RC(upload(c, hstg.data(), sizeof(int64_t) * (nitems + 1), stg_off));
+    RC(upload(c, hcnt.data(), sizeof(int) * 2 * nchunks, ccount));
     CK(launch_split_items(nsplit, split_list, split_P, ioff, item_col, item_pr, c->stream));
     bool any_private = false;
     for (int s2 = 0; s2 < nsplit && !any_private; s2++) any_private = variant_of(hP[hl[s2]]) == 4;
@@ -668,24 +718,24 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
                 RC(scratch(c, "scan_tmp", scan_tmp_bytes(hc[b]), &tmp));
                 {   // largest columns first (LPT): homogeneous chunks, hubs start first
                     std::vector<int32_t> hl((size_t)hc[b]);
-                    std::vector<int64_t> hfl((size_t)pr.n);
-                    CK(cudaMemcpyAsync(hl.data(), a.list, sizeof(int32_t) * hc[b],
-                                       cudaMemcpyDeviceToHost, c->stream));
-                    CK(cudaMemcpyAsync(hfl.data(), f, sizeof(int64_t) * pr.n, cudaMemcpyDeviceToHost,
-                                       c->stream));
-                    CK(cudaStreamSynchronize(c->stream));
-                    std::stable_sort(hl.begin(), hl.end(),
-                                     [&](int32_t x, int32_t y) { return hfl[x] > hfl[y]; });
-                    CK(cudaMemcpyAsync(const_cast<int32_t *>(a.list), hl.data(),
-                                       sizeof(int32_t) * hc[b], cudaMemcpyHostToDevice, c->stream));
-                    CK(cudaStreamSynchronize(c->stream));
+                    std::vector<int64_t> hfl((size_t)hc[b]);
+                    int64_t *gf;
+                    RC(scratch_t(c, "gbin_flops", (size_t)hc[b], &gf));
+                    CK(launch_gather_i64(hc[b], a.list, f, gf, c->stream));
+                    RC(readback(c, a.list, sizeof(int32_t) * hc[b], hl.data()));
+                    RC(readback(c, gf, sizeof(int64_t) * hc[b], hfl.data()));
+                    std::vector<int> ord((size_t)hc[b]);
+                    for (int i = 0; i < hc[b]; i++) ord[i] = i;
+                    std::stable_sort(ord.begin(), ord.end(),
+                                     [&](int x, int y) { return hfl[x] > hfl[y]; });
+                    std::vector<int32_t> sl((size_t)hc[b]);
+                    for (int i = 0; i < hc[b]; i++) sl[i] = hl[ord[i]];
+                    RC(upload(c, sl.data(), sizeof(int32_t) * hc[b], const_cast<int32_t *>(a.list)));
                 }
                 CK(launch_global_layout(hc[b], a.list, gcap_col, gcap, gcap64, c->stream));
                 CK(launch_scan_i64(gcap64, goff, hc[b], tmp, c->stream));
                 std::vector<int64_t> hoff((size_t)hc[b] + 1);
-                CK(cudaMemcpyAsync(hoff.data(), goff, sizeof(int64_t) * (hc[b] + 1),
-                                   cudaMemcpyDeviceToHost, c->stream));
-                CK(cudaStreamSynchronize(c->stream));
+                RC(readback(c, goff, sizeof(int64_t) * (hc[b] + 1), hoff.data()));
                 const int64_t slots_budget = std::max<int64_t>(c->gbin_budget / 12, 1 << 20);
                 CK(cudaEventRecord(c->bev[2 * b], c->stream));
                 for (int i0 = 0; i0 < hc[b];) {
@@ -697,8 +747,7 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
                     RC(scratch_t(c, "gkeys", (size_t)chunk, &gkeys));
                     RC(scratch_t(c, "gvals", (size_t)chunk, &gvals));
                     const int cnt_chunk = i1 - i0;
-                    CK(cudaMemcpyAsync(gcount, &cnt_chunk, sizeof(int), cudaMemcpyHostToDevice,
-                                       c->stream));
+                    RC(upload(c, &cnt_chunk, sizeof(int), gcount));
                     CK(cudaMemsetAsync(gcount + 1, 0, sizeof(int), c->stream));
                     BinArgs ag = a;
                     ag.list = a.list + i0;
@@ -1288,8 +1337,10 @@ int mcl_ctx_create(mcl_ctx_t *out, int device, void *stream, mcl_alloc_fn alloc,
     if (const char *e = getenv("MCLX_SPLIT_CAND")) c->split_cand = atoi(e) != 0;
     if (const char *e = getenv("MCLX_PHASES")) c->force_phases = atoi(e);
     if (const char *e = getenv("MCLX_PHASE_BUDGET_MB")) c->phase_budget = (int64_t)atoll(e) << 20;
-    if (cudaMallocHost(&c->pin, kPinBytes) != cudaSuccess) {
-        delete c;
+    if (ensure_pin(c, &c->pin, &c->pin_bytes, kPinBytes) != MCL_OK ||
+        ensure_pin(c, &c->pin_up, &c->pin_up_bytes, kPinBytes) != MCL_OK ||
+        cudaEventCreateWithFlags(&c->up_ev, cudaEventDisableTiming) != cudaSuccess) {
+        mcl_ctx_destroy(c);
         return MCL_ERR_CUDA;
     }
     for (int i = 0; i < 8; i++) cudaEventCreate(&c->ev[i]);
@@ -1337,6 +1388,8 @@ int mcl_ctx_destroy(mcl_ctx_t c) {
         if (c->qev[i]) cudaEventDestroy(c->qev[i]);
     if (c->cstream) cudaStreamDestroy(c->cstream);
     if (c->pin) cudaFreeHost(c->pin);
+    if (c->pin_up) cudaFreeHost(c->pin_up);
+    if (c->up_ev) cudaEventDestroy(c->up_ev);
     delete c;
     return MCL_OK;
 }
@@ -1840,11 +1893,10 @@ int mcl_summa_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, 
         int64_t *szd;
         RC(scratch_t(c, "summa_sz", (size_t)P, &szd));
         const int64_t my = A->nnz;
-        CK(cudaMemcpyAsync(szd + c->rank, &my, sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
+        RC(upload(c, &my, sizeof(int64_t), szd + c->rank));
         NC(ncclAllGather(szd + c->rank, szd, 1, ncclInt64, c->world, c->stream));
         std::vector<int64_t> sz(P), off(P + 1, 0);
-        CK(cudaMemcpyAsync(sz.data(), szd, sizeof(int64_t) * P, cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaStreamSynchronize(c->stream));
+        RC(readback(c, szd, sizeof(int64_t) * P, sz.data()));
         for (int r = 0; r < P; r++) off[r + 1] = off[r] + sz[r];
         const int64_t tot = off[P];
         int64_t *fcp, *cps;
@@ -1910,7 +1962,7 @@ int mcl_summa_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, 
         float chaos = st ? st->chaos : 0.f;
         float *cm;
         RC(scratch_t(c, "chaos_max", 4, &cm));
-        CK(cudaMemcpyAsync(cm, &chaos, sizeof(float), cudaMemcpyHostToDevice, c->stream));
+        RC(upload(c, &chaos, sizeof(float), cm));
         NC(ncclAllReduce(cm, cm, 1, ncclFloat32, ncclMax, c->world, c->stream));
         RC(readback(c, cm, sizeof(float), &chaos));
         if (st) {
@@ -1957,8 +2009,7 @@ int mcl_summa_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, 
             RC(readback(c, bcp_own + (int64_t)q * (nj + 1) + nj, sizeof(int64_t), &mine[2 * q + 1]));
         }
     }
-    CK(cudaMemcpyAsync(hdr + (int64_t)2 * s * c->rank, mine.data(), sizeof(int64_t) * 2 * s,
-                       cudaMemcpyHostToDevice, c->stream));
+    RC(upload(c, mine.data(), sizeof(int64_t) * 2 * s, hdr + (int64_t)2 * s * c->rank));
     NC(ncclAllGather(hdr + (int64_t)2 * s * c->rank, hdr, 2 * s, ncclInt64, c->world, c->stream));
     std::vector<int64_t> table((size_t)2 * s * pr * pc);
     RC(readback(c, hdr, sizeof(int64_t) * table.size(), table.data()));
@@ -2186,7 +2237,7 @@ int mcl_summa_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, 
     CK(cudaEventRecord(c->sev[2], c->stream));
     float *cm;
     RC(scratch_t(c, "chaos_max", 4, &cm));
-    CK(cudaMemcpyAsync(cm, &chaos, sizeof(float), cudaMemcpyHostToDevice, c->stream));
+    RC(upload(c, &chaos, sizeof(float), cm));
     NC(ncclAllReduce(cm, cm, 1, ncclFloat32, ncclMax, c->world, c->stream));
     RC(readback(c, cm, sizeof(float), &chaos));
     if (st) {

@@ -138,6 +138,11 @@ cudaError_t launch_rowpart(int64_t ncols, const int64_t *cp, const int32_t *row,
                            int *rowpart, cudaStream_t s, int nparts = 32);
 
 // misc kernels (kernels_misc.cu)
+// dst[i] = src[idx[i]]
+cudaError_t launch_gather_i32(int64_t n, const int32_t *idx, const int32_t *src, int32_t *dst,
+                              cudaStream_t s);
+cudaError_t launch_gather_i64(int64_t n, const int32_t *idx, const int64_t *src, int64_t *dst,
+                              cudaStream_t s);
 // phase planner (capi.cu plan_phases): per-column byte estimates and the batch cuts
 cudaError_t launch_affine_i64(int64_t n, const int64_t *x, int64_t a, int64_t b, int64_t *bytes,
                               bool accumulate, cudaStream_t s);

@@ -135,6 +135,35 @@ cudaError_t launch_phase_cuts(const int64_t *prefix, int64_t n, int h, int64_t *
     return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ gathers for host plans
+// dst[i] = src[idx[i]] (the split path's part counts / the global bin's flops per listed
+// column: read back instead of whole n-length arrays)
+template <typename T>
+__global__ void k_gather(int64_t n, const int32_t *__restrict__ idx, const T *__restrict__ src,
+                         T *__restrict__ dst) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[idx[i]];
+}
+cudaError_t launch_gather_i32(int64_t n, const int32_t *idx, const int32_t *src, int32_t *dst,
+                              cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    int64_t b = (n + 255) / 256;
+    if (b > g_sms * 16) b = g_sms * 16;
+    ++g_launches;
+    k_gather<int32_t><<<(int)b, 256, 0, s>>>(n, idx, src, dst);
+    return cudaGetLastError();
+}
+cudaError_t launch_gather_i64(int64_t n, const int32_t *idx, const int64_t *src, int64_t *dst,
+                              cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    int64_t b = (n + 255) / 256;
+    if (b > g_sms * 16) b = g_sms * 16;
+    ++g_launches;
+    k_gather<int64_t><<<(int)b, 256, 0, s>>>(n, idx, src, dst);
+    return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ CSC validation
 // MCLX_VALIDATE=1 (include/mclx.h MCL_ERR_FORMAT): the CSC invariants of the header --
 // col_ptr[0] = 0, non-decreasing, col_ptr[n] = nnz; rows in [0, nrows) and strictly
