@@ -503,6 +503,9 @@ def run_gpu(args):
                                  "variant_ms": s0["split_vms"],
                                  "variants": ["hashed 8192-slot parts", "hashed 16384-slot parts",
                                               "dense row tiles"]},
+                       "esc": {"cols": int(s0["esc_cols"]), "flops": int(s0["esc_flops"]),
+                               "ms": s0["esc_ms"]},
+                       "phases": int(s0["phases"]),
                        "step_ms_min": min(step_ms), "step_ms_max": max(step_ms)},
             "roofline": roof,
             "cpu_baseline": cpu,

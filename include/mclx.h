@@ -129,6 +129,11 @@ typedef struct {
                                 16384-slot shared tables, fp64 global tables                    */
     float split_vms[3];      /* device time per part variant (parts + stitch + prune)           */
     int32_t stages;          /* SUMMA inner panels (stage products per phase), 0 if none        */
+    int64_t esc_cols;        /* low-cf columns run by expand-sort-compress (env MCLX_ESC_CF = the
+                                cf threshold, default 1.5; 0 turns it off), not in bin_*       */
+    int64_t esc_flops;
+    int64_t esc_out;         /* entries the ESC kernel wrote (fused: kept entries)             */
+    float esc_ms;            /* its device time                                                */
 } mcl_stats_t;
 
 /* Allocator callbacks: device memory, stream-ordered.  NULL callbacks select the

@@ -72,7 +72,8 @@ class StatsT(C.Structure):
                 ("peak_partial", C.c_int64), ("split_cols", C.c_int64),
                 ("split_items", C.c_int64), ("split_ms", C.c_float),
                 ("split_vcols", C.c_int64 * 3), ("split_vms", C.c_float * 3),
-                ("stages", C.c_int32)]
+                ("stages", C.c_int32), ("esc_cols", C.c_int64), ("esc_flops", C.c_int64),
+                ("esc_out", C.c_int64), ("esc_ms", C.c_float)]
 
     def as_dict(self) -> dict:
         d = {k: getattr(self, k) for k, _ in self._fields_}

@@ -10,8 +10,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libmclx.so")
-SOURCES = ["kernels_spgemm.cu", "kernels_dense.cu", "kernels_misc.cu", "kernels_summa.cu", "capi.cu",
-           "io.cc"]
+SOURCES = ["kernels_spgemm.cu", "kernels_dense.cu", "kernels_esc.cu", "kernels_misc.cu",
+           "kernels_summa.cu", "capi.cu", "io.cc"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 EXTRA = os.environ.get("MCLX_NVCC_EXTRA", "").split()
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

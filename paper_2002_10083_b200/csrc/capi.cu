@@ -64,6 +64,7 @@ struct mcl_ctx {
     bool split_private = true;                // MCLX_SPLIT_PRIVATE=0: P <= 4 parts shared-table too
     bool validate = false;                    // MCLX_VALIDATE=1: check input CSC invariants
     bool split_cand = true;                   // MCLX_SPLIT_CAND=0: split parts stage every entry
+    double esc_cf = 1.5;                      // MCLX_ESC_CF: cf below which a small column runs ESC (0: off)
     int force_phases = 0;                     // MCLX_PHASES=h forces h column batches (tests)
     int64_t phase_budget = -1;                // MCLX_PHASE_BUDGET_MB: bytes per batch (else
                                               // mem_safety x free HBM)
@@ -542,8 +543,14 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
     counters = counts + NB1;
     retry_count = counters + NB1;
     err = retry_count + 1;
-    RC(scratch_t(c, "bin_flops", 3 * NB1, &bflops));
+    RC(scratch_t(c, "bin_flops", 3 * NB1 + 2, &bflops));
     unsigned long long *bnnzb = bflops + NB1, *bout = bflops + 2 * NB1;
+    // low-cf columns: expand-sort-compress list (kernels_esc.cu), round 0 only
+    unsigned long long *esc_flops = bflops + 3 * NB1, *esc_out = esc_flops + 1;
+    int *esc_count = counts + 2 * NB1 + 2, *esc_counter = esc_count + 1;
+    int32_t *esc_list = nullptr;
+    const bool use_esc = c->esc_cf > 0.0 && mode != kPart;
+    if (use_esc) RC(scratch_t(c, "esc_list", (size_t)std::max<int64_t>(n, 1), &esc_list));
     RC(scratch_t(c, "bin_lists", (size_t)NB1 * std::max<int64_t>(n, 1), &lists));
     RC(scratch_t(c, "gcap_col", (size_t)std::max<int64_t>(n, 1), &gcap_col));
     RC(scratch_t(c, "retry_list", (size_t)std::max<int64_t>(n, 1), &retry_list));
@@ -598,7 +605,8 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
     const int nrounds = 3;
     for (int round = 0; round < nrounds; round++) {
         CK(cudaMemsetAsync(counts, 0, sizeof(int) * (2 * NB1 + 1), c->stream));
-        CK(cudaMemsetAsync(bflops, 0, sizeof(unsigned long long) * 3 * NB1, c->stream));
+        CK(cudaMemsetAsync(esc_count, 0, sizeof(int) * 2, c->stream));
+        CK(cudaMemsetAsync(bflops, 0, sizeof(unsigned long long) * (3 * NB1 + 2), c->stream));
         ClassifyArgs ca;
         memset(&ca, 0, sizeof ca);
         ca.n = ncls;
@@ -623,6 +631,13 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
         ca.bin_nnzb = bnnzb;
         ca.colbin = colbin;
         ca.fp64_terms = c->fp64_terms;
+        if (use_esc && round == 0) {
+            ca.esc_max = kEscCap;
+            ca.esc_cf = c->esc_cf;
+            ca.esc_count = esc_count;
+            ca.esc_list = esc_list;
+            ca.esc_flops = esc_flops;
+        }
         if (use_split && round < 2) {
             // the exact round stays in the global bin, which cannot overflow
             ca.split_max = INT64_MAX;  // the global-table variant takes any size
@@ -641,8 +656,9 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
         int hc[2 * kAllBins + 1];
         unsigned long long hf[3 * kAllBins];
         RC(readback(c, counts, sizeof(int) * NB1, hc));
-        int nsplit = 0;
+        int nsplit = 0, nesc = 0;
         if (ca.split_max > 0) RC(readback(c, split_count, sizeof(int), &nsplit));
+        if (ca.esc_max > 0) RC(readback(c, esc_count, sizeof(int), &nesc));
         RC(readback(c, bflops, sizeof(unsigned long long) * 2 * NB1, hf));
         if (st && round == 0) {
             for (int b = 0; b < NB1; b++) {
@@ -679,6 +695,36 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
                 st->split_ms += ms;
                 if (round == 0) st->split_cols += nsplit;
                 st->split_items += nitems;
+            }
+        }
+        if (nesc > 0) {  // low-cf columns: expand, sort, compress (one CTA per column)
+            BinArgs a = base;
+            a.acp = pr.A->col_ptr;
+            a.arow = pr.A->row_idx;
+            a.aval = pr.A->val;
+            a.m = pr.A->nrows;
+            a.bcp = pr.B->col_ptr;
+            a.brow = pr.B->row_idx;
+            a.bval = pr.B->val;
+            a.cb = pr.cb;
+            a.flops = f;
+            a.list = esc_list;
+            a.count = esc_count;
+            a.counter = esc_counter;
+            a.err_flag = err;
+            a.bin_out = esc_out;
+            const int grid = (int)std::min<int64_t>(nesc, (int64_t)std::max(1, esc_occupancy(mode)) * c->sms);
+            CK(cudaEventRecord(c->vev[0], c->stream));
+            CK(launch_esc(mode, a, grid, c->stream));
+            CK(cudaEventRecord(c->vev[1], c->stream));
+            if (st) {
+                unsigned long long ef = 0;
+                RC(readback(c, esc_flops, sizeof ef, &ef));
+                float ms = 0.f;
+                CK(cudaEventElapsedTime(&ms, c->vev[0], c->vev[1]));
+                st->esc_cols += nesc;
+                st->esc_flops += (int64_t)ef;
+                st->esc_ms += ms;
             }
         }
         bool launched[kAllBins] = {};
@@ -792,9 +838,10 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
         cls_list = retry_in;
     }
     if (st) {
-        unsigned long long ho[kAllBins];
-        RC(readback(c, bout, sizeof(unsigned long long) * NB1, ho));
+        unsigned long long ho[kAllBins + 2];
+        RC(readback(c, bout, sizeof(unsigned long long) * (NB1 + 2), ho));
         for (int b = 0; b < NB1; b++) st->bin_out[b % kFamily] += (int64_t)ho[b];
+        st->esc_out += (int64_t)ho[NB1 + 1];
     }
     int herr = 0;
     RC(readback(c, err, sizeof(int), &herr));
@@ -1086,6 +1133,10 @@ void add_stats(mcl_stats_t *st, const mcl_stats_t &q) {
         st->split_vcols[v] += q.split_vcols[v];
         st->split_vms[v] += q.split_vms[v];
     }
+    st->esc_cols += q.esc_cols;
+    st->esc_flops += q.esc_flops;
+    st->esc_out += q.esc_out;
+    st->esc_ms += q.esc_ms;
     st->peak_bytes = std::max(st->peak_bytes, q.peak_bytes);
     st->launches += q.launches;
     st->estimator_used = q.estimator_used;
@@ -1335,6 +1386,7 @@ int mcl_ctx_create(mcl_ctx_t *out, int device, void *stream, mcl_alloc_fn alloc,
     if (const char *e = getenv("MCLX_VALIDATE")) c->validate = atoi(e) != 0;
     if (const char *e = getenv("MCLX_FAMILY")) c->family = atoi(e);
     if (const char *e = getenv("MCLX_SPLIT_CAND")) c->split_cand = atoi(e) != 0;
+    if (const char *e = getenv("MCLX_ESC_CF")) c->esc_cf = atof(e);
     if (const char *e = getenv("MCLX_PHASES")) c->force_phases = atoi(e);
     if (const char *e = getenv("MCLX_PHASE_BUDGET_MB")) c->phase_budget = (int64_t)atoll(e) << 20;
     if (ensure_pin(c, &c->pin, &c->pin_bytes, kPinBytes) != MCL_OK ||

@@ -126,6 +126,13 @@ constexpr int kFamily = kNumBins + 1;
 constexpr int kAllBins = 2 * kFamily;
 constexpr int kShortSegment = 16;  // flops_j / nnz(B_*j) below this -> atomic family
 
+// expand-sort-compress kernel of low-cf columns (kernels_esc.cu): one CTA per column of
+// at most kEscCap products
+constexpr int kEscCap = 1024;
+constexpr int kEscThreads = 128;
+cudaError_t launch_esc(int mode, const BinArgs &a, int grid, cudaStream_t s);
+int esc_occupancy(int mode);
+
 // One launch of bin `bin` (0..kAllBins-1) in mode `mode`; grid chosen from occupancy.
 cudaError_t launch_bin(int mode, int bin, const BinArgs &a, int grid, cudaStream_t s);
 // Max resident CTAs per SM for (mode, bin); also sets the dynamic smem attribute.
@@ -189,6 +196,13 @@ struct ClassifyArgs {
     int64_t split_min;       // also split smaller columns with need > split_min (tests)
     int64_t split_part_need; // distinct rows a part is sized for (kPartNeed)
     int64_t fp64_terms;      // nnz(B_*j) above which a column accumulates in fp64 (kFp64Terms)
+    // low-cf columns (kernels_esc.cu): f_j <= esc_max and f_j < esc_cf x (estimated or exact
+    // nnz_j) run the expand-sort-compress kernel; esc_max = 0 disables
+    int64_t esc_max;
+    double esc_cf;
+    int *esc_count;
+    int32_t *esc_list;
+    unsigned long long *esc_flops;
     int *split_count;
     int32_t *split_list;
     int32_t *split_P;

@@ -403,6 +403,16 @@ __global__ void k_classify(ClassifyArgs c) {
             if (e < (double)need) need = (int64_t)e;
         }
         const int64_t nb = c.bcp[c.cb + col + 1] - c.bcp[c.cb + col];
+        if (c.esc_max > 0 && c.force_bin < 0 && f <= c.esc_max) {
+            // low compression factor: expand-sort-compress
+            const double nest = c.exact ? (double)c.exact[col] : c.est ? (double)c.est[col] : (double)ub;
+            if ((double)f < c.esc_cf * (nest > 1.0 ? nest : 1.0)) {
+                c.esc_list[atomicAdd(c.esc_count, 1)] = (int32_t)col;
+                if (c.colbin) c.colbin[col] = -1;
+                atomicAdd(c.esc_flops, (unsigned long long)f);
+                continue;
+            }
+        }
         int b = 0;
         while (b < kNumBins && (double)need > c.max_load * bin_cap(b)) b++;
         if (nb > c.fp64_terms) b = kNumBins;

@@ -438,3 +438,34 @@ def test_iterate_split_columns_all_entries(monkeypatch, graph):
     _, info = O.prune_inflate(Cr, 1e-4, 1100, 1400, 0.9, 2.0)
     kept_parity(host_mat(Ag), Cr, info, (1e-4, 1100, 1400, 0.9))
     assert st["split_cols"] > 0
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_esc_low_cf_columns(monkeypatch, seed):
+    """Expand-sort-compress (kernels_esc.cu), forced onto every column with <= 1024 products
+    (MCLX_ESC_CF huge): unpruned product bit-exact in structure, exact symbolic counts, and the
+    fused iterate equal to the oracle's."""
+    monkeypatch.setenv("MCLX_ESC_CF", "1e9")
+    rng = np.random.default_rng(70 + seed)
+    n = int(rng.integers(200, 3000))
+    A = synth.random_sparse(n, n, float(rng.uniform(0.002, 0.01)), seed=seed, empty_cols=0.05,
+                            degree_skew=bool(seed % 2))
+    ctx = M.Context()
+    Cg, st = ctx.expand(dev(A))
+    Cr, fl = O.expand(A)
+    assert_unpruned_parity(host_mat(Cg), Cr)
+    assert st["esc_cols"] > 0 and st["esc_flops"] <= int(fl.sum())
+    nnz, tot = ctx.symbolic(dev(A))
+    assert np.array_equal(nnz.cpu().numpy(), np.diff(Cr.colptr))
+    A1 = f32(O.preprocess(synth.planted_partition()))
+    A1, _ = O.prune_inflate(O.expand(A1)[0], 1e-4, 1100, 1400, 0.9, 2.0)
+    A1 = f32(A1)
+    for it in range(3):  # late iterations: cf -> 1
+        C1, _ = O.expand(A1)
+        Ag, st = ctx.iterate(dev(A1), M.Params())
+        _, info = O.prune_inflate(C1, 1e-4, 1100, 1400, 0.9, 2.0)
+        kept_parity(host_mat(Ag), C1, info, (1e-4, 1100, 1400, 0.9))
+        A1, _ = O.prune_inflate(C1, 1e-4, 1100, 1400, 0.9, 2.0)
+        A1 = f32(A1)
+    assert st["esc_cols"] > 0
+    ctx.close()
