@@ -85,7 +85,12 @@ class Clocks:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
+
+    def mark(self):
+        """Start of the timed region: samples before it are not reported (the sampler is
+        started before the warm-up so that its own start-up does not stall a timed step)."""
+        self.t0 = time.time()
 
     def stop(self):
         if not self.proc:
@@ -98,7 +103,10 @@ class Clocks:
         self.t.join(timeout=2)
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        t0 = getattr(self, "t0", 0.0)
+        for t, ln in self.lines:
+            if t < t0:
+                continue
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 6:
                 continue
@@ -279,13 +287,13 @@ def run_gpu(args):
         full = allgather_csc(dist, M, blk, n, A.nrows, dev)
         return full, st
 
+    clocks = Clocks(local)
+    clocks.start()
     for _ in range(args.warmup):
         out, st = step()
         del out
     torch.cuda.synchronize()
-
-    clocks = Clocks(local)
-    clocks.start()
+    clocks.mark()
     stream = torch.cuda.current_stream()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     stats = []
@@ -506,7 +514,8 @@ def run_gpu(args):
                        "esc": {"cols": int(s0["esc_cols"]), "flops": int(s0["esc_flops"]),
                                "ms": s0["esc_ms"]},
                        "phases": int(s0["phases"]),
-                       "step_ms_min": min(step_ms), "step_ms_max": max(step_ms)},
+                       "step_ms_min": min(step_ms), "step_ms_max": max(step_ms),
+                       "step_ms_median": float(np.median(step_ms))},
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -40,7 +40,7 @@ struct mcl_ctx {
     size_t pin_up_bytes = 0;
     cudaEvent_t up_ev = nullptr;
     cudaEvent_t ev[8] = {};
-    cudaEvent_t bev[2 * kAllBins] = {};
+    cudaEvent_t bev[2 * kAllBins + 2] = {};  // per bin (+ the ESC kernel)
     cudaEvent_t pev[6] = {};  // phases of the distributed prune
     cudaEvent_t sev[3] = {};  // SUMMA iteration (ev[] is reused by the stage products)
     cudaEvent_t vev[2] = {};  // split path, per part variant
@@ -539,11 +539,20 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
     int *counts, *counters, *retry_count, *err;
     unsigned long long *bflops;
     int32_t *lists, *gcap_col, *retry_list, *retry_in;
-    RC(scratch_t(c, "bin_counts", 4 * NB1 + 8, &counts));
+    // the bins' metadata in ONE buffer, so a round reads it back with one host sync after
+    // the classification and one after the kernels.  ints: [0, NB1) bin counts, [NB1, 2 NB1)
+    // work counters, 2 NB1 retry count, +1 error flag, +2 / +3 ESC count / counter, +4 split
+    // count; then unsigned long longs: bin flops, bin nnz(B_*j), bin outputs, ESC flops / out
+    const int kInts = 2 * NB1 + 6;
+    const size_t ints_bytes = ((size_t)kInts * sizeof(int) + 15) & ~(size_t)15;
+    const size_t ulls_bytes = sizeof(unsigned long long) * (3 * NB1 + 2);
+    unsigned char *meta;
+    RC(scratch(c, "bin_meta", ints_bytes + ulls_bytes, (void **)&meta));
+    counts = reinterpret_cast<int *>(meta);
     counters = counts + NB1;
     retry_count = counters + NB1;
     err = retry_count + 1;
-    RC(scratch_t(c, "bin_flops", 3 * NB1 + 2, &bflops));
+    bflops = reinterpret_cast<unsigned long long *>(meta + ints_bytes);
     unsigned long long *bnnzb = bflops + NB1, *bout = bflops + 2 * NB1;
     // low-cf columns: expand-sort-compress list (kernels_esc.cu), round 0 only
     unsigned long long *esc_flops = bflops + 3 * NB1, *esc_out = esc_flops + 1;
@@ -590,7 +599,7 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
     if (use_split) {
         RC(scratch_t(c, "split_list", (size_t)std::max<int64_t>(n, 1), &split_list));
         RC(scratch_t(c, "split_P", (size_t)std::max<int64_t>(n, 1), &split_P));
-        RC(scratch_t(c, "split_count", 2, &split_count));
+        split_count = counts + 2 * NB1 + 4;
         RC(scratch_t(c, "col_flag", (size_t)std::max<int64_t>(n, 1), &col_flag));
     }
 
@@ -603,10 +612,12 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
     int64_t ncls = n;
     const int32_t *cls_list = nullptr;
     const int nrounds = 3;
+    int herr = 0;
     for (int round = 0; round < nrounds; round++) {
+        // everything but the error flag (bins, counters, retry, ESC, split counts; stats)
         CK(cudaMemsetAsync(counts, 0, sizeof(int) * (2 * NB1 + 1), c->stream));
-        CK(cudaMemsetAsync(esc_count, 0, sizeof(int) * 2, c->stream));
-        CK(cudaMemsetAsync(bflops, 0, sizeof(unsigned long long) * (3 * NB1 + 2), c->stream));
+        CK(cudaMemsetAsync(esc_count, 0, ints_bytes - sizeof(int) * (2 * NB1 + 2) + ulls_bytes,
+                           c->stream));
         ClassifyArgs ca;
         memset(&ca, 0, sizeof ca);
         ca.n = ncls;
@@ -646,28 +657,16 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
             ca.split_count = split_count;
             ca.split_list = split_list;
             ca.split_P = split_P;
-            CK(cudaMemsetAsync(split_count, 0, sizeof(int), c->stream));
             CK(cudaMemsetAsync(col_flag, 0, sizeof(int) * std::max<int64_t>(n, 1), c->stream));
         }
         CK(launch_classify(ca, c->stream));
         if (colbin)
             CK(launch_order_lists(ncls, cls_list, colbin, okey, ohist, ooffs, otmp, lists,
                                   ca.list_stride, c->stream));
-        int hc[2 * kAllBins + 1];
-        unsigned long long hf[3 * kAllBins];
-        RC(readback(c, counts, sizeof(int) * NB1, hc));
-        int nsplit = 0, nesc = 0;
-        if (ca.split_max > 0) RC(readback(c, split_count, sizeof(int), &nsplit));
-        if (ca.esc_max > 0) RC(readback(c, esc_count, sizeof(int), &nesc));
-        RC(readback(c, bflops, sizeof(unsigned long long) * 2 * NB1, hf));
-        if (st && round == 0) {
-            for (int b = 0; b < NB1; b++) {
-                st->bin_cols[b % kFamily] += hc[b];
-                st->bin_flops[b % kFamily] += (int64_t)hf[b];
-                st->bin_nnzb[b % kFamily] += (int64_t)hf[NB1 + b];
-            }
-            st->bin_cols[kNumBins] += nsplit;  // split columns are reported with the global bin
-        }
+        int hc[2 * kAllBins + 6];
+        RC(readback(c, counts, sizeof(int) * kInts, hc));  // sync 1 of the round
+        const int nesc = ca.esc_max > 0 ? hc[2 * NB1 + 2] : 0;
+        const int nsplit = ca.split_max > 0 ? hc[2 * NB1 + 4] : 0;
         if (nsplit > 0) {
             BinArgs a = base;
             a.acp = pr.A->col_ptr;
@@ -714,18 +713,9 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
             a.err_flag = err;
             a.bin_out = esc_out;
             const int grid = (int)std::min<int64_t>(nesc, (int64_t)std::max(1, esc_occupancy(mode)) * c->sms);
-            CK(cudaEventRecord(c->vev[0], c->stream));
+            CK(cudaEventRecord(c->bev[2 * kAllBins], c->stream));
             CK(launch_esc(mode, a, grid, c->stream));
-            CK(cudaEventRecord(c->vev[1], c->stream));
-            if (st) {
-                unsigned long long ef = 0;
-                RC(readback(c, esc_flops, sizeof ef, &ef));
-                float ms = 0.f;
-                CK(cudaEventElapsedTime(&ms, c->vev[0], c->vev[1]));
-                st->esc_cols += nesc;
-                st->esc_flops += (int64_t)ef;
-                st->esc_ms += ms;
-            }
+            CK(cudaEventRecord(c->bev[2 * kAllBins + 1], c->stream));
         }
         bool launched[kAllBins] = {};
         for (int bi = kAllBins - 1; bi >= 0; bi--) {
@@ -818,14 +808,34 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
             CK(cudaEventRecord(c->bev[2 * b + 1], c->stream));
             launched[b] = true;
         }
-        int nretry = 0;
-        RC(readback(c, retry_count, sizeof(int), &nretry));
+        // sync 2 of the round: retries, the error flag and (with stats) the bin counters
+        std::vector<unsigned char> hm(ints_bytes + ulls_bytes);
+        RC(readback(c, meta, st ? ints_bytes + ulls_bytes : ints_bytes, hm.data()));
+        const int *hi = reinterpret_cast<const int *>(hm.data());
+        const unsigned long long *hf = reinterpret_cast<const unsigned long long *>(hm.data() + ints_bytes);
+        const int nretry = hi[2 * NB1];
+        herr = hi[2 * NB1 + 1];
         if (st) {
             for (int b = 0; b < NB1; b++) {
+                if (round == 0) {
+                    st->bin_cols[b % kFamily] += hc[b];
+                    st->bin_flops[b % kFamily] += (int64_t)hf[b];
+                    st->bin_nnzb[b % kFamily] += (int64_t)hf[NB1 + b];
+                }
+                st->bin_out[b % kFamily] += (int64_t)hf[2 * NB1 + b];
                 if (!launched[b]) continue;
                 float ms = 0.f;
                 CK(cudaEventElapsedTime(&ms, c->bev[2 * b], c->bev[2 * b + 1]));
                 st->bin_ms[b % kFamily] += ms;
+            }
+            if (round == 0) st->bin_cols[kNumBins] += nsplit;  // split columns: with the global bin
+            if (nesc > 0) {
+                float ms = 0.f;
+                CK(cudaEventElapsedTime(&ms, c->bev[2 * kAllBins], c->bev[2 * kAllBins + 1]));
+                st->esc_cols += nesc;
+                st->esc_flops += (int64_t)hf[3 * NB1];
+                st->esc_out += (int64_t)hf[3 * NB1 + 1];
+                st->esc_ms += ms;
             }
         }
         if (nretry == 0) break;
@@ -837,14 +847,6 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
         ncls = nretry;
         cls_list = retry_in;
     }
-    if (st) {
-        unsigned long long ho[kAllBins + 2];
-        RC(readback(c, bout, sizeof(unsigned long long) * (NB1 + 2), ho));
-        for (int b = 0; b < NB1; b++) st->bin_out[b % kFamily] += (int64_t)ho[b];
-        st->esc_out += (int64_t)ho[NB1 + 1];
-    }
-    int herr = 0;
-    RC(readback(c, err, sizeof(int), &herr));
     if (herr) return fail(c, MCL_ERR_INTERNAL, "device consistency check failed (code %d)", herr);
     return MCL_OK;
 }
@@ -1396,7 +1398,7 @@ int mcl_ctx_create(mcl_ctx_t *out, int device, void *stream, mcl_alloc_fn alloc,
         return MCL_ERR_CUDA;
     }
     for (int i = 0; i < 8; i++) cudaEventCreate(&c->ev[i]);
-    for (int i = 0; i < 2 * kAllBins; i++) cudaEventCreate(&c->bev[i]);
+    for (int i = 0; i < 2 * kAllBins + 2; i++) cudaEventCreate(&c->bev[i]);
     for (int i = 0; i < 6; i++) cudaEventCreate(&c->pev[i]);
     for (int i = 0; i < 3; i++) cudaEventCreate(&c->sev[i]);
     for (int i = 0; i < 2; i++) cudaEventCreate(&c->vev[i]);
@@ -1428,7 +1430,7 @@ int mcl_ctx_destroy(mcl_ctx_t c) {
     cudaStreamSynchronize(c->stream);
     for (int i = 0; i < 8; i++)
         if (c->ev[i]) cudaEventDestroy(c->ev[i]);
-    for (int i = 0; i < 2 * kAllBins; i++)
+    for (int i = 0; i < 2 * kAllBins + 2; i++)
         if (c->bev[i]) cudaEventDestroy(c->bev[i]);
     for (int i = 0; i < 6; i++)
         if (c->pev[i]) cudaEventDestroy(c->pev[i]);
@@ -1637,9 +1639,14 @@ int mcl_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, mcl_cs
     return mcl_iterate_range(c, A, 0, A->ncols, pin, A_next, st);
 }
 
-// one phase of mcl_iterate_range: the fused iteration on output columns [col_begin, col_end)
+constexpr int kNeedPhases = 1;  // iterate_range_impl: the columns do not fit one phase
+
+// one phase of mcl_iterate_range: the fused iteration on output columns [col_begin, col_end).
+// check_budget: return kNeedPhases (nothing allocated) when the staging of the pruned
+// columns + A_next, 16 B x sum_j min(max(S,R), f_j, m) + 16 B x n, exceeds the phase budget.
 static int iterate_range_impl(mcl_ctx_t c, const mcl_csc_t *A, int64_t col_begin, int64_t col_end,
-                              const mcl_params_t *pin, mcl_csc_t *A_next, mcl_stats_t *st) {
+                              const mcl_params_t *pin, mcl_csc_t *A_next, mcl_stats_t *st,
+                              bool check_budget = false) {
     if (!c) return MCL_ERR_INVALID_ARG;
     if (!A_next || !pin) return fail(c, MCL_ERR_INVALID_ARG, "NULL argument");
     zero_csc(A_next);
@@ -1700,6 +1707,13 @@ static int iterate_range_impl(mcl_ctx_t c, const mcl_csc_t *A, int64_t col_begin
     CK(launch_scan_i64(kcap, soff, n, tmp, c->stream));
     int64_t stot = 0;
     RC(readback(c, soff + n, sizeof(int64_t), &stot));
+    if (check_budget) {
+        const double bytes = 16.0 * (double)stot + 16.0 * (double)n;
+        // (the free-memory query only for sizable iterations, or an explicit budget)
+        if ((bytes > (double)(1 << 30) || c->phase_budget > 0) &&
+            bytes > phase_budget(c, pin->mem_safety))
+            return kNeedPhases;
+    }
     RC(scratch_t(c, "s_row", (size_t)std::max<int64_t>(stot, 1), &srow));
     RC(scratch_t(c, "s_val", (size_t)std::max<int64_t>(stot, 1), &sval));
     CK(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * std::max<int64_t>(n, 1), c->stream));
@@ -1770,6 +1784,13 @@ int mcl_iterate_range(mcl_ctx_t c, const mcl_csc_t *A, int64_t col_begin, int64_
     // near-equal bytes within mem_safety x free HBM, each batch runs as one fused iteration
     // and the batches' outputs are concatenated.
     const int64_t n = col_end - col_begin;
+    if (c->force_phases <= 1) {  // one phase unless it would not fit (checked inside)
+        const int rc = iterate_range_impl(c, A, col_begin, col_end, pin, A_next, st, true);
+        if (rc != kNeedPhases) {
+            if (rc == MCL_OK && st) st->phases = 1;
+            return rc;
+        }
+    }
     const PruneParams pp = prune_params(pin);
     int64_t *f, *bytes;
     RC(scratch_t(c, "phase_flops", (size_t)std::max<int64_t>(n, 1), &f));

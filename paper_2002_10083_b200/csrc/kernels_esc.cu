@@ -11,8 +11,8 @@
 //   expand   warps copy the products b_kj a_ik of the column's segments A_*k into shared
 //            memory (row, value) arrays, lanes over a segment's entries (coalesced);
 //   sort     bitonic sort by row (f_j <= kEscCap, padded to a power of two);
-//   compress a row's run of equal rows is summed by the run's head thread (a block scan of
-//            the head flags gives each distinct row its output slot).
+//   compress a row's run of equal rows is summed (fp64) by the run's head thread (a block
+//            scan of the head flags gives each distinct row its output slot).
 // The compressed column is sorted by construction, so kNum writes it out directly and kFused
 // hands it to prune_column (threshold / select / recover / inflate, Q1-Q9); kSym counts it.
 #include "kernels.h"
@@ -88,11 +88,11 @@ __global__ void __launch_bounds__(kEscThreads) k_esc(BinArgs a) {
             const int head = i < f && (i == 0 || srow[i] != srow[i - 1]);
             int t2;
             const int pos = block_excl_scan<NT>(head, sscan, t2);
-            if (head) {
-                float v = 0.f;
-                for (int q = i; q < f && srow[q] == srow[i]; q++) v += sval[q];
+            if (head) {  // fp64 run sums (a forced ESC column may have long runs)
+                double v = 0.0;
+                for (int q = i; q < f && srow[q] == srow[i]; q++) v += (double)sval[q];
                 orow[nnz + pos] = srow[i];
-                oval[nnz + pos] = v;
+                oval[nnz + pos] = (float)v;
             }
             nnz += t2;
         }

@@ -457,15 +457,15 @@ def test_esc_low_cf_columns(monkeypatch, seed):
     assert st["esc_cols"] > 0 and st["esc_flops"] <= int(fl.sum())
     nnz, tot = ctx.symbolic(dev(A))
     assert np.array_equal(nnz.cpu().numpy(), np.diff(Cr.colptr))
-    A1 = f32(O.preprocess(synth.planted_partition()))
-    A1, _ = O.prune_inflate(O.expand(A1)[0], 1e-4, 1100, 1400, 0.9, 2.0)
-    A1 = f32(A1)
-    for it in range(3):  # late iterations: cf -> 1
+    A1 = f32(O.preprocess(synth.protein_like(n=3000, seed=seed)))
+    esc = 0
+    for it in range(6):  # MCL iterations 0-5: cf falls towards 1, more columns take ESC
         C1, _ = O.expand(A1)
         Ag, st = ctx.iterate(dev(A1), M.Params())
         _, info = O.prune_inflate(C1, 1e-4, 1100, 1400, 0.9, 2.0)
         kept_parity(host_mat(Ag), C1, info, (1e-4, 1100, 1400, 0.9))
+        esc += st["esc_cols"]
         A1, _ = O.prune_inflate(C1, 1e-4, 1100, 1400, 0.9, 2.0)
         A1 = f32(A1)
-    assert st["esc_cols"] > 0
+    assert esc > 0
     ctx.close()
