@@ -1957,7 +1957,7 @@ int mcl_summa_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, 
         A->col0 != cut(n, pc, gj) || A->ncols != cut(n, pc, gj + 1) - cut(n, pc, gj))
         return fail(c, MCL_ERR_DIM, "block (%d,%d) does not match the %dx%d grid of n=%lld", gi, gj,
                     pr, pc, (long long)n);
-    if (pr == 1 && !getenv("MCLX_SUMMA_STAGED")) {
+    if (pr == 1 && !getenv("MCLX_SUMMA_STAGED") && !getenv("MCLX_SUMMA_ACCUM")) {
         // 1 x pc grid: every column of C = A*A lives on one rank.  The stage broadcasts of
         // the A-panels (the pc column stripes) are issued together, and instead of
         // materialising one partial product per stage and merging them (Alg. 2), all stages
@@ -2197,30 +2197,22 @@ int mcl_summa_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, 
         return Pb;
     };
 
-    // ---- phases (Q15): the partials Alg. 2 holds for a column are
-    // estimated from Cohen's estimate of every stage product (on the resident
-    // panels), 8 B x 1.3 x sum_q est_q(j) x 2 (partials + the merge's copy) + 16 B; the
-    // estimates are all-reduced (max) over the column communicator, whose ranks split the
-    // same columns and must run the same batches for the distributed prune
-    int64_t *pbytes;
-    float *pest;
-    RC(scratch_t(c, "summa_phase_bytes", (size_t)std::max<int64_t>(nj, 1), &pbytes));
-    RC(scratch_t(c, "summa_phase_est", (size_t)std::max<int64_t>(nj, 1), &pest));
-    CK(cudaMemsetAsync(pbytes, 0, sizeof(int64_t) * std::max<int64_t>(nj, 1), c->stream));
-    for (int q = 0; q < s; q++) {
-        CK(cudaStreamWaitEvent(c->stream, ready[q], 0));
-        mcl_csc_t Pa = panel_a(q), Pb = panel_b(q);
-        RC(cohen(c, Prod{&Pa, &Pb, 0, nj}, pin->est_keys, pin->seed, pest, nullptr));
-        CK(launch_affine_est(nj, pest, 8.0 * 1.3 * 2.0, q == 0 ? 16 : 0, pbytes, c->stream));
-    }
-    if (pr > 1 && nj > 0) NC(ncclAllReduce(pbytes, pbytes, nj, ncclInt64, ncclMax, c->colc, c->stream));
+    // ---- phases (Q15) and the products.  Two forms:
+    //  * accumulating (default for pr > 1): C_ij = sum_q A_iq B_qj = A[rows_i, :] A[:, cols_j].
+    //    The A-panels are the column ranges of the row stripe and the B-panels the row ranges
+    //    of the column stripe, so stacking them gives both stripes and ONE binned hash SpGEMM
+    //    forms C_ij: every stage's products land in the same hash tables, the per-stage
+    //    partials and Alg. 2's merges are never materialised.  Phases are sized by the
+    //    product's upper-bound slots, 16 B x min(f_j, m_i).
+    //  * staged (MCLX_SUMMA_STAGED=1): one product per stage and the Alg. 2 binary merge
+    //    (P:509-529), phases sized by Cohen's estimate of every stage product:
+    //    8 B x 1.3 x sum_q est_q(j) x 2 (partials + the merge's copy) + 16 B.
+    // Either way the byte estimates are all-reduced (max) over the column communicator, whose
+    // ranks split the same columns and must run the same batches for the distributed prune.
+    const bool staged = getenv("MCLX_SUMMA_STAGED") != nullptr;
     std::vector<int64_t> bounds;
     int64_t est_bytes = 0;
-    RC(plan_phases(c, pbytes, nj, phase_budget(c, pin->mem_safety), bounds, &est_bytes));
-    const int h = (int)bounds.size() - 1;
-
-    // ---- per phase: stage products on the phase's columns, Alg. 2 binary merge
-    // (P:509-529), distributed prune / inflate
+    int h = 1;
     std::vector<mcl_csc_t> pieces;
     std::vector<mcl_csc_t> stack;
     int64_t peak_partial = 0, flops = 0, nnz_unpruned = 0;
@@ -2233,13 +2225,159 @@ int mcl_summa_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, 
         for (auto &x : v) free_csc(c, &x);
         v.clear();
     };
-    for (int ph = 0; ph < h && rc == MCL_OK; ph++) {
-        const int64_t c0 = bounds[ph], c1 = bounds[ph + 1];
-        int64_t live_partial = 0;
-        for (int q = 0; q < s && rc == MCL_OK; q++) {
-            mcl_csc_t Pa = panel_a(q), Pb = panel_b(q), Pq;
+    mcl_csc_t Ai, Bj;
+    zero_csc(&Ai);
+    zero_csc(&Bj);
+    if (staged) {
+        int64_t *pbytes;
+        float *pest;
+        RC(scratch_t(c, "summa_phase_bytes", (size_t)std::max<int64_t>(nj, 1), &pbytes));
+        RC(scratch_t(c, "summa_phase_est", (size_t)std::max<int64_t>(nj, 1), &pest));
+        CK(cudaMemsetAsync(pbytes, 0, sizeof(int64_t) * std::max<int64_t>(nj, 1), c->stream));
+        for (int q = 0; q < s; q++) {
+            CK(cudaStreamWaitEvent(c->stream, ready[q], 0));
+            mcl_csc_t Pa = panel_a(q), Pb = panel_b(q);
+            RC(cohen(c, Prod{&Pa, &Pb, 0, nj}, pin->est_keys, pin->seed, pest, nullptr));
+            CK(launch_affine_est(nj, pest, 8.0 * 1.3 * 2.0, q == 0 ? 16 : 0, pbytes, c->stream));
+        }
+        if (pr > 1 && nj > 0) NC(ncclAllReduce(pbytes, pbytes, nj, ncclInt64, ncclMax, c->colc, c->stream));
+        RC(plan_phases(c, pbytes, nj, phase_budget(c, pin->mem_safety), bounds, &est_bytes));
+        h = (int)bounds.size() - 1;
+        // per phase: stage products on the phase's columns, Alg. 2 binary merge, distributed
+        // prune / inflate
+        for (int ph = 0; ph < h && rc == MCL_OK; ph++) {
+            const int64_t c0 = bounds[ph], c1 = bounds[ph + 1];
+            int64_t live_partial = 0;
+            for (int q = 0; q < s && rc == MCL_OK; q++) {
+                mcl_csc_t Pa = panel_a(q), Pb = panel_b(q), Pq;
+                mcl_stats_t sst;
+                if ((rc = spgemm_impl(c, &Pa, &Pb, c0, c1, pin, &Pq, &sst)) != MCL_OK) break;
+                flops += sst.flops;
+                for (int b = 0; b <= kNumBins; b++) {
+                    bin_ms[b] += sst.bin_ms[b];
+                    bin_flops[b] += sst.bin_flops[b];
+                    bin_cols[b] += sst.bin_cols[b];
+                    bin_nnzb[b] += sst.bin_nnzb[b];
+                    bin_out[b] += sst.bin_out[b];
+                }
+                Pq.row0 = A->row0;
+                Pq.col0 = A->col0 + c0;
+                Pq.n_global = n;
+                stack.push_back(Pq);
+                live_partial += Pq.nnz;
+                peak_partial = std::max(peak_partial, live_partial);
+                // Alg. 2 lines 5-14: merge nmerges+1 lists when the stage count is even
+                int jj = q + 1, nmerges = 0;
+                while (jj % 2 == 0 && jj != 0) {
+                    nmerges++;
+                    jj /= 2;
+                }
+                if (nmerges > 0) {
+                    std::vector<mcl_csc_t> L(stack.end() - (nmerges + 1), stack.end());
+                    mcl_csc_t merged;
+                    if ((rc = merge_impl(c, (int32_t)L.size(), L.data(), &merged)) != MCL_OK) break;
+                    for (auto &x : L) {
+                        live_partial -= x.nnz;
+                        free_csc(c, &x);
+                    }
+                    stack.resize(stack.size() - L.size());
+                    stack.push_back(merged);
+                    live_partial += merged.nnz;
+                    peak_partial = std::max(peak_partial, live_partial);
+                }
+            }
+            if (rc == MCL_OK && stack.size() > 1) {  // Q16: stage counts that are not powers of two
+                mcl_csc_t merged;
+                rc = merge_impl(c, (int32_t)stack.size(), stack.data(), &merged);
+                if (rc == MCL_OK) {
+                    drop(stack);
+                    stack.push_back(merged);
+                }
+            }
+            if (rc != MCL_OK) break;
+            mcl_csc_t Cb = stack[0], piece;
+            stack.clear();
+            float ch = 0.f;
+            rc = dist_prune(c, &Cb, pr > 1 ? c->colc : nullptr, pp, &piece, &ch);
+            nnz_unpruned += Cb.nnz;
+            free_csc(c, &Cb);
+            if (rc != MCL_OK) break;
+            pieces.push_back(piece);
+            chaos = std::max(chaos, ch);
+        }
+    } else {
+        if (s > kMaxStages) return fail(c, MCL_ERR_NOT_IMPLEMENTED, "more than %d inner panels", kMaxStages);
+        int64_t nnzAi = 0, nnzBj = 0;
+        for (int q = 0; q < s; q++) {
+            CK(cudaStreamWaitEvent(c->stream, ready[q], 0));
+            nnzAi += pan[q].nnzA;
+            nnzBj += pan[q].nnzB;
+        }
+        int64_t *aicp, *bjcp, *bjcnt;
+        int32_t *airow, *bjrow;
+        float *aival, *bjval;
+        RC(scratch_t(c, "summa_aicp", (size_t)n + 1, &aicp));
+        RC(scratch_t(c, "summa_airow", (size_t)std::max<int64_t>(nnzAi, 1), &airow));
+        RC(scratch_t(c, "summa_aival", (size_t)std::max<int64_t>(nnzAi, 1), &aival));
+        RC(scratch_t(c, "summa_bjcp", (size_t)nj + 1, &bjcp));
+        RC(scratch_t(c, "summa_bjcnt", (size_t)std::max<int64_t>(nj, 1), &bjcnt));
+        RC(scratch_t(c, "summa_bjrow", (size_t)std::max<int64_t>(nnzBj, 1), &bjrow));
+        RC(scratch_t(c, "summa_bjval", (size_t)std::max<int64_t>(nnzBj, 1), &bjval));
+        int64_t off = 0;
+        for (int q = 0; q < s; q++) {  // A[rows_i, :]: the A-panels side by side
+            CK(launch_offset_colptr(pan[q].kq + 1, pan[q].acp, off, aicp + pan[q].k0, c->stream));
+            if (pan[q].nnzA) {
+                CK(cudaMemcpyAsync(airow + off, pan[q].arow, sizeof(int32_t) * pan[q].nnzA,
+                                   cudaMemcpyDeviceToDevice, c->stream));
+                CK(cudaMemcpyAsync(aival + off, pan[q].aval, sizeof(float) * pan[q].nnzA,
+                                   cudaMemcpyDeviceToDevice, c->stream));
+            }
+            off += pan[q].nnzA;
+        }
+        VStack v;  // A[:, cols_j]: the B-panels stacked by rows
+        memset(&v, 0, sizeof v);
+        v.s = s;
+        for (int q = 0; q < s; q++) {
+            v.cp[q] = pan[q].bcp;
+            v.row[q] = pan[q].brow;
+            v.val[q] = pan[q].bval;
+            v.k0[q] = pan[q].k0;
+        }
+        CK(launch_vstack(nj, v, bjcnt, nullptr, nullptr, nullptr, true, c->stream));
+        CK(launch_scan_i64(bjcnt, bjcp, nj, tmp, c->stream));
+        CK(launch_vstack(nj, v, nullptr, bjcp, bjrow, bjval, false, c->stream));
+        Ai.nrows = mi;
+        Ai.ncols = n;
+        Ai.nnz = nnzAi;
+        Ai.row0 = A->row0;
+        Ai.n_global = n;
+        Ai.col_ptr = aicp;
+        Ai.row_idx = airow;
+        Ai.val = aival;
+        Bj.nrows = n;
+        Bj.ncols = nj;
+        Bj.nnz = nnzBj;
+        Bj.col0 = A->col0;
+        Bj.n_global = n;
+        Bj.col_ptr = bjcp;
+        Bj.row_idx = bjrow;
+        Bj.val = bjval;
+        int64_t *pbytes, *pf;
+        RC(scratch_t(c, "summa_phase_bytes", (size_t)std::max<int64_t>(nj, 1), &pbytes));
+        RC(scratch_t(c, "summa_phase_flops", (size_t)std::max<int64_t>(nj, 1), &pf));
+        CK(launch_flops(nj, Ai.col_ptr, Bj.col_ptr, Bj.row_idx, 0, pf, c->stream));
+        CK(launch_kcap(nj, pf, mi, INT32_MAX, pbytes, c->stream));
+        CK(launch_affine_i64(nj, pbytes, 16, 16, pbytes, false, c->stream));
+        if (pr > 1 && nj > 0) NC(ncclAllReduce(pbytes, pbytes, nj, ncclInt64, ncclMax, c->colc, c->stream));
+        RC(plan_phases(c, pbytes, nj,
+                       std::min(phase_budget(c, pin->mem_safety), 2.0 * (double)c->cap_budget), bounds,
+                       &est_bytes));
+        h = (int)bounds.size() - 1;
+        for (int ph = 0; ph < h && rc == MCL_OK; ph++) {
+            const int64_t c0 = bounds[ph], c1 = bounds[ph + 1];
+            mcl_csc_t Cb, piece;
             mcl_stats_t sst;
-            if ((rc = spgemm_impl(c, &Pa, &Pb, c0, c1, pin, &Pq, &sst)) != MCL_OK) break;
+            if ((rc = spgemm_impl(c, &Ai, &Bj, c0, c1, pin, &Cb, &sst)) != MCL_OK) break;
             flops += sst.flops;
             for (int b = 0; b <= kNumBins; b++) {
                 bin_ms[b] += sst.bin_ms[b];
@@ -2248,50 +2386,18 @@ int mcl_summa_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, 
                 bin_nnzb[b] += sst.bin_nnzb[b];
                 bin_out[b] += sst.bin_out[b];
             }
-            Pq.row0 = A->row0;
-            Pq.col0 = A->col0 + c0;
-            Pq.n_global = n;
-            stack.push_back(Pq);
-            live_partial += Pq.nnz;
-            peak_partial = std::max(peak_partial, live_partial);
-            // Alg. 2 lines 5-14: merge nmerges+1 lists when the stage count is even
-            int jj = q + 1, nmerges = 0;
-            while (jj % 2 == 0 && jj != 0) {
-                nmerges++;
-                jj /= 2;
-            }
-            if (nmerges > 0) {
-                std::vector<mcl_csc_t> L(stack.end() - (nmerges + 1), stack.end());
-                mcl_csc_t merged;
-                if ((rc = merge_impl(c, (int32_t)L.size(), L.data(), &merged)) != MCL_OK) break;
-                for (auto &x : L) {
-                    live_partial -= x.nnz;
-                    free_csc(c, &x);
-                }
-                stack.resize(stack.size() - L.size());
-                stack.push_back(merged);
-                live_partial += merged.nnz;
-                peak_partial = std::max(peak_partial, live_partial);
-            }
+            Cb.row0 = A->row0;
+            Cb.col0 = A->col0 + c0;
+            Cb.n_global = n;
+            peak_partial = std::max(peak_partial, Cb.nnz);
+            float ch = 0.f;
+            rc = dist_prune(c, &Cb, pr > 1 ? c->colc : nullptr, pp, &piece, &ch);
+            nnz_unpruned += Cb.nnz;
+            free_csc(c, &Cb);
+            if (rc != MCL_OK) break;
+            pieces.push_back(piece);
+            chaos = std::max(chaos, ch);
         }
-        if (rc == MCL_OK && stack.size() > 1) {  // Q16: stage counts that are not powers of two
-            mcl_csc_t merged;
-            rc = merge_impl(c, (int32_t)stack.size(), stack.data(), &merged);
-            if (rc == MCL_OK) {
-                drop(stack);
-                stack.push_back(merged);
-            }
-        }
-        if (rc != MCL_OK) break;
-        mcl_csc_t Cb = stack[0], piece;
-        stack.clear();
-        float ch = 0.f;
-        rc = dist_prune(c, &Cb, pr > 1 ? c->colc : nullptr, pp, &piece, &ch);
-        nnz_unpruned += Cb.nnz;
-        free_csc(c, &Cb);
-        if (rc != MCL_OK) break;
-        pieces.push_back(piece);
-        chaos = std::max(chaos, ch);
     }
     if (rc != MCL_OK) {
         drop(stack);
@@ -2320,7 +2426,7 @@ int mcl_summa_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, 
         st->chaos = chaos;
         st->phases = h;
         st->stages = s;
-        st->est_nnz = (double)est_bytes / (8.0 * 1.3 * 2.0);
+        st->est_nnz = staged ? (double)est_bytes / (8.0 * 1.3 * 2.0) : -1.0;
         st->estimator_used = 1;
         float tot = -1.f;
         cudaEventSynchronize(c->sev[2]);

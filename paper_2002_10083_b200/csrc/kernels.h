@@ -266,6 +266,17 @@ cudaError_t launch_cc(int64_t n, const int64_t *cp, const int32_t *row, int32_t 
                       cudaStream_t s);
 
 // SUMMA kernels (kernels_summa.cu)
+constexpr int kMaxStages = 16;
+struct VStack {  // s <= kMaxStages B-panels (row ranges starting at k0[q]) of one column stripe
+    const int64_t *cp[kMaxStages];
+    const int32_t *row[kMaxStages];
+    const float *val[kMaxStages];
+    int64_t k0[kMaxStages];
+    int s;
+};
+// count_only: cnt[j] = nnz of stacked column j; else copy into (ocp, orow, oval)
+cudaError_t launch_vstack(int64_t nj, const VStack &v, int64_t *cnt, const int64_t *ocp, int32_t *orow,
+                          float *oval, bool count_only, cudaStream_t s);
 cudaError_t launch_rebase_colptr(int64_t n1, const int64_t *cp, int64_t *out, cudaStream_t s);
 cudaError_t launch_rowslice_count(int64_t ncols, const int64_t *cp, const int32_t *rows, int64_t r0,
                                   int64_t r1, int64_t *first, int64_t *cnt, cudaStream_t s);

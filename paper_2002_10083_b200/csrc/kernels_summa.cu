@@ -33,6 +33,50 @@ cudaError_t launch_rebase_colptr(int64_t n1, const int64_t *cp, int64_t *out, cu
     return cudaGetLastError();
 }
 
+// Column j of the vertical stack of the s B-panels (row ranges K_q of the column stripe):
+// panel 0's column j, then panel 1's (rows + k0_1), ... -- rows stay sorted because the K_q
+// ascend.  Gives rank (i, j) the column stripe A[:, cols_j] as one CSC.
+__global__ void k_vstack_count(int64_t nj, VStack v, int64_t *__restrict__ cnt) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nj;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        int64_t c = 0;
+        for (int q = 0; q < v.s; q++) c += v.cp[q][j + 1] - v.cp[q][j];
+        cnt[j] = c;
+    }
+}
+__global__ void k_vstack_copy(int64_t nj, VStack v, const int64_t *__restrict__ ocp,
+                              int32_t *__restrict__ orow, float *__restrict__ oval) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t j = w0; j < nj; j += nw) {
+        int64_t o = ocp[j];
+        for (int q = 0; q < v.s; q++) {
+            const int64_t a = v.cp[q][j], b = v.cp[q][j + 1];
+            for (int64_t e = a + lane; e < b; e += 32) {
+                orow[o + e - a] = (int32_t)(v.row[q][e] + v.k0[q]);
+                oval[o + e - a] = v.val[q][e];
+            }
+            o += b - a;
+        }
+    }
+}
+cudaError_t launch_vstack(int64_t nj, const VStack &v, int64_t *cnt, const int64_t *ocp, int32_t *orow,
+                          float *oval, bool count_only, cudaStream_t s) {
+    if (nj <= 0) return cudaSuccess;
+    ++g_launches;
+    if (count_only) {
+        int64_t b = (nj + 255) / 256;
+        if (b > g_sms * 16) b = g_sms * 16;
+        k_vstack_count<<<(int)b, 256, 0, s>>>(nj, v, cnt);
+    } else {
+        int64_t b = (nj * 32 + 255) / 256;
+        if (b > g_sms * 32) b = g_sms * 32;
+        k_vstack_copy<<<(int)b, 256, 0, s>>>(nj, v, ocp, orow, oval);
+    }
+    return cudaGetLastError();
+}
+
 __device__ __forceinline__ int64_t lb_rows(const int32_t *rows, int64_t lo, int64_t hi, int64_t key) {
     while (lo < hi) {
         const int64_t mid = (lo + hi) >> 1;

@@ -74,8 +74,12 @@ def test_iterate_phases_from_budget(monkeypatch):
 
 @pytest.mark.parametrize("name", ["C1it1", "C2"])
 @pytest.mark.parametrize("phases", [1, 3])
-def test_summa_staged_1x1(monkeypatch, name, phases):
-    monkeypatch.setenv("MCLX_SUMMA_STAGED", "1")
+@pytest.mark.parametrize("form", ["staged", "accumulating"])
+def test_summa_staged_1x1(monkeypatch, name, phases, form):
+    """form staged: one product per stage + Alg. 2 merges; accumulating (the pr > 1 default,
+    forced on 1 x 1 by MCLX_SUMMA_ACCUM): the 4 A-panels side by side and the 4 B-panels
+    stacked, one product, then the distributed prune."""
+    monkeypatch.setenv("MCLX_SUMMA_STAGED" if form == "staged" else "MCLX_SUMMA_ACCUM", "1")
     monkeypatch.setenv("MCLX_SUMMA_STAGES", "4")
     monkeypatch.setenv("MCLX_PHASES", str(phases))
     A, prm = _input(name)
@@ -89,7 +93,8 @@ def test_summa_staged_1x1(monkeypatch, name, phases):
     assert st["stages"] == 4 and st["phases"] == phases
     assert st["flops"] == int(fl.sum())
     assert st["nnz_unpruned"] == Cr.nnz
-    # Alg. 2 on 4 stages keeps at most 3 lists alive (m12, l3, l4 before the last merge)
-    assert 0 < st["peak_partial"] <= 3 * Cr.nnz
+    # Alg. 2 on 4 stages keeps at most 3 lists alive (m12, l3, l4 before the last merge);
+    # the accumulating form holds one phase's unpruned block
+    assert 0 < st["peak_partial"] <= (3 if form == "staged" else 1) * Cr.nnz
     assert st["chaos"] == pytest.approx(info.chaos.max(), rel=1e-3, abs=1e-5)
     ctx.close()
