@@ -60,7 +60,7 @@ struct mcl_ctx {
     int64_t split_min_need = INT64_MAX;       // MCLX_SPLIT_MIN_NEED: split smaller columns too
     int64_t split_part_need = kPartNeed;      // MCLX_SPLIT_PART_NEED (<= kPartNeed; tests)
     int64_t fp64_terms = kFp64Terms;          // MCLX_FP64_TERMS (tests)
-    int64_t cap_budget = (int64_t)16 << 30;   // unfused products: upper-bound slots up to this
+    int64_t cap_budget = (int64_t)48 << 30;   // unfused products: upper-bound slots up to this
     bool split_private = true;                // MCLX_SPLIT_PRIVATE=0: P <= 4 parts shared-table too
     bool validate = false;                    // MCLX_VALIDATE=1: check input CSC invariants
     bool split_cand = true;                   // MCLX_SPLIT_CAND=0: split parts stage every entry

@@ -135,6 +135,8 @@ __device__ __forceinline__ bool insert4b(int *keys, V *vals, uint32_t cap, const
     return ok;
 }
 
+constexpr int kLongSeg = 128;  // CTA-shared family: segments walked by a whole warp
+
 __device__ __forceinline__ int group_size_for(int64_t avg) {
     return avg >= 24 ? 32 : avg >= 12 ? 16 : avg >= 6 ? 8 : 4;
 }
@@ -286,7 +288,7 @@ __global__ void __launch_bounds__(NT, (bin_min_blocks<CAP, NT, MODE, GLOBAL, ATO
             __shared__ int st_k[NT];
             __shared__ float st_b[NT];
             __shared__ int s_fill[1];
-            __shared__ int s_next[1];
+            __shared__ int s_next[2];
             if (tid == 0) s_fill[0] = 0;
             __syncthreads();
             // ---- accumulate C_*j = sum_k b_kj A_*k.  Each lane gathers 4 consecutive
@@ -295,54 +297,63 @@ __global__ void __launch_bounds__(NT, (bin_min_blocks<CAP, NT, MODE, GLOBAL, ATO
             const int limit = (int)(cap - (cap >> 3));
             const int64_t bj = a.cb + col;
             const int64_t q0 = a.bcp[bj], q1 = a.bcp[bj + 1];
-            const int64_t nb = q1 - q0;
-            // a part sees (p1 - p0) / 32 of every segment on average
-            const int64_t fcol = MODE == kPart
-                                     ? a.flops[col] * ((s_pr >> 8) - (s_pr & 0xff)) / kParts
-                                     : a.flops[col];
-            const int g = group_size_for(nb > 0 ? fcol / (4 * nb) : 0);
-            const int lane_g = lane & (g - 1);
-            const int grp = tid / g;        // group index in the CTA
-            const int ngrp = NT / g;
             volatile int *vovf = &s_ovf;
+            __shared__ int s_nl, s_ns, s_sumS;
             for (int64_t c0 = q0; c0 < q1; c0 += NT) {
                 const int cnt = (int)((q1 - c0) < NT ? (q1 - c0) : NT);
+                if (tid == 0) {
+                    s_nl = 0;
+                    s_ns = 0;
+                    s_sumS = 0;
+                }
+                __syncthreads();
+                // descriptors, split in two classes (R-MAT columns mix hub segments of
+                // thousands of entries with 1-3 entry ones): long segments listed from the
+                // front and walked by whole warps, short ones from the back with a group size
+                // from their own mean length; empty (part) segments dropped
                 if (tid < cnt) {
                     const int k = __ldg(a.brow + c0 + tid);
                     const int64_t st = __ldg(a.acp + k);
+                    int64_t s0 = st;
+                    int len;
                     if (MODE == kPart) {
                         // the part's rows: positions [rowpart[k][p0], rowpart[k][p1]) of A_*k
                         const int *pk = a.rowpart + (int64_t)k * (kParts + 1);
                         const int r0 = __ldg(pk + (s_pr & 0xff)), r1 = __ldg(pk + (s_pr >> 8));
-                        st_start[tid] = st + r0;
-                        st_k[tid] = r1 - r0;
+                        s0 = st + r0;
+                        len = r1 - r0;
                     } else {
-                        st_start[tid] = st;
-                        st_k[tid] = (int)(__ldg(a.acp + k + 1) - st);  // segment length
+                        len = (int)(__ldg(a.acp + k + 1) - st);  // segment length
                     }
-                    st_b[tid] = __ldg(a.bval + c0 + tid);
+                    if (len > 0) {
+                        int slot;
+                        if (len >= kLongSeg) {
+                            slot = atomicAdd(&s_nl, 1);
+                        } else {
+                            slot = NT - 1 - atomicAdd(&s_ns, 1);
+                            atomicAdd(&s_sumS, len);
+                        }
+                        st_start[slot] = s0;
+                        st_k[slot] = len;
+                        st_b[slot] = __ldg(a.bval + c0 + tid);
+                    }
                 }
-                if (tid == 0) s_next[0] = 0;
+                if (tid == 0) {
+                    s_next[0] = 0;
+                    s_next[1] = 0;
+                }
                 __syncthreads();
-                // segments are handed out dynamically, 32/g per warp at a time, so warps that
-                // drew short segments take more instead of idling at the batch barrier
-                (void)grp;
-                (void)ngrp;
-                for (;;) {
-                    int e0 = 0;
-                    if (lane == 0) e0 = atomicAdd(&s_next[0], 32 / g);
-                    e0 = __shfl_sync(0xffffffffu, e0, 0);
-                    if (e0 >= cnt || !ok) break;  // warp-uniform
-                    if (*vovf) {
-                        ok = false;
-                        break;
-                    }
-                    const int e = e0 + lane / g;
-                    int lo = 0, hi = 0;     // valid element window relative to the aligned base
+                const int nl = s_nl, ns = s_ns;
+                const int gS = group_size_for(ns > 0 ? s_sumS / (4 * ns) : 0);
+                // one group of g lanes per segment, 4 consecutive entries per lane per step
+                // (16-byte gathers from the 4-aligned base, head / tail masked)
+                auto walk = [&](int g, int e, bool has) {
+                    const int lane_g = lane & (g - 1);
+                    int lo = 0, hi = 0;  // valid element window relative to the aligned base
                     float bkj = 0.f;
                     const int *rp = a.arow;
                     const float *vp = a.aval;
-                    if (e < cnt) {
+                    if (has) {
                         const int64_t t0 = st_start[e];
                         const int64_t ab = t0 & ~(int64_t)3;
                         rp = a.arow + ab;
@@ -377,6 +388,32 @@ __global__ void __launch_bounds__(NT, (bin_min_blocks<CAP, NT, MODE, GLOBAL, ATO
                         if (!__all_sync(0xffffffffu, ok)) break;
                     }
                     ok = __all_sync(0xffffffffu, ok);
+                };
+                // segments are handed out dynamically, so warps that drew short segments take
+                // more instead of idling at the batch barrier: long ones one per warp (g = 32),
+                // then short ones 32/gS per warp
+                for (;;) {
+                    int e0 = 0;
+                    if (lane == 0) e0 = atomicAdd(&s_next[0], 1);
+                    e0 = __shfl_sync(0xffffffffu, e0, 0);
+                    if (e0 >= nl || !ok) break;  // warp-uniform
+                    if (*vovf) {
+                        ok = false;
+                        break;
+                    }
+                    walk(32, e0, true);
+                }
+                for (;;) {
+                    int e0 = 0;
+                    if (lane == 0) e0 = atomicAdd(&s_next[1], 32 / gS);
+                    e0 = __shfl_sync(0xffffffffu, e0, 0);
+                    if (e0 >= ns || !ok) break;  // warp-uniform
+                    if (*vovf) {
+                        ok = false;
+                        break;
+                    }
+                    const int es = e0 + lane / gS;
+                    walk(gS, NT - 1 - es, es < ns);
                 }
                 __syncthreads();
             }
