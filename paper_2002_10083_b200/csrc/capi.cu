@@ -65,6 +65,7 @@ struct mcl_ctx {
     bool validate = false;                    // MCLX_VALIDATE=1: check input CSC invariants
     bool split_cand = true;                   // MCLX_SPLIT_CAND=0: split parts stage every entry
     double esc_cf = 1.5;                      // MCLX_ESC_CF: cf below which a small column runs ESC (0: off)
+    double esc_iter_cf = 2.0;                 // MCLX_ESC_ITER_CF: ... when the product's cf is below this
     int force_phases = 0;                     // MCLX_PHASES=h forces h column batches (tests)
     int64_t phase_budget = -1;                // MCLX_PHASE_BUDGET_MB: bytes per batch (else
                                               // mem_safety x free HBM)
@@ -532,8 +533,13 @@ int run_split(mcl_ctx *c, const Prod &pr, int nsplit, int32_t *split_list,
 // Classify the columns of a product into bins and run every bin kernel in `mode`;
 // columns whose table overflowed (estimate too small) are re-binned with the exact
 // bound min(f_j, m) and re-run.  `base` carries the mode's outputs.
+// product_cf: the multiplication's estimated compression factor (flops / sum of the size
+// estimates; <= 0 unknown).  The ESC kernel is considered only for a product whose cf is below
+// c->esc_iter_cf -- HipMCL's hybrid picks the kernel per multiplication by cf (P:789-794,
+// P:812-815) -- and then per column (c->esc_cf).
 int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float *est,
-             const int64_t *exact, int force_bin, BinArgs base, mcl_stats_t *st) {
+             const int64_t *exact, int force_bin, BinArgs base, mcl_stats_t *st,
+             double product_cf = -1.0) {
     const int64_t n = pr.n;
     const int NB1 = kAllBins;  // both kernel families
     int *counts, *counters, *retry_count, *err;
@@ -558,7 +564,8 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
     unsigned long long *esc_flops = bflops + 3 * NB1, *esc_out = esc_flops + 1;
     int *esc_count = counts + 2 * NB1 + 2, *esc_counter = esc_count + 1;
     int32_t *esc_list = nullptr;
-    const bool use_esc = c->esc_cf > 0.0 && mode != kPart;
+    const bool use_esc = c->esc_cf > 0.0 && mode != kPart &&
+                         (product_cf > 0.0 ? product_cf : 1e300) < c->esc_iter_cf;
     if (use_esc) RC(scratch_t(c, "esc_list", (size_t)std::max<int64_t>(n, 1), &esc_list));
     RC(scratch_t(c, "bin_lists", (size_t)NB1 * std::max<int64_t>(n, 1), &lists));
     RC(scratch_t(c, "gcap_col", (size_t)std::max<int64_t>(n, 1), &gcap_col));
@@ -1389,6 +1396,7 @@ int mcl_ctx_create(mcl_ctx_t *out, int device, void *stream, mcl_alloc_fn alloc,
     if (const char *e = getenv("MCLX_FAMILY")) c->family = atoi(e);
     if (const char *e = getenv("MCLX_SPLIT_CAND")) c->split_cand = atoi(e) != 0;
     if (const char *e = getenv("MCLX_ESC_CF")) c->esc_cf = atof(e);
+    if (const char *e = getenv("MCLX_ESC_ITER_CF")) c->esc_iter_cf = atof(e);
     if (const char *e = getenv("MCLX_PHASES")) c->force_phases = atoi(e);
     if (const char *e = getenv("MCLX_PHASE_BUDGET_MB")) c->phase_budget = (int64_t)atoll(e) << 20;
     if (ensure_pin(c, &c->pin, &c->pin_bytes, kPinBytes) != MCL_OK ||
@@ -1733,7 +1741,7 @@ static int iterate_range_impl(mcl_ctx_t c, const mcl_csc_t *A, int64_t col_begin
         for (int b = 0; b <= kNumBins; b++) st->bin_cols[b] = st->bin_flops[b] = 0;
     }
     RC(run_bins(c, kFused, pr, f, use_exact ? nullptr : est, use_exact ? nnzc : nullptr,
-                p.force_bin, base, st));
+                p.force_bin, base, st, cf_est));
     CK(cudaEventRecord(c->ev[4], c->stream));
     // a8: assemble A_next
     int64_t nnz = 0;

@@ -443,9 +443,10 @@ def test_iterate_split_columns_all_entries(monkeypatch, graph):
 @pytest.mark.parametrize("seed", range(3))
 def test_esc_low_cf_columns(monkeypatch, seed):
     """Expand-sort-compress (kernels_esc.cu), forced onto every column with <= 1024 products
-    (MCLX_ESC_CF huge): unpruned product bit-exact in structure, exact symbolic counts, and the
-    fused iterate equal to the oracle's."""
+    (MCLX_ESC_CF huge, and the per-product gate MCLX_ESC_ITER_CF open): unpruned product
+    bit-exact in structure, exact symbolic counts, and the fused iterate equal to the oracle's."""
     monkeypatch.setenv("MCLX_ESC_CF", "1e9")
+    monkeypatch.setenv("MCLX_ESC_ITER_CF", "1e30")
     rng = np.random.default_rng(70 + seed)
     n = int(rng.integers(200, 3000))
     A = synth.random_sparse(n, n, float(rng.uniform(0.002, 0.01)), seed=seed, empty_cols=0.05,
