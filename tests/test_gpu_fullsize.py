@@ -147,6 +147,8 @@ def test_fullsize_parity(cfg, it):
     """P1 on all columns (check_p1_all_columns), then P1 rows + P2 values of sampled
     unpruned columns (mcl_spgemm on the gathered columns: the expansion kernels) and P3 of
     the fused mcl_iterate output on the same columns."""
+    if f"nnz_{cfg}_it{it}" not in META:
+        pytest.skip(f"tests/golden has no oracle cache for {cfg} it{it} (tools/oracle_cache.py)")
     A = iterate_input(cfg, it)
     check_p1_all_columns(cfg, it, A)
     nrand, nheavy = SAMPLE[(cfg, it)]

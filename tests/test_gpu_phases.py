@@ -15,7 +15,7 @@ import torch
 
 import oracle as O
 import synth
-from test_gpu_parity import dev, f32, host_mat, kept_parity
+from test_gpu_parity import c1_it1, dev, f32, host_mat, kept_parity, oexp, opi
 
 pytestmark = pytest.mark.gpu
 
@@ -32,9 +32,7 @@ def _params(prm):
 
 def _input(name):
     if name == "C1it1":  # C1's first iterate: dense columns, every bin
-        A0 = O.preprocess(synth.planted_partition())
-        A1, _ = O.prune_inflate(O.expand(A0)[0], 1e-4, 1100, 1400, 0.9, 2.0)
-        return f32(A1), CASES["C1"]
+        return c1_it1(), CASES["C1"]
     return f32(O.preprocess(synth.config_graph(name))), CASES[name]
 
 
@@ -45,8 +43,8 @@ def test_iterate_phase_invariance(monkeypatch, name, h):
     A, prm = _input(name)
     ctx = M.Context()
     Ag, st = ctx.iterate(dev(A), _params(prm))
-    Cr, fl = O.expand(A)
-    _, info = O.prune_inflate(Cr, *prm, 2.0)
+    Cr, fl = oexp(A)
+    _, info = opi(Cr, *prm, 2.0)
     kept_parity(host_mat(Ag), Cr, info, prm)
     assert st["phases"] == h
     assert st["flops"] == int(fl.sum())
@@ -66,8 +64,8 @@ def test_iterate_phases_from_budget(monkeypatch):
     np.add.at(f, np.repeat(np.arange(A.ncols), deg), deg[A.rows])
     need = int((16 * np.minimum(np.minimum(f, A.nrows), max(prm[1], prm[2])) + 16).sum())
     assert st["phases"] == -(-need // (1 << 20))
-    Cr, _ = O.expand(A)
-    _, info = O.prune_inflate(Cr, *prm, 2.0)
+    Cr, _ = oexp(A)
+    _, info = opi(Cr, *prm, 2.0)
     kept_parity(host_mat(Ag), Cr, info, prm)
     ctx.close()
 
@@ -87,8 +85,8 @@ def test_summa_staged_1x1(monkeypatch, name, phases, form):
     ctx.set_grid(1, 1, 0, M.nccl_unique_id())
     blk = ctx.block(dev(A), (0, A.nrows), (0, A.ncols))
     Ag, st = ctx.summa_iterate(blk, _params(prm))
-    Cr, fl = O.expand(A)
-    _, info = O.prune_inflate(Cr, *prm, 2.0)
+    Cr, fl = oexp(A)
+    _, info = opi(Cr, *prm, 2.0)
     kept_parity(host_mat(Ag), Cr, info, prm)
     assert st["stages"] == 4 and st["phases"] == phases
     assert st["flops"] == int(fl.sum())
