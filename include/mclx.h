@@ -257,6 +257,24 @@ int mcl_ctx_set_grid(mcl_ctx_t ctx, int pr, int pc, int rank, const unsigned cha
 int mcl_summa_iterate(mcl_ctx_t ctx, const mcl_csc_t *A, const mcl_params_t *p, mcl_csc_t *A_next,
                       mcl_stats_t *st);
 
+/* Host-memory-backed iteration: the Pipelined Sparse SUMMA of P:337-363
+ * §III on one GPU, for an iterate larger than the device's memory.  A_host is a square CSC in
+ * HOST memory (pinned memory lets the copies run asynchronously).  The output columns run in
+ * `phases` batches of near-equal nnz; within a phase the inner dimension is cut
+ * into `stages` panels: the column panel A[:, K_q] is copied to the device on a copy stream,
+ * double-buffered so that stage q+1's copy overlaps stage q's product; the rows K_q
+ * of the phase's columns (copied once per phase) are sliced on the device; the partial
+ * products are merged on the device by Alg. 2 -- the paper merges them on the
+ * host, this library does no arithmetic on the CPU -- and the merged batch is pruned /
+ * inflated and copied back to host memory.  The device holds two A-panels, one phase's
+ * columns, its partials and staging, not A.  stages / phases <= 0: chosen from
+ * mem_safety x free HBM.  A_next_host receives pinned HOST arrays allocated by the library,
+ * freed with mcl_host_csc_release.  st->stages / phases / peak_partial; st->comm_bytes = the
+ * host -> device bytes. */
+int mcl_iterate_hostmem(mcl_ctx_t ctx, const mcl_csc_t *A_host, const mcl_params_t *p,
+                        int32_t stages, int32_t phases, mcl_csc_t *A_next_host, mcl_stats_t *st);
+int mcl_host_csc_release(mcl_csc_t *m);
+
 /* ------------------------------------------------------------------ I/O around the kernel
  * Host-side (no CUDA) ingestion of a weighted graph and the cluster output file (SURVEY §8(f)
  * row 4; SPEC S:547-559 load_graph / run).  All arrays are HOST memory owned by the struct. */

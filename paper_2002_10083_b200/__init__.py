@@ -125,6 +125,9 @@ _sig = {
     "mcl_ctx_set_grid": ([_P, C.c_int, C.c_int, C.c_int, C.c_char * 128], C.c_int),
     "mcl_summa_iterate": ([_P, C.POINTER(CscT), C.POINTER(ParamsT), C.POINTER(CscT),
                            C.POINTER(StatsT)], C.c_int),
+    "mcl_iterate_hostmem": ([_P, C.POINTER(CscT), C.POINTER(ParamsT), C.c_int32, C.c_int32,
+                             C.POINTER(CscT), C.POINTER(StatsT)], C.c_int),
+    "mcl_host_csc_release": ([C.POINTER(CscT)], C.c_int),
     "mcl_graph_read": ([C.c_char_p, C.c_int, C.POINTER(GraphT), C.c_char_p, C.c_size_t], C.c_int),
     "mcl_graph_free": ([C.POINTER(GraphT)], None),
     "mcl_clusters_write": ([C.c_char_p, _P, _i64, C.POINTER(GraphT)], C.c_int),
@@ -344,6 +347,31 @@ class Context:
                                         C.byref(st))
         self._check(rc)
         return self._adopt(out), st.as_dict()
+
+    def iterate_hostmem(self, A_host, params: Params | None = None, stages: int = 0,
+                        phases: int = 0):
+        """One MCL iteration of an iterate held in HOST memory (mcl_iterate_hostmem: column
+        panels streamed to the device, Alg. 2 on the device, pruned phases back to host).
+        A_host: any object with nrows/ncols/colptr/rows/vals (numpy); it is pinned here.
+        Returns (HostGraph of numpy arrays, stats)."""
+        self._sync_stream()
+        cp = torch.from_numpy(np.ascontiguousarray(A_host.colptr, np.int64)).pin_memory()
+        rw = torch.from_numpy(np.ascontiguousarray(A_host.rows, np.int32)).pin_memory()
+        vl = torch.from_numpy(np.ascontiguousarray(A_host.vals, np.float32)).pin_memory()
+        n = int(A_host.ncols)
+        a = CscT(int(A_host.nrows), n, int(rw.numel()), 0, 0, n, cp.data_ptr(),
+                 rw.data_ptr() if rw.numel() else None, vl.data_ptr() if vl.numel() else None)
+        out, st = CscT(), StatsT()
+        self._check(_lib.mcl_iterate_hostmem(self.h, C.byref(a), C.byref((params or Params()).c()),
+                                             int(stages), int(phases), C.byref(out), C.byref(st)))
+        try:
+            nnz = int(out.nnz)
+            ocp = np.ctypeslib.as_array(C.cast(out.col_ptr, C.POINTER(C.c_int64)), shape=(n + 1,)).copy()
+            orw = np.ctypeslib.as_array(C.cast(out.row_idx, C.POINTER(C.c_int32)), shape=(max(nnz, 1),))[:nnz].copy()
+            ovl = np.ctypeslib.as_array(C.cast(out.val, C.POINTER(C.c_float)), shape=(max(nnz, 1),))[:nnz].copy()
+        finally:
+            _lib.mcl_host_csc_release(C.byref(out))
+        return HostGraph(n, n, ocp, orw, ovl), st.as_dict()
 
     def clusters(self, A: CSC):
         self._sync_stream()

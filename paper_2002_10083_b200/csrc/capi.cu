@@ -1860,6 +1860,315 @@ int mcl_clusters(mcl_ctx_t c, const mcl_csc_t *A, int32_t *labels_dev, int64_t *
     return MCL_OK;
 }
 
+int mcl_host_csc_release(mcl_csc_t *m) {
+    if (!m) return MCL_ERR_INVALID_ARG;
+    if (m->col_ptr) cudaFreeHost(m->col_ptr);
+    if (m->row_idx) cudaFreeHost(m->row_idx);
+    if (m->val) cudaFreeHost(m->val);
+    zero_csc(m);
+    return MCL_OK;
+}
+
+// Host-memory-backed iteration: the Pipelined Sparse SUMMA of P:337-363 §III on one GPU, for
+// an iterate that does not fit the device.  See include/mclx.h.
+int mcl_iterate_hostmem(mcl_ctx_t c, const mcl_csc_t *Ah, const mcl_params_t *pin, int32_t stages,
+                        int32_t phases, mcl_csc_t *out, mcl_stats_t *st) {
+    if (!c) return MCL_ERR_INVALID_ARG;
+    if (!Ah || !pin || !out) return fail(c, MCL_ERR_INVALID_ARG, "NULL argument");
+    zero_csc(out);
+    cudaSetDevice(c->device);
+    RC(check_params(c, pin));
+    if (Ah->nrows != Ah->ncols || Ah->nrows < 0 || Ah->nnz < 0 || !Ah->col_ptr ||
+        (Ah->nnz > 0 && (!Ah->row_idx || !Ah->val)))
+        return fail(c, MCL_ERR_DIM, "A must be a square host CSC");
+    init_stats(st);
+    const int64_t launches0 = g_launches;
+    const int64_t n = Ah->ncols, nnz = Ah->nnz;
+    const PruneParams pp = prune_params(pin);
+    // sizes: an A-panel holds nnz / s entries (two of them live), a phase's B columns nnz / h
+    // plus its partial products; both cut so they stay well inside mem_safety x free HBM
+    const double budget = phase_budget(c, pin->mem_safety);
+    const int64_t s = stages > 0 ? stages
+                                 : std::max<int64_t>(1, (int64_t)std::ceil(12.0 * (double)nnz / (0.1 * budget)));
+    const int64_t h = phases > 0 ? phases
+                                 : std::max<int64_t>(1, (int64_t)std::ceil(12.0 * (double)nnz / (0.1 * budget)));
+    if (s > n && n > 0) return fail(c, MCL_ERR_INVALID_ARG, "more stages than columns");
+    cudaStream_t cs;
+    CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    cudaEvent_t ready[2], freed[2], start, stop;
+    for (int i = 0; i < 2; i++) {
+        cudaEventCreateWithFlags(&ready[i], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&freed[i], cudaEventDisableTiming);
+    }
+    cudaEventCreate(&start);
+    cudaEventCreate(&stop);
+    struct Cleanup {
+        cudaStream_t cs;
+        cudaEvent_t *ev;
+        ~Cleanup() {
+            cudaStreamSynchronize(cs);
+            cudaStreamDestroy(cs);
+            for (int i = 0; i < 6; i++) cudaEventDestroy(ev[i]);
+        }
+    } ;
+    cudaEvent_t evs[6] = {ready[0], ready[1], freed[0], freed[1], start, stop};
+    Cleanup cleanup{cs, evs};
+    CK(cudaEventRecord(start, c->stream));
+    // the phases: column batches of near-equal nnz(B_*j), cut on the device from col_ptr
+    int64_t *dcp;
+    RC(scratch_t(c, "hm_colptr", (size_t)n + 1, &dcp));
+    CK(cudaMemcpyAsync(dcp, Ah->col_ptr, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, c->stream));
+    std::vector<int64_t> bounds{0};
+    if (h > 1 && n > 0) {
+        int64_t *cut;
+        RC(scratch_t(c, "hm_cut", (size_t)h, &cut));
+        CK(launch_phase_cuts(dcp, n, (int)h, cut, c->stream));
+        std::vector<int64_t> hc((size_t)h - 1);
+        RC(readback(c, cut, sizeof(int64_t) * (h - 1), hc.data()));
+        for (int64_t v : hc)
+            if (v > bounds.back() && v < n) bounds.push_back(v);
+    }
+    bounds.push_back(n);
+    const int nph = (int)bounds.size() - 1;
+    // the A-panels (columns K_q of A, contiguous in CSC): double-buffered on the copy stream
+    int64_t max_k = 1, max_pa = 1;
+    for (int64_t q = 0; q < s; q++) {
+        const int64_t k0 = cut(n, (int)s, (int)q), k1 = cut(n, (int)s, (int)q + 1);
+        max_k = std::max(max_k, k1 - k0);
+        max_pa = std::max(max_pa, Ah->col_ptr[k1] - Ah->col_ptr[k0]);
+    }
+    struct Buf2 {
+        int64_t *cp, *cpraw;
+        int32_t *row;
+        float *val;
+    } pa[2];
+    for (int i = 0; i < 2; i++) {
+        const std::string t = std::to_string(i);
+        RC(scratch_t(c, ("hm_pa_cp" + t).c_str(), (size_t)max_k + 1, &pa[i].cp));
+        RC(scratch_t(c, ("hm_pa_cpraw" + t).c_str(), (size_t)max_k + 1, &pa[i].cpraw));
+        RC(scratch_t(c, ("hm_pa_row" + t).c_str(), (size_t)max_pa, &pa[i].row));
+        RC(scratch_t(c, ("hm_pa_val" + t).c_str(), (size_t)max_pa, &pa[i].val));
+    }
+    std::vector<mcl_csc_t> hpieces;  // pruned phases, host (pinned)
+    auto drop_host = [&]() {
+        for (auto &x : hpieces) mcl_host_csc_release(&x);
+        hpieces.clear();
+    };
+    int64_t flops = 0, nnz_unpruned = 0, peak_partial = 0, h2d = 0;
+    float chaos = 0.f;
+    int rc = MCL_OK;
+    int64_t issued = 0;  // A-panel copies issued so far (buffer = issued & 1)
+    auto issue_panel = [&](int64_t q) -> int {
+        const int64_t k0 = cut(n, (int)s, (int)q), k1 = cut(n, (int)s, (int)q + 1);
+        const int64_t a0 = Ah->col_ptr[k0], a1 = Ah->col_ptr[k1];
+        Buf2 &B = pa[issued & 1];
+        if (issued >= 2) CK(cudaStreamWaitEvent(cs, freed[issued & 1], 0));  // product done with it
+        CK(cudaMemcpyAsync(B.cpraw, Ah->col_ptr + k0, sizeof(int64_t) * (k1 - k0 + 1),
+                           cudaMemcpyHostToDevice, cs));
+        CK(launch_rebase_colptr(k1 - k0 + 1, B.cpraw, B.cp, cs));
+        if (a1 > a0) {
+            CK(cudaMemcpyAsync(B.row, Ah->row_idx + a0, sizeof(int32_t) * (a1 - a0),
+                               cudaMemcpyHostToDevice, cs));
+            CK(cudaMemcpyAsync(B.val, Ah->val + a0, sizeof(float) * (a1 - a0), cudaMemcpyHostToDevice, cs));
+        }
+        CK(cudaEventRecord(ready[issued & 1], cs));
+        h2d += (k1 - k0 + 1) * 8 + (a1 - a0) * 8;
+        issued++;
+        return MCL_OK;
+    };
+    for (int ph = 0; ph < nph && rc == MCL_OK; ph++) {
+        const int64_t c0 = bounds[ph], c1 = bounds[ph + 1], nb = c1 - c0;
+        const int64_t b0 = Ah->col_ptr[c0], b1 = Ah->col_ptr[c1];
+        // the phase's columns B = A[:, c0:c1) (copied once), sliced by rows per stage below
+        int64_t *bcp, *bcpraw, *first, *bcnt, *pbcp;
+        int32_t *brow, *pbrow;
+        float *bval, *pbval;
+        void *tmp;
+        RC(scratch_t(c, "hm_b_cp", (size_t)nb + 1, &bcp));
+        RC(scratch_t(c, "hm_b_cpraw", (size_t)nb + 1, &bcpraw));
+        RC(scratch_t(c, "hm_b_row", (size_t)std::max<int64_t>(b1 - b0, 1), &brow));
+        RC(scratch_t(c, "hm_b_val", (size_t)std::max<int64_t>(b1 - b0, 1), &bval));
+        RC(scratch_t(c, "hm_first", (size_t)std::max<int64_t>(nb, 1), &first));
+        RC(scratch_t(c, "hm_bcnt", (size_t)std::max<int64_t>(nb, 1), &bcnt));
+        RC(scratch_t(c, "hm_pb_cp", (size_t)nb + 1, &pbcp));
+        RC(scratch_t(c, "hm_pb_row", (size_t)std::max<int64_t>(b1 - b0, 1), &pbrow));
+        RC(scratch_t(c, "hm_pb_val", (size_t)std::max<int64_t>(b1 - b0, 1), &pbval));
+        RC(scratch(c, "scan_tmp", scan_tmp_bytes(nb + 1), &tmp));
+        CK(cudaMemcpyAsync(bcpraw, Ah->col_ptr + c0, sizeof(int64_t) * (nb + 1), cudaMemcpyHostToDevice,
+                           c->stream));
+        CK(launch_rebase_colptr(nb + 1, bcpraw, bcp, c->stream));
+        if (b1 > b0) {
+            CK(cudaMemcpyAsync(brow, Ah->row_idx + b0, sizeof(int32_t) * (b1 - b0), cudaMemcpyHostToDevice,
+                               c->stream));
+            CK(cudaMemcpyAsync(bval, Ah->val + b0, sizeof(float) * (b1 - b0), cudaMemcpyHostToDevice,
+                               c->stream));
+        }
+        h2d += (nb + 1) * 8 + (b1 - b0) * 8;
+        std::vector<mcl_csc_t> stack;
+        int64_t live = 0;
+        if (ph == 0) RC(issue_panel(0));
+        for (int64_t q = 0; q < s && rc == MCL_OK; q++) {
+            // the next A-panel streams in while this stage multiplies
+            const int64_t qn = q + 1 < s ? q + 1 : (ph + 1 < nph ? 0 : -1);
+            const int cur = (int)((issued - 1) & 1);
+            if (qn >= 0 && (rc = issue_panel(qn)) != MCL_OK) break;
+            const int64_t k0 = cut(n, (int)s, (int)q), k1 = cut(n, (int)s, (int)q + 1);
+            CK(cudaStreamWaitEvent(c->stream, ready[cur], 0));
+            // rows K_q of the phase's columns
+            CK(launch_rowslice_count(nb, bcp, brow, k0, k1, first, bcnt, c->stream));
+            CK(launch_scan_i64(bcnt, pbcp, nb, tmp, c->stream));
+            int64_t nbq = 0;
+            RC(readback(c, pbcp + nb, sizeof(int64_t), &nbq));
+            CK(launch_rowslice_copy(nb, first, pbcp, brow, bval, k0, pbrow, pbval, c->stream));
+            mcl_csc_t Pa, Pb, Pq;
+            zero_csc(&Pa);
+            zero_csc(&Pb);
+            Pa.nrows = n;
+            Pa.ncols = k1 - k0;
+            Pa.nnz = Ah->col_ptr[k1] - Ah->col_ptr[k0];
+            Pa.col0 = k0;
+            Pa.n_global = n;
+            Pa.col_ptr = pa[cur].cp;
+            Pa.row_idx = pa[cur].row;
+            Pa.val = pa[cur].val;
+            Pb.nrows = k1 - k0;
+            Pb.ncols = nb;
+            Pb.nnz = nbq;
+            Pb.row0 = k0;
+            Pb.col0 = c0;
+            Pb.n_global = n;
+            Pb.col_ptr = pbcp;
+            Pb.row_idx = pbrow;
+            Pb.val = pbval;
+            mcl_stats_t sst;
+            if ((rc = spgemm_impl(c, &Pa, &Pb, 0, nb, pin, &Pq, &sst)) != MCL_OK) break;
+            CK(cudaEventRecord(freed[cur], c->stream));
+            flops += sst.flops;
+            Pq.col0 = c0;
+            stack.push_back(Pq);
+            live += Pq.nnz;
+            peak_partial = std::max(peak_partial, live);
+            // Alg. 2: merge nmerges+1 lists at even stage counts
+            int64_t jj = q + 1;
+            int nmerges = 0;
+            while (jj % 2 == 0 && jj != 0) {
+                nmerges++;
+                jj /= 2;
+            }
+            if (nmerges > 0) {
+                std::vector<mcl_csc_t> L(stack.end() - (nmerges + 1), stack.end());
+                mcl_csc_t merged;
+                if ((rc = merge_impl(c, (int32_t)L.size(), L.data(), &merged)) != MCL_OK) break;
+                for (auto &x : L) {
+                    live -= x.nnz;
+                    free_csc(c, &x);
+                }
+                stack.resize(stack.size() - L.size());
+                stack.push_back(merged);
+                live += merged.nnz;
+                peak_partial = std::max(peak_partial, live);
+            }
+        }
+        if (rc == MCL_OK && stack.size() > 1) {  // Q16
+            mcl_csc_t merged;
+            rc = merge_impl(c, (int32_t)stack.size(), stack.data(), &merged);
+            if (rc == MCL_OK) {
+                for (auto &x : stack) free_csc(c, &x);
+                stack.assign(1, merged);
+            }
+        }
+        if (rc != MCL_OK) {
+            for (auto &x : stack) free_csc(c, &x);
+            break;
+        }
+        // prune / inflate the phase on the device, then its pruned columns to host memory
+        mcl_csc_t Cb = stack[0], piece;
+        float ch = 0.f;
+        rc = dist_prune(c, &Cb, nullptr, pp, &piece, &ch);
+        nnz_unpruned += Cb.nnz;
+        free_csc(c, &Cb);
+        if (rc != MCL_OK) break;
+        chaos = std::max(chaos, ch);
+        mcl_csc_t hp;
+        zero_csc(&hp);
+        hp.nrows = n;
+        hp.ncols = nb;
+        hp.nnz = piece.nnz;
+        hp.col0 = c0;
+        hp.n_global = n;
+        cudaError_t e = cudaMallocHost(&hp.col_ptr, sizeof(int64_t) * (nb + 1));
+        if (e == cudaSuccess) e = cudaMallocHost(&hp.row_idx, sizeof(int32_t) * std::max<int64_t>(piece.nnz, 1));
+        if (e == cudaSuccess) e = cudaMallocHost(&hp.val, sizeof(float) * std::max<int64_t>(piece.nnz, 1));
+        if (e == cudaSuccess) e = cudaMemcpyAsync(hp.col_ptr, piece.col_ptr, sizeof(int64_t) * (nb + 1),
+                                                  cudaMemcpyDeviceToHost, c->stream);
+        if (e == cudaSuccess && piece.nnz)
+            e = cudaMemcpyAsync(hp.row_idx, piece.row_idx, sizeof(int32_t) * piece.nnz, cudaMemcpyDeviceToHost,
+                                c->stream);
+        if (e == cudaSuccess && piece.nnz)
+            e = cudaMemcpyAsync(hp.val, piece.val, sizeof(float) * piece.nnz, cudaMemcpyDeviceToHost, c->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+        free_csc(c, &piece);
+        hpieces.push_back(hp);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            rc = fail(c, MCL_ERR_CUDA, "hostmem phase output: %s", cudaGetErrorString(e));
+        }
+    }
+    if (rc != MCL_OK) {
+        drop_host();
+        return rc;
+    }
+    // the phases, concatenated in host memory (each phase's col_ptr is 0-based)
+    int64_t tot = 0;
+    for (auto &x : hpieces) tot += x.nnz;
+    mcl_csc_t o;
+    zero_csc(&o);
+    cudaError_t e = cudaMallocHost(&o.col_ptr, sizeof(int64_t) * (n + 1));
+    if (e == cudaSuccess) e = cudaMallocHost(&o.row_idx, sizeof(int32_t) * std::max<int64_t>(tot, 1));
+    if (e == cudaSuccess) e = cudaMallocHost(&o.val, sizeof(float) * std::max<int64_t>(tot, 1));
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        mcl_host_csc_release(&o);
+        drop_host();
+        return fail(c, MCL_ERR_OOM, "cannot allocate the host output");
+    }
+    int64_t coff = 0, off = 0;
+    o.col_ptr[0] = 0;
+    for (auto &x : hpieces) {
+        for (int64_t j = 1; j <= x.ncols; j++) o.col_ptr[coff + j] = x.col_ptr[j] + off;
+        memcpy(o.row_idx + off, x.row_idx, sizeof(int32_t) * x.nnz);
+        memcpy(o.val + off, x.val, sizeof(float) * x.nnz);
+        coff += x.ncols;
+        off += x.nnz;
+    }
+    drop_host();
+    o.nrows = n;
+    o.ncols = n;
+    o.nnz = tot;
+    o.n_global = n;
+    *out = o;
+    CK(cudaEventRecord(stop, c->stream));
+    if (st) {
+        CK(cudaEventSynchronize(stop));
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, start, stop);
+        st->ms[6] = ms;
+        st->flops = flops;
+        st->nnz_in = nnz;
+        st->nnz_unpruned = nnz_unpruned;
+        st->nnz_out = tot;
+        st->chaos = chaos;
+        st->phases = nph;
+        st->stages = (int32_t)s;
+        st->peak_partial = peak_partial;
+        st->comm_bytes = h2d;  // host -> device bytes of the panels and phase columns
+        st->peak_bytes = (int64_t)c->peak;
+        st->launches = g_launches - launches0;
+        st->estimator_used = 1;
+    }
+    return MCL_OK;
+}
+
 int mcl_merge(mcl_ctx_t c, int32_t L, const mcl_csc_t *lists, mcl_csc_t *out) {
     if (!c) return MCL_ERR_INVALID_ARG;
     if (!out || !lists || L < 1) return fail(c, MCL_ERR_INVALID_ARG, "bad merge arguments");

@@ -96,3 +96,24 @@ def test_summa_staged_1x1(monkeypatch, name, phases, form):
     assert 0 < st["peak_partial"] <= (3 if form == "staged" else 1) * Cr.nnz
     assert st["chaos"] == pytest.approx(info.chaos.max(), rel=1e-3, abs=1e-5)
     ctx.close()
+
+
+@pytest.mark.parametrize("name", ["C1it1", "C2"])
+@pytest.mark.parametrize("stages,phases", [(1, 1), (3, 1), (4, 3), (0, 0)])
+def test_iterate_hostmem(name, stages, phases):
+    """Host-memory-backed iteration (the Pipelined Sparse SUMMA of
+    P:337-363 on one GPU): A in pinned host memory, column panels streamed in, Alg. 2 merges
+    and the prune on the device, pruned phases back to host -- the oracle's iterate."""
+    A, prm = _input(name)
+    ctx = M.Context()
+    G, st = ctx.iterate_hostmem(A, _params(prm), stages=stages, phases=phases)
+    Cr, fl = oexp(A)
+    _, info = opi(Cr, *prm, 2.0)
+    kept_parity(O.Mat(G.nrows, G.ncols, G.colptr, G.rows, G.vals.astype(np.float64)), Cr, info, prm)
+    assert st["flops"] == int(fl.sum()) and st["nnz_unpruned"] == Cr.nnz
+    if stages > 0:
+        assert st["stages"] == stages and st["phases"] == phases
+        assert 0 < st["peak_partial"] <= 3 * Cr.nnz
+    assert st["chaos"] == pytest.approx(info.chaos.max(), rel=1e-3, abs=1e-5)
+    assert st["comm_bytes"] >= 8 * A.nnz  # every column panel crossed the host link
+    ctx.close()
