@@ -257,6 +257,14 @@ int mcl_ctx_set_grid(mcl_ctx_t ctx, int pr, int pc, int rank, const unsigned cha
 int mcl_summa_iterate(mcl_ctx_t ctx, const mcl_csc_t *A, const mcl_params_t *p, mcl_csc_t *A_next,
                       mcl_stats_t *st);
 
+/* The schedule mcl_summa_iterate runs (host arithmetic only; no device, no NCCL): for rank
+ * `rank` of a pr x pc grid over n vertices with s = lcm(pr, pc) x stage_mult inner panels,
+ * out[0..3] = the rank's block rows [r0, r1) and columns [c0, c1); then for every stage q,
+ * out[4 + 5q ..] = k0, k1 (the inner panel K_q), the grid column of the A-panel's owner in the
+ * rank's row, the grid row of the B-panel's owner in its column, and Alg. 2's nmerges after
+ * pushing stage q's partial.  cap: entries of out (>= 4 + 5 s).  Returns s. */
+int mcl_summa_schedule(int pr, int pc, int rank, int64_t n, int stage_mult, int64_t *out, int64_t cap);
+
 /* Host-memory-backed iteration: the Pipelined Sparse SUMMA of P:337-363
  * §III on one GPU, for an iterate larger than the device's memory.  A_host is a square CSC in
  * HOST memory (pinned memory lets the copies run asynchronously).  The output columns run in

@@ -128,6 +128,7 @@ _sig = {
     "mcl_iterate_hostmem": ([_P, C.POINTER(CscT), C.POINTER(ParamsT), C.c_int32, C.c_int32,
                              C.POINTER(CscT), C.POINTER(StatsT)], C.c_int),
     "mcl_host_csc_release": ([C.POINTER(CscT)], C.c_int),
+    "mcl_summa_schedule": ([C.c_int, C.c_int, C.c_int, _i64, C.c_int, _P, _i64], C.c_int),
     "mcl_graph_read": ([C.c_char_p, C.c_int, C.POINTER(GraphT), C.c_char_p, C.c_size_t], C.c_int),
     "mcl_graph_free": ([C.POINTER(GraphT)], None),
     "mcl_clusters_write": ([C.c_char_p, _P, _i64, C.POINTER(GraphT)], C.c_int),
@@ -494,6 +495,20 @@ def prof_read(reset: bool = True):
     v = (C.c_uint64 * 12)()
     _lib.mcl_prof_read(C.byref(v), int(reset))
     return list(v)
+
+
+def summa_schedule(pr: int, pc: int, rank: int, n: int, stage_mult: int = 1) -> dict:
+    """The 2D Sparse-SUMMA schedule of mcl_summa_iterate, from the library (host arithmetic):
+    block ranges, and per stage the inner panel, the two panel owners and Alg. 2's nmerges."""
+    cap = 4 + 5 * pr * pc * stage_mult
+    buf = (C.c_int64 * cap)()
+    s = _lib.mcl_summa_schedule(pr, pc, rank, n, stage_mult, C.cast(buf, C.c_void_p), cap)
+    if s < 0:
+        raise MclError(s, "mcl_summa_schedule")
+    v = list(buf)
+    return {"rows": (v[0], v[1]), "cols": (v[2], v[3]), "s": s,
+            "stages": [dict(k0=v[4 + 5 * q], k1=v[5 + 5 * q], a_owner_col=v[6 + 5 * q],
+                            b_owner_row=v[7 + 5 * q], nmerges=v[8 + 5 * q]) for q in range(s)]}
 
 
 def nccl_unique_id() -> bytes:

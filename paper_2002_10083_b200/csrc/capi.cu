@@ -1225,6 +1225,17 @@ int merge_impl(mcl_ctx_t c, int32_t L, const mcl_csc_t *lists, mcl_csc_t *out) {
 int64_t cut(int64_t n, int parts, int k) { return (int64_t)((__int128)k * n / parts); }
 int gcd_i(int a, int b) { return b ? gcd_i(b, a % b) : a; }
 
+// Alg. 2 lines 5-8: after pushing list i (1-based), merge nmerges + 1 lists,
+// nmerges = the number of times i halves while even
+int alg2_nmerges(int64_t i) {
+    int nm = 0;
+    while (i % 2 == 0 && i != 0) {
+        nm++;
+        i /= 2;
+    }
+    return nm;
+}
+
 // Distributed prune / select / recover / inflate of a block column set whose columns are
 // split over the ranks of `comm` (the column communicator; nullptr = whole columns).
 int dist_prune(mcl_ctx *c, const mcl_csc_t *C, ncclComm_t comm, const PruneParams &pp,
@@ -1860,6 +1871,28 @@ int mcl_clusters(mcl_ctx_t c, const mcl_csc_t *A, int32_t *labels_dev, int64_t *
     return MCL_OK;
 }
 
+int mcl_summa_schedule(int pr, int pc, int rank, int64_t n, int stage_mult, int64_t *out,
+                       int64_t cap) {
+    if (pr < 1 || pc < 1 || rank < 0 || rank >= pr * pc || n < 0 || stage_mult < 1 || !out)
+        return MCL_ERR_INVALID_ARG;
+    const int s = pr / gcd_i(pr, pc) * pc * stage_mult;
+    if (cap < 4 + 5 * (int64_t)s) return MCL_ERR_INVALID_ARG;
+    const int gi = rank / pc, gj = rank % pc;
+    out[0] = cut(n, pr, gi);
+    out[1] = cut(n, pr, gi + 1);
+    out[2] = cut(n, pc, gj);
+    out[3] = cut(n, pc, gj + 1);
+    for (int q = 0; q < s; q++) {
+        int64_t *o = out + 4 + 5 * q;
+        o[0] = cut(n, s, q);
+        o[1] = cut(n, s, q + 1);
+        o[2] = (int64_t)q * pc / s;  // the A-panel's owner: (gi, o[2]), broadcast along my row
+        o[3] = (int64_t)q * pr / s;  // the B-panel's owner: (o[3], gj), along my column
+        o[4] = alg2_nmerges(q + 1);
+    }
+    return s;
+}
+
 int mcl_host_csc_release(mcl_csc_t *m) {
     if (!m) return MCL_ERR_INVALID_ARG;
     if (m->col_ptr) cudaFreeHost(m->col_ptr);
@@ -2049,12 +2082,7 @@ int mcl_iterate_hostmem(mcl_ctx_t c, const mcl_csc_t *Ah, const mcl_params_t *pi
             live += Pq.nnz;
             peak_partial = std::max(peak_partial, live);
             // Alg. 2: merge nmerges+1 lists at even stage counts
-            int64_t jj = q + 1;
-            int nmerges = 0;
-            while (jj % 2 == 0 && jj != 0) {
-                nmerges++;
-                jj /= 2;
-            }
+            const int nmerges = alg2_nmerges(q + 1);
             if (nmerges > 0) {
                 std::vector<mcl_csc_t> L(stack.end() - (nmerges + 1), stack.end());
                 mcl_csc_t merged;
@@ -2584,11 +2612,7 @@ int mcl_summa_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, 
                 live_partial += Pq.nnz;
                 peak_partial = std::max(peak_partial, live_partial);
                 // Alg. 2 lines 5-14: merge nmerges+1 lists when the stage count is even
-                int jj = q + 1, nmerges = 0;
-                while (jj % 2 == 0 && jj != 0) {
-                    nmerges++;
-                    jj /= 2;
-                }
+                const int nmerges = alg2_nmerges(q + 1);
                 if (nmerges > 0) {
                     std::vector<mcl_csc_t> L(stack.end() - (nmerges + 1), stack.end());
                     mcl_csc_t merged;

@@ -1,8 +1,11 @@
-"""Multi-process (gloo, world size 2, 4 and 8 on CPU) check of the Sparse-SUMMA schedule of
-paper_2002_10083_b200.grid: every rank holds only its block, owners broadcast the panels
-named by the grid arithmetic, each rank multiplies them (oracle spgemm) and merges the
-stage partials under Alg. 2; the result must equal the oracle's A.A restricted to the
-block (C_ij = sum_k A_ik B_kj)."""
+"""Multi-process (gloo, world size 2, 4 and 8 on CPU) check of the Sparse-SUMMA schedule that
+libmclx.so's mcl_summa_iterate runs (block ranges, inner panels, panel owners, Alg. 2 merge
+points, read from the library's mcl_summa_schedule through paper_2002_10083_b200.grid): every
+rank holds only its block, owners broadcast the panels the schedule names, each rank
+multiplies them (oracle spgemm) and merges the stage partials where the schedule says; the
+result must equal the oracle's A.A restricted to the block (C_ij = sum_k A_ik
+B_kj).  The device products and NCCL broadcasts themselves are covered by the GPU tests and
+the torchrun logs (profiles/r2_mgpu/)."""
 import os
 import socket
 
@@ -13,7 +16,7 @@ import torch.multiprocessing as mp
 
 import oracle as O
 import synth
-from paper_2002_10083_b200.grid import Grid, binary_merge_schedule
+from paper_2002_10083_b200.grid import Grid
 
 
 def _sub(M, r0, r1, c0, c1):
@@ -30,12 +33,12 @@ def _sub(M, r0, r1, c0, c1):
                  np.concatenate(vals) if vals else np.zeros(0))
 
 
-def _worker(rank, world, pr, pc, port, errq):
+def _worker(rank, world, pr, pc, port, errq, mult=1):
     try:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
         dist.init_process_group("gloo", rank=rank, world_size=world)
-        g = Grid(pr, pc, rank)
+        g = Grid(pr, pc, rank, mult)
         A = O.preprocess(synth.planted_partition())
         n = A.ncols
         r0, r1 = g.rows(n)
@@ -44,7 +47,6 @@ def _worker(rank, world, pr, pc, port, errq):
         row_groups = [dist.new_group([i * pc + j for j in range(pc)]) for i in range(pr)]
         col_groups = [dist.new_group([i * pc + j for i in range(pr)]) for j in range(pc)]
         stack = []
-        sched = binary_merge_schedule(g.s)
         for q in range(g.s):
             k0, k1 = g.panel(n, q)
             ca, rb = g.a_owner_col(q), g.b_owner_row(q)
@@ -54,7 +56,7 @@ def _worker(rank, world, pr, pc, port, errq):
             dist.broadcast_object_list(pb, src=rb * pc + g.j, group=col_groups[g.j])
             P, _ = O.spgemm(pa[0], pb[0])
             stack.append(P)
-            nm = sched[q][1]
+            nm = g.nmerges(q)
             if nm:
                 L = [stack.pop() for _ in range(nm + 1)][::-1]
                 stack.append(O.merge(L))
@@ -77,13 +79,15 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("pr,pc", [(1, 2), (2, 1), (2, 2), (1, 4), (1, 8), (2, 4)])
-def test_summa_schedule_gloo(pr, pc):
+@pytest.mark.parametrize("pr,pc,mult", [(1, 2, 1), (2, 1, 1), (2, 2, 1), (1, 4, 1), (1, 8, 1),
+                                         (2, 4, 1), (2, 2, 2)])
+def test_summa_schedule_gloo(pr, pc, mult):
     ctx = mp.get_context("spawn")
     errq = ctx.Queue()
     world = pr * pc
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, pr, pc, port, errq)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, pr, pc, port, errq, mult))
+             for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
@@ -106,4 +110,14 @@ def test_grid_arithmetic_matches_paper_square_case():
     assert g.s == 4 and (g.i, g.j) == (1, 1)
     assert [g.a_owner_col(q) for q in range(4)] == [0, 1, 2, 3]
     assert [g.b_owner_row(q) for q in range(4)] == [0, 0, 1, 1]
-    assert binary_merge_schedule(4) == [(1, 0), (2, 1), (3, 0), (4, 2)]
+    assert [g.nmerges(q) for q in range(4)] == [0, 1, 0, 2]  # Alg. 2 trace
+    # every inner panel lies inside one row stripe and one column stripe (Q17)
+    for pr, pc, m in [(2, 4, 1), (4, 2, 1), (3, 2, 2)]:
+        for r in range(pr * pc):
+            g = Grid(pr, pc, r, m)
+            n = 1000
+            for q in range(g.s):
+                k0, k1 = g.panel(n, q)
+                c0, c1 = g.cols(n, g.a_owner_col(q))
+                r0, r1 = g.rows(n, g.b_owner_row(q))
+                assert c0 <= k0 < k1 <= c1 and r0 <= k0 < k1 <= r1
