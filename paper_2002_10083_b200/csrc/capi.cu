@@ -64,6 +64,7 @@ struct mcl_ctx {
     bool split_private = true;                // MCLX_SPLIT_PRIVATE=0: P <= 4 parts shared-table too
     bool validate = false;                    // MCLX_VALIDATE=1: check input CSC invariants
     bool split_cand = true;                   // MCLX_SPLIT_CAND=0: split parts stage every entry
+    int dense_min_P = 64;                     // MCLX_DENSE_MIN_P: split columns of more parts go dense
     double esc_cf = 1.5;                      // MCLX_ESC_CF: cf below which a small column runs ESC (0: off)
     double esc_iter_cf = 2.0;                 // MCLX_ESC_ITER_CF: ... when the product's cf is below this
     int force_phases = 0;                     // MCLX_PHASES=h forces h column batches (tests)
@@ -367,17 +368,18 @@ int run_split(mcl_ctx *c, const Prod &pr, int nsplit, int32_t *split_list,
     // (the private family addresses A with 32-bit offsets; its 128-way row index costs a
     // pass over A, so it is built only when enough columns use it)
     auto priv_ok = [&](int Pf) {
-        return (Pf & ~(kSplitFp64 | kSplitShared)) <= 16 && !(Pf & (kSplitFp64 | kSplitShared));
+        return (Pf & ~kSplitFlags) <= 16 && !(Pf & kSplitFlags);
     };
     int64_t npriv = 0;
     for (int s2 = 0; s2 < nsplit; s2++) npriv += priv_ok(hP[hl[s2]]);
     const bool priv = c->split_private && pr.A->nnz < ((int64_t)1 << 32) &&
                       (npriv >= 4096 || c->split_min_need != INT64_MAX);
     auto variant_of = [&](int Pf) {
-        const int P = Pf & ~(kSplitFp64 | kSplitShared);
+        const int P = Pf & ~kSplitFlags;
         return (Pf & kSplitFp64) ? 3
+               : (Pf & kSplitDense) ? 2
                : priv && priv_ok(Pf) ? 4
-               : P <= 32 ? 0 : P == 64 ? 1 : 2;
+               : P <= 32 ? 0 : 1;
     };
     const int vorder[5] = {4, 0, 1, 2, 3};
     for (int o = 4; o >= 0; o--)  // stable: variant order 4, 0, 1, 2, 3; columns keep their order
@@ -394,7 +396,7 @@ int run_split(mcl_ctx *c, const Prod &pr, int nsplit, int32_t *split_list,
     hstg.reserve((size_t)nsplit * 4 + 1);
     int64_t stg = 0;
     for (int s2 = 0; s2 < nsplit; s2++) {
-        const int v = variant_of(hP[hl[s2]]), P = hP[hl[s2]] & ~(kSplitFp64 | kSplitShared);
+        const int v = variant_of(hP[hl[s2]]), P = hP[hl[s2]] & ~kSplitFlags;
         const int parts = split_parts(hP[hl[s2]]);
         hoff[s2 + 1] = hoff[s2] + parts;
         // a dense part's slot: its rows, or twice its share of the column's size bound
@@ -661,6 +663,7 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
             ca.split_max = INT64_MAX;  // the global-table variant takes any size
             ca.split_min = c->split_min_need;
             ca.split_part_need = c->split_part_need;
+            ca.dense_min_P = c->dense_min_P;
             ca.split_count = split_count;
             ca.split_list = split_list;
             ca.split_P = split_P;
@@ -1406,6 +1409,7 @@ int mcl_ctx_create(mcl_ctx_t *out, int device, void *stream, mcl_alloc_fn alloc,
     if (const char *e = getenv("MCLX_VALIDATE")) c->validate = atoi(e) != 0;
     if (const char *e = getenv("MCLX_FAMILY")) c->family = atoi(e);
     if (const char *e = getenv("MCLX_SPLIT_CAND")) c->split_cand = atoi(e) != 0;
+    if (const char *e = getenv("MCLX_DENSE_MIN_P")) c->dense_min_P = std::max(1, std::min(64, atoi(e)));
     if (const char *e = getenv("MCLX_ESC_CF")) c->esc_cf = atof(e);
     if (const char *e = getenv("MCLX_ESC_ITER_CF")) c->esc_iter_cf = atof(e);
     if (const char *e = getenv("MCLX_PHASES")) c->force_phases = atoi(e);

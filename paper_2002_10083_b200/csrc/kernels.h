@@ -106,11 +106,14 @@ constexpr int kSweepSeg = 2048;            // segment descriptors (cursor, end, 
 constexpr int kSplitFp64 = 1 << 30;
 // split_P flag: short sub-segments, run the parts in the CTA-shared-table family
 constexpr int kSplitShared = 1 << 29;
+// split_P flag: sweep the column's row ranges with dense tiles (kernels_dense.cu)
+constexpr int kSplitDense = 1 << 28;
+constexpr int kSplitFlags = kSplitFp64 | kSplitShared | kSplitDense;
 // work items (row-range parts) of a split column from its split_P entry: the dense variants
 // (more than 64 virtual parts, or fp64) sweep kDenseParts ranges, hashed parts min(P, 32)
 __host__ __device__ inline int split_parts(int Pf) {
-    const int P = Pf & ~(kSplitFp64 | kSplitShared);
-    return ((Pf & kSplitFp64) || P > 64) ? kDenseParts : (P < 32 ? P : 32);
+    const int P = Pf & ~kSplitFlags;
+    return (Pf & (kSplitFp64 | kSplitDense)) ? kDenseParts : (P < 32 ? P : 32);
 }
 cudaError_t launch_dense_part(bool fp64, const BinArgs &a, int grid, cudaStream_t s);
 int dense_part_occupancy(bool fp64);
@@ -195,6 +198,7 @@ struct ClassifyArgs {
     int64_t split_max;       // 0 disables
     int64_t split_min;       // also split smaller columns with need > split_min (tests)
     int64_t split_part_need; // distinct rows a part is sized for (kPartNeed)
+    int dense_min_P;         // virtual part counts above this (<= 64) take the dense sweep
     int64_t fp64_terms;      // nnz(B_*j) above which a column accumulates in fp64 (kFp64Terms)
     // low-cf columns (kernels_esc.cu): f_j <= esc_max and f_j < esc_cf x (estimated or exact
     // nnz_j) run the expand-sort-compress kernel; esc_max = 0 disables

@@ -508,3 +508,17 @@ def test_esc_low_cf_columns(monkeypatch, seed):
         A1 = f32(A1)
     assert esc > 0
     ctx.close()
+
+
+@pytest.mark.parametrize("graph", ["rmat14", "C1it1"])
+def test_iterate_dense_sweep_threshold(monkeypatch, graph):
+    """Every split column swept with dense tiles (MCLX_DENSE_MIN_P=1), candidates on."""
+    monkeypatch.setenv("MCLX_DENSE_MIN_P", "1")
+    monkeypatch.setenv("MCLX_SPLIT_MIN_NEED", "100")
+    A = f32(O.preprocess(synth.rmat(scale=14, seed=4))) if graph == "rmat14" else c1_it1()
+    ctx = M.Context()
+    Ag, st = ctx.iterate(dev(A), M.Params())
+    Cr, fl = oexp(A)
+    _, info = opi(Cr, 1e-4, 1100, 1400, 0.9, 2.0)
+    kept_parity(host_mat(Ag), Cr, info, (1e-4, 1100, 1400, 0.9))
+    assert st["split_vcols"][2] == st["split_cols"] > 0
