@@ -90,6 +90,74 @@ def test_prune_invariants_and_topk(seed, params):
         np.testing.assert_allclose(np.sort(kv), np.sort(w ** 2 / (w ** 2).sum()), rtol=1e-12)
 
 
+def _cols(A):
+    return [(A.rows[A.colptr[j]:A.colptr[j + 1]], A.vals[A.colptr[j]:A.colptr[j + 1]])
+            for j in range(A.ncols)]
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_prune_branch_properties(seed):
+    """Properties of the prune branches (readings Q5-Q8) that do not restate the branch rule:
+    each would catch a flipped comparison, a swapped S / R, or a dropped branch."""
+    Cm = _random_columns(seed)
+    cols = _cols(Cm)
+    # threshold only (S large, no recovery): kept = exactly the entries >= theta, or the
+    # single largest entry when none reaches theta (Q8)
+    A, _ = O.prune_inflate(Cm, 1e-2, 10 ** 6, 0, 0.9, 2.0)
+    for (r, v), (kr, _) in zip(cols, _cols(A)):
+        if len(v) == 0:
+            continue
+        if (v >= 1e-2).any():
+            assert kr.tolist() == r[v >= 1e-2].tolist()
+        else:
+            assert len(kr) == 1 and v[np.searchsorted(r, kr[0])] == v.max()
+    # select: growing S only ever adds entries (nested kept sets), and never more than S
+    prev = None
+    for S in (1, 3, 7, 15):
+        A, _ = O.prune_inflate(Cm, 0.0, S, 0, 0.9, 2.0)
+        ks = [set(kr.tolist()) for kr, _ in _cols(A)]
+        for (r, v), k in zip(cols, ks):
+            assert len(k) == min(S, len(v))
+        if prev is not None:
+            assert all(a <= b for a, b in zip(prev, ks))
+        prev = ks
+    # every kept entry is >= every dropped one (a top set, whatever the branch)
+    for params in [(1e-2, 5, 8, 0.9), (0.05, 3, 30, 0.5), (1e-3, 2, 0, 0.9)]:
+        A, _ = O.prune_inflate(Cm, *params, 2.0)
+        for (r, v), (kr, _) in zip(cols, _cols(A)):
+            keep = np.isin(r, kr)
+            if keep.any() and (~keep).any():
+                assert v[keep].min() >= v[~keep].max()
+    # recovery: with a threshold above every entry and mass below pct, recovery keeps
+    # min(R, nnz) entries; with R = 0 the same columns keep one entry
+    A, _ = O.prune_inflate(Cm, 2.0, 10, 4, 1.0, 2.0)
+    B, _ = O.prune_inflate(Cm, 2.0, 10, 0, 1.0, 2.0)
+    for (r, v), (ka, _), (kb, _) in zip(cols, _cols(A), _cols(B)):
+        if len(v):
+            assert len(ka) == min(4, len(v)) and len(kb) == 1
+    # scale invariance: multiplying a column by c and theta, pct by c leaves A' unchanged
+    c = 8.0
+    Cs = O.Mat(Cm.nrows, Cm.ncols, Cm.colptr, Cm.rows, Cm.vals * c)
+    A1, _ = O.prune_inflate(Cm, 1e-2, 5, 8, 0.6, 2.0)
+    A2, _ = O.prune_inflate(Cs, 1e-2 * c, 5, 8, 0.6 * c, 2.0)
+    assert np.array_equal(A1.colptr, A2.colptr) and np.array_equal(A1.rows, A2.rows)
+    np.testing.assert_allclose(A1.vals, A2.vals, rtol=1e-12)
+
+
+def test_max_abs_change_dense():
+    """O.max_abs_change (SPEC S:484's alternative convergence measure, a logging helper)
+    against dense arrays: max |A - B| with absent entries = 0."""
+    for seed in range(3):
+        a = synth.random_sparse(40, 30, 0.1, seed=seed)
+        b = synth.random_sparse(40, 30, 0.1, seed=seed + 10)
+        da, db = np.zeros((40, 30)), np.zeros((40, 30))
+        for d, m in ((da, a), (db, b)):
+            for j in range(30):
+                for q in range(m.colptr[j], m.colptr[j + 1]):
+                    d[m.rows[q], j] = m.vals[q]
+        assert O.max_abs_change(O.as_mat(a), O.as_mat(b)) == pytest.approx(np.abs(da - db).max(), abs=0)
+
+
 def test_identity_fixed_point():
     n = 50
     I = synth.Csc(n, n, np.arange(n + 1, dtype=np.int64), np.arange(n, dtype=np.int32),
