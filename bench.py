@@ -32,6 +32,10 @@ import time
 
 import numpy as np
 
+# the library allocates its outputs and scratch through torch's caching allocator; large
+# phases of the pr > 1 SUMMA (C4) fragment fixed-size segments
+os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 

@@ -2715,8 +2715,8 @@ int mcl_summa_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, 
         CK(launch_affine_i64(nj, pbytes, 16, 16, pbytes, false, c->stream));
         if (pr > 1 && nj > 0) NC(ncclAllReduce(pbytes, pbytes, nj, ncclInt64, ncclMax, c->colc, c->stream));
         RC(plan_phases(c, pbytes, nj,
-                       std::min(phase_budget(c, pin->mem_safety), 2.0 * (double)c->cap_budget), bounds,
-                       &est_bytes));
+                       std::min(0.5 * phase_budget(c, pin->mem_safety), 2.0 * (double)c->cap_budget),
+                       bounds, &est_bytes));
         h = (int)bounds.size() - 1;
         for (int ph = 0; ph < h && rc == MCL_OK; ph++) {
             const int64_t c0 = bounds[ph], c1 = bounds[ph + 1];
