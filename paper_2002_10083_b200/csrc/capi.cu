@@ -390,7 +390,10 @@ int run_split(mcl_ctx *c, const Prod &pr, int nsplit, int32_t *split_list,
     // of them (exact: the column's kept set lies in the union of its parts' top-max(S, R)
     // for every branch of Alg. 1 l.4, readings Q5-Q8), so the stitched columns k_prune reads
     // are short; MCLX_SPLIT_CAND=0 stages every entry instead
-    const int cand_k = (c->split_cand && a.pp.kmax <= kCandMax) ? a.pp.kmax : 0;
+    // candidate mode (a.cand_k > 0, run_bins): the stitched columns are cut to their top
+    // max(S, R) unscaled (k_cand_select) instead of pruned, so the parts always stage candidates
+    const bool candm = a.cand_k > 0;
+    const int cand_k = ((c->split_cand || candm) && a.pp.kmax <= kCandMax) ? a.pp.kmax : 0;
     std::vector<int64_t> hoff((size_t)nsplit + 1, 0);   // first item of each column
     std::vector<int64_t> hstg;                          // staging offset of each item
     hstg.reserve((size_t)nsplit * 4 + 1);
@@ -526,8 +529,13 @@ int run_split(mcl_ctx *c, const Prod &pr, int nsplit, int32_t *split_list,
                                stg_nnz, stg_m, stg_s, fnnz, fm, fs, c->stream));
         CK(launch_split_gather(nit, stg_cnt, stg_off + item0, stg_row - hstg[item0],
                                stg_val - hstg[item0], sioff, crow, cval, c->stream));
-        CK(launch_prune(nc, ccp, crow, cval, a.soff, a.s_row, a.s_val, a.s_cnt, a.chaos,
-                        a.chaos_max, a.pp, pgrid, c->stream, colmap, out_count, fnnz, fm, fs));
+        if (candm)
+            CK(launch_cand_select(nc, ccp, crow, cval, colmap, a.cand_k, fnnz, fm, fs, a.soff, a.s_row,
+                                  a.s_val, a.s_cnt, a.stg_nnz, a.stg_m, a.stg_s, out_count, pgrid,
+                                  c->stream));
+        else
+            CK(launch_prune(nc, ccp, crow, cval, a.soff, a.s_row, a.s_val, a.s_cnt, a.chaos,
+                            a.chaos_max, a.pp, pgrid, c->stream, colmap, out_count, fnnz, fm, fs));
     }
     return MCL_OK;
 }
@@ -566,7 +574,10 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
     unsigned long long *esc_flops = bflops + 3 * NB1, *esc_out = esc_flops + 1;
     int *esc_count = counts + 2 * NB1 + 2, *esc_counter = esc_count + 1;
     int32_t *esc_list = nullptr;
-    const bool use_esc = c->esc_cf > 0.0 && mode != kPart &&
+    // candidate mode (base.cand_k > 0, kFused): every kernel writes top-max(S, R) candidates and
+    // column statistics instead of pruned columns; the ESC kernel has no such epilogue
+    const bool candm = mode == kFused && base.cand_k > 0;
+    const bool use_esc = c->esc_cf > 0.0 && mode != kPart && !candm &&
                          (product_cf > 0.0 ? product_cf : 1e300) < c->esc_iter_cf;
     if (use_esc) RC(scratch_t(c, "esc_list", (size_t)std::max<int64_t>(n, 1), &esc_list));
     RC(scratch_t(c, "bin_lists", (size_t)NB1 * std::max<int64_t>(n, 1), &lists));
@@ -602,7 +613,7 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
     // split columns (kFused only): big columns as row-range parts, see run_split
     // (the row-range parts address A with 32-bit positions)
     const bool use_split = c->split && mode == kFused && pr.A->ncols > 0 &&
-                           pr.A->nnz < ((int64_t)1 << 32);
+                           pr.A->nnz < ((int64_t)1 << 32) && (!candm || base.pp.kmax <= kCandMax);
     int32_t *split_list = nullptr, *split_P = nullptr;
     int *split_count = nullptr, *col_flag = nullptr;
     if (use_split) {
@@ -1239,10 +1250,21 @@ int alg2_nmerges(int64_t i) {
     return nm;
 }
 
+// Candidate mode of iterate_range_impl: column statistics of the unpruned product (device
+// arrays of the range's n columns: entries, entries >= theta, their fp64 mass).
+struct CandOut {
+    int64_t *nnz, *m;
+    double *s;
+};
+
 // Distributed prune / select / recover / inflate of a block column set whose columns are
 // split over the ranks of `comm` (the column communicator; nullptr = whole columns).
+// pre: C holds only each row block's top-max(S, R) candidates (iterate_range_impl's
+// candidate mode) and pre the statistics of the unpruned block columns.  Exact for every
+// branch: the kept set is the column's top-K (K <= max(S, R)) or its entries >= theta when
+// there are at most S of them, and both lie among the row blocks' top-max(S, R).
 int dist_prune(mcl_ctx *c, const mcl_csc_t *C, ncclComm_t comm, const PruneParams &pp,
-               mcl_csc_t *out, float *chaos_out) {
+               mcl_csc_t *out, float *chaos_out, const CandOut *pre = nullptr) {
     const int64_t n = C->ncols;
     const int64_t n1 = std::max<int64_t>(n, 1);
     const int grid = (int)std::min<int64_t>(n1, (int64_t)c->sms * 8);
@@ -1279,7 +1301,15 @@ int dist_prune(mcl_ctx *c, const mcl_csc_t *C, ncclComm_t comm, const PruneParam
     RC(scratch_t(c, "chaos_max", 4, &cmax));
     RC(scratch(c, "scan_tmp", scan_tmp_bytes(n + 1), &tmp));
     CK(cudaEventRecord(c->pev[0], c->stream));
-    CK(launch_dp_stats(n, C->col_ptr, C->val, pp.theta, nnz, m, sm, grid, c->stream));
+    if (pre) {  // C holds candidates: the statistics of the unpruned columns come with them
+        if (n > 0) {
+            CK(cudaMemcpyAsync(nnz, pre->nnz, sizeof(int64_t) * n, cudaMemcpyDeviceToDevice, c->stream));
+            CK(cudaMemcpyAsync(m, pre->m, sizeof(int64_t) * n, cudaMemcpyDeviceToDevice, c->stream));
+            CK(cudaMemcpyAsync(sm, pre->s, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+        }
+    } else {
+        CK(launch_dp_stats(n, C->col_ptr, C->val, pp.theta, nnz, m, sm, grid, c->stream));
+    }
     if (comm) {
         NC(ncclGroupStart());
         NC(ncclAllReduce(nnz, nnz, 2 * n1, ncclInt64, ncclSum, comm, c->stream));
@@ -1664,27 +1694,36 @@ int mcl_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, mcl_cs
 
 constexpr int kNeedPhases = 1;  // iterate_range_impl: the columns do not fit one phase
 
-// one phase of mcl_iterate_range: the fused iteration on output columns [col_begin, col_end).
+// one phase of mcl_iterate_range: the fused iteration on output columns [col_begin, col_end)
+// of A * B (B = A for the expansion).
 // check_budget: return kNeedPhases (nothing allocated) when the staging of the pruned
 // columns + A_next, 16 B x sum_j min(max(S,R), f_j, m) + 16 B x n, exceeds the phase budget.
-static int iterate_range_impl(mcl_ctx_t c, const mcl_csc_t *A, int64_t col_begin, int64_t col_end,
-                              const mcl_params_t *pin, mcl_csc_t *A_next, mcl_stats_t *st,
-                              bool check_budget = false) {
+// cand (the 2D SUMMA's row blocks): A_next receives every column's top-max(S, R) entries,
+// unscaled, and cand its statistics -- the prune needs the sums over all row blocks.
+static int iterate_range_impl(mcl_ctx_t c, const mcl_csc_t *A, const mcl_csc_t *B, int64_t col_begin,
+                              int64_t col_end, const mcl_params_t *pin, mcl_csc_t *A_next,
+                              mcl_stats_t *st, bool check_budget = false,
+                              const CandOut *cand = nullptr) {
     if (!c) return MCL_ERR_INVALID_ARG;
     if (!A_next || !pin) return fail(c, MCL_ERR_INVALID_ARG, "NULL argument");
     zero_csc(A_next);
     cudaSetDevice(c->device);
     RC(check_params(c, pin));
     RC(check_csc(c, A, "A"));
-    if (A->nrows != A->ncols) return fail(c, MCL_ERR_DIM, "mcl_iterate needs a square A");
-    if (col_begin < 0 || col_end > A->ncols || col_begin > col_end)
+    if (B == A) {
+        if (A->nrows != A->ncols) return fail(c, MCL_ERR_DIM, "mcl_iterate needs a square A");
+    } else {
+        RC(check_csc(c, B, "B"));
+        if (A->ncols != B->nrows) return fail(c, MCL_ERR_DIM, "inner dimensions differ");
+    }
+    if (col_begin < 0 || col_end > B->ncols || col_begin > col_end)
         return fail(c, MCL_ERR_DIM, "bad column range [%lld,%lld)", (long long)col_begin,
                     (long long)col_end);
     init_stats(st);
     const int64_t launches0 = g_launches;
     const mcl_params_t &p = *pin;
     const int64_t n = col_end - col_begin;
-    Prod pr{A, A, col_begin, n};
+    Prod pr{A, B, col_begin, n};
     const PruneParams pp = prune_params(pin);
     CK(cudaEventRecord(c->ev[0], c->stream));
     int64_t *f, *kcap, *soff, *cnt, *nnzc = nullptr;
@@ -1704,7 +1743,7 @@ static int iterate_range_impl(mcl_ctx_t c, const mcl_csc_t *A, int64_t col_begin
     RC(scratch(c, "scan_tmp", scan_tmp_bytes(n + 1), &tmp));
 
     // a1: flops and the total
-    CK(launch_flops(n, A->col_ptr, A->col_ptr, A->row_idx, col_begin, f, c->stream));
+    CK(launch_flops(n, A->col_ptr, B->col_ptr, B->row_idx, col_begin, f, c->stream));
     CK(launch_reduce_i64(f, n, tot, c->stream));
     CK(cudaEventRecord(c->ev[1], c->stream));
     // a2: Cohen estimate, then the P:1076-1077 policy
@@ -1752,6 +1791,16 @@ static int iterate_range_impl(mcl_ctx_t c, const mcl_csc_t *A, int64_t col_begin
     base.chaos = chaos;
     base.chaos_max = cmax;
     base.pp = pp;
+    if (cand) {  // columns without products keep zero statistics
+        base.cand_k = pp.kmax;
+        base.stg_nnz = cand->nnz;
+        base.stg_m = cand->m;
+        base.stg_s = cand->s;
+        const size_t n1 = (size_t)std::max<int64_t>(n, 1);
+        CK(cudaMemsetAsync(cand->nnz, 0, sizeof(int64_t) * n1, c->stream));
+        CK(cudaMemsetAsync(cand->m, 0, sizeof(int64_t) * n1, c->stream));
+        CK(cudaMemsetAsync(cand->s, 0, sizeof(double) * n1, c->stream));
+    }
     if (st) {
         for (int b = 0; b <= kNumBins; b++) st->bin_cols[b] = st->bin_flops[b] = 0;
     }
@@ -1763,7 +1812,7 @@ static int iterate_range_impl(mcl_ctx_t c, const mcl_csc_t *A, int64_t col_begin
     OutGuard guard(c, A_next);
     RC(assemble(c, A->nrows, n, cnt, soff, srow, sval, A_next, &nnz));
     A_next->row0 = A->row0;
-    A_next->col0 = A->col0 + col_begin;
+    A_next->col0 = B->col0 + col_begin;
     A_next->n_global = A->n_global ? A->n_global : A->nrows;
     CK(cudaEventRecord(c->ev[5], c->stream));
     float hmax = 0.f;
@@ -1808,7 +1857,7 @@ int mcl_iterate_range(mcl_ctx_t c, const mcl_csc_t *A, int64_t col_begin, int64_
     // and the batches' outputs are concatenated.
     const int64_t n = col_end - col_begin;
     if (c->force_phases <= 1) {  // one phase unless it would not fit (checked inside)
-        const int rc = iterate_range_impl(c, A, col_begin, col_end, pin, A_next, st, true);
+        const int rc = iterate_range_impl(c, A, A, col_begin, col_end, pin, A_next, st, true);
         if (rc != kNeedPhases) {
             if (rc == MCL_OK && st) st->phases = 1;
             return rc;
@@ -1825,7 +1874,7 @@ int mcl_iterate_range(mcl_ctx_t c, const mcl_csc_t *A, int64_t col_begin, int64_
     RC(plan_phases(c, bytes, n, phase_budget(c, pin->mem_safety), bounds, nullptr));
     const int h = (int)bounds.size() - 1;
     if (h <= 1) {
-        const int rc = iterate_range_impl(c, A, col_begin, col_end, pin, A_next, st);
+        const int rc = iterate_range_impl(c, A, A, col_begin, col_end, pin, A_next, st);
         if (rc == MCL_OK && st) st->phases = 1;
         return rc;
     }
@@ -1835,7 +1884,7 @@ int mcl_iterate_range(mcl_ctx_t c, const mcl_csc_t *A, int64_t col_begin, int64_
     for (int q = 0; q < h && rc == MCL_OK; q++) {
         mcl_csc_t piece;
         mcl_stats_t sq;
-        rc = iterate_range_impl(c, A, col_begin + bounds[q], col_begin + bounds[q + 1], pin, &piece,
+        rc = iterate_range_impl(c, A, A, col_begin + bounds[q], col_begin + bounds[q + 1], pin, &piece,
                                 st ? &sq : nullptr);
         if (rc == MCL_OK) {
             pieces.push_back(piece);
@@ -2707,12 +2756,17 @@ int mcl_summa_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, 
         Bj.col_ptr = bjcp;
         Bj.row_idx = bjrow;
         Bj.val = bjval;
+        // fused (default): the product runs in candidate mode -- every output column's
+        // top-max(S, R) entries and the statistics of all its entries, from the same kernels as
+        // the 1-GPU fused iteration (hub columns as row-range parts) -- so the unpruned C_ij is
+        // never written; MCLX_SUMMA_UNFUSED=1 forms C_ij unpruned (spgemm) instead
+        const bool fused = getenv("MCLX_SUMMA_UNFUSED") == nullptr;
         int64_t *pbytes, *pf;
         RC(scratch_t(c, "summa_phase_bytes", (size_t)std::max<int64_t>(nj, 1), &pbytes));
         RC(scratch_t(c, "summa_phase_flops", (size_t)std::max<int64_t>(nj, 1), &pf));
         CK(launch_flops(nj, Ai.col_ptr, Bj.col_ptr, Bj.row_idx, 0, pf, c->stream));
-        CK(launch_kcap(nj, pf, mi, INT32_MAX, pbytes, c->stream));
-        CK(launch_affine_i64(nj, pbytes, 16, 16, pbytes, false, c->stream));
+        CK(launch_kcap(nj, pf, mi, fused ? pp.kmax : INT32_MAX, pbytes, c->stream));
+        CK(launch_affine_i64(nj, pbytes, 16, fused ? 40 : 16, pbytes, false, c->stream));
         if (pr > 1 && nj > 0) NC(ncclAllReduce(pbytes, pbytes, nj, ncclInt64, ncclMax, c->colc, c->stream));
         RC(plan_phases(c, pbytes, nj,
                        std::min(0.5 * phase_budget(c, pin->mem_safety), 2.0 * (double)c->cap_budget),
@@ -2722,7 +2776,17 @@ int mcl_summa_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, 
             const int64_t c0 = bounds[ph], c1 = bounds[ph + 1];
             mcl_csc_t Cb, piece;
             mcl_stats_t sst;
-            if ((rc = spgemm_impl(c, &Ai, &Bj, c0, c1, pin, &Cb, &sst)) != MCL_OK) break;
+            CandOut co{nullptr, nullptr, nullptr};
+            if (fused) {
+                const size_t nc1 = (size_t)std::max<int64_t>(c1 - c0, 1);
+                RC(scratch_t(c, "cand_nnz", nc1, &co.nnz));
+                RC(scratch_t(c, "cand_m", nc1, &co.m));
+                RC(scratch_t(c, "cand_s", nc1, &co.s));
+                rc = iterate_range_impl(c, &Ai, &Bj, c0, c1, pin, &Cb, &sst, false, &co);
+            } else {
+                rc = spgemm_impl(c, &Ai, &Bj, c0, c1, pin, &Cb, &sst);
+            }
+            if (rc != MCL_OK) break;
             flops += sst.flops;
             for (int b = 0; b <= kNumBins; b++) {
                 bin_ms[b] += sst.bin_ms[b];
@@ -2735,9 +2799,18 @@ int mcl_summa_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, 
             Cb.col0 = A->col0 + c0;
             Cb.n_global = n;
             peak_partial = std::max(peak_partial, Cb.nnz);
+            int64_t unpruned = Cb.nnz;
+            if (fused && c1 > c0) {  // the local block's unpruned entries, from the statistics
+                unsigned long long *tot;
+                RC(scratch_t(c, "tot", 4, &tot));
+                CK(launch_reduce_i64(co.nnz, c1 - c0, tot, c->stream));
+                unsigned long long hu = 0;
+                RC(readback(c, tot, sizeof hu, &hu));
+                unpruned = (int64_t)hu;
+            }
             float ch = 0.f;
-            rc = dist_prune(c, &Cb, pr > 1 ? c->colc : nullptr, pp, &piece, &ch);
-            nnz_unpruned += Cb.nnz;
+            rc = dist_prune(c, &Cb, pr > 1 ? c->colc : nullptr, pp, &piece, &ch, fused ? &co : nullptr);
+            nnz_unpruned += unpruned;
             free_csc(c, &Cb);
             if (rc != MCL_OK) break;
             pieces.push_back(piece);

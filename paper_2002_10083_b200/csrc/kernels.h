@@ -80,6 +80,10 @@ struct BinArgs {
     // kPart with cand_k > 0: a part stages only its top-cand_k entries (value desc, row asc;
     // cand_k = max(S, R), so the column's kept set is among them for every branch of
     // Alg. 1 l.4) and reports the statistics of ALL its entries for the branch decision
+    // kFused with cand_k > 0 (candidate mode, the 2D SUMMA's row blocks): the same epilogue per
+    // output column -- its top-cand_k entries unscaled into (soff, s_row, s_val, s_cnt) and its
+    // statistics into stg_nnz / stg_m / stg_s indexed by column; the prune runs after the
+    // column communicator has summed the statistics of all row blocks (dist_prune)
     int cand_k;
     int64_t *stg_nnz;  // [items] entries of the part
     int64_t *stg_m;    // [items] entries >= theta
@@ -250,6 +254,13 @@ cudaError_t launch_stack_identity(int64_t n, int L, int64_t *cp, int32_t *row, f
 cudaError_t launch_copy_cols(int64_t ncols, const int64_t *cnt, const int64_t *soff,
                              const int32_t *srow, const float *sval, const int64_t *cp,
                              int32_t *orow, float *oval, cudaStream_t s);
+// candidate mode: cut stitched split columns to their top-K, write them to the staging slots
+// and scatter their statistics to column-indexed arrays (onnz, om, os)
+cudaError_t launch_cand_select(int64_t ncols, const int64_t *ccp, const int32_t *crow, const float *cval,
+                               const int32_t *colmap, int K, const int64_t *fnnz, const int64_t *fm,
+                               const double *fs, const int64_t *soff, int32_t *srow, float *sval,
+                               int64_t *scnt, int64_t *onnz, int64_t *om, double *os,
+                               unsigned long long *out_count, int grid, cudaStream_t s);
 cudaError_t launch_prune(int64_t ncols, const int64_t *ccp, const int32_t *crow, const float *cval,
                          const int64_t *soff, int32_t *srow, float *sval, int64_t *scnt,
                          float *chaos, float *chaos_max, const PruneParams &pp, int grid,

@@ -780,6 +780,71 @@ __global__ void __launch_bounds__(kPruneNT)
     }
 }
 
+// Candidate mode (the fused 2D SUMMA, capi.cu): a stitched split column's candidates are cut
+// back to its top-K (value desc, row asc) and written, rows ascending, to the column's staging
+// slot; the column's statistics (nnz, m, s of all its entries) go to arrays indexed by column.
+__global__ void __launch_bounds__(kPruneNT)
+    k_cand_select(int64_t ncols, const int64_t *__restrict__ ccp, const int32_t *__restrict__ crow,
+                  const float *__restrict__ cval, const int32_t *__restrict__ colmap, int K,
+                  const int64_t *__restrict__ fnnz, const int64_t *__restrict__ fm,
+                  const double *__restrict__ fs, const int64_t *__restrict__ soff,
+                  int32_t *__restrict__ srow, float *__restrict__ sval, int64_t *__restrict__ scnt,
+                  int64_t *__restrict__ onnz, int64_t *__restrict__ om, double *__restrict__ os,
+                  unsigned long long *out_count) {
+    __shared__ unsigned hist[256];
+    __shared__ int sint[4];
+    __shared__ int sscan[kPruneNT / 32];
+    for (int64_t ci = blockIdx.x; ci < ncols; ci += gridDim.x) {
+        const int64_t col = colmap[ci];
+        if (col < 0) continue;
+        const int64_t base = ccp[ci];
+        const int n = (int)(ccp[ci + 1] - base);
+        uint32_t t = 0;
+        int rowcut = 0x7fffffff;
+        if (n > K) radix_select_topk<kPruneNT, float>(crow + base, cval + base, n, K, t, rowcut, hist, sint);
+        const int64_t dst = soff[col];
+        int kept = 0;
+        for (int c0 = 0; c0 < n; c0 += kPruneNT) {
+            const int i = c0 + threadIdx.x;
+            int f = 0, r = 0;
+            float v = 0.f;
+            if (i < n) {
+                r = crow[base + i];
+                v = cval[base + i];
+                const uint32_t b = val_bits(v);
+                f = n <= K || b > t || (b == t && r <= rowcut);
+            }
+            int tot;
+            const int pos = block_excl_scan<kPruneNT>(f, sscan, tot);
+            if (f) {
+                srow[dst + kept + pos] = r;
+                sval[dst + kept + pos] = v;
+            }
+            kept += tot;
+        }
+        if (threadIdx.x == 0) {
+            scnt[col] = kept;
+            onnz[col] = fnnz[ci];
+            om[col] = fm[ci];
+            os[col] = fs[ci];
+            if (out_count) atomicAdd(out_count, (unsigned long long)kept);
+        }
+        __syncthreads();
+    }
+}
+
+cudaError_t launch_cand_select(int64_t ncols, const int64_t *ccp, const int32_t *crow, const float *cval,
+                               const int32_t *colmap, int K, const int64_t *fnnz, const int64_t *fm,
+                               const double *fs, const int64_t *soff, int32_t *srow, float *sval,
+                               int64_t *scnt, int64_t *onnz, int64_t *om, double *os,
+                               unsigned long long *out_count, int grid, cudaStream_t s) {
+    if (ncols <= 0) return cudaSuccess;
+    ++g_launches;
+    k_cand_select<<<grid, kPruneNT, 0, s>>>(ncols, ccp, crow, cval, colmap, K, fnnz, fm, fs, soff, srow,
+                                            sval, scnt, onnz, om, os, out_count);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_prune(int64_t ncols, const int64_t *ccp, const int32_t *crow, const float *cval,
                          const int64_t *soff, int32_t *srow, float *sval, int64_t *scnt,
                          float *chaos, float *chaos_max, const PruneParams &pp, int grid,

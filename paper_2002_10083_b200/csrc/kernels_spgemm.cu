@@ -608,7 +608,10 @@ __global__ void __launch_bounds__(NT, (bin_min_blocks<CAP, NT, MODE, GLOBAL, ATO
             if (tid == 0) PROF_ADD(6, clock64() - prof_e0);  // compaction of the slices
             const long long prof_e1 = clock64();
 #endif
-            if (MODE == kPart && a.cand_k > 0) {
+            // candidate mode (kFused, cand_k > 0): the kPart candidate epilogue per column
+            const bool candm = MODE == kFused && a.cand_k > 0;
+            const int64_t sidx = MODE == kPart ? idx : col;
+            if ((MODE == kPart || candm) && a.cand_k > 0) {
                 // candidates: statistics of all the part's entries, then each warp keeps its
                 // slice's share of the part's top-cand_k (segmented radix select)
                 const double theta = a.pp.theta;
@@ -637,9 +640,9 @@ __global__ void __launch_bounds__(NT, (bin_min_blocks<CAP, NT, MODE, GLOBAL, ATO
                     sm += swd[0][w2];
                 }
                 if (tid == 0) {
-                    a.stg_nnz[idx] = nnz;
-                    a.stg_m[idx] = m;
-                    a.stg_s[idx] = sm;
+                    a.stg_nnz[sidx] = nnz;
+                    a.stg_m[sidx] = m;
+                    a.stg_s[sidx] = sm;
                 }
                 if (nnz > a.cand_k) {
                     uint32_t t = 0;
@@ -652,7 +655,7 @@ __global__ void __launch_bounds__(NT, (bin_min_blocks<CAP, NT, MODE, GLOBAL, ATO
                 }
                 __syncthreads();  // swi reuse below
             }
-            if (MODE == kNum || MODE == kPart) {
+            if (MODE == kNum || MODE == kPart || candm) {
                 if (lane == 0) swi[0][warp] = cnt_w;
                 __syncthreads();
                 int off = 0, tot = 0;
@@ -671,6 +674,13 @@ __global__ void __launch_bounds__(NT, (bin_min_blocks<CAP, NT, MODE, GLOBAL, ATO
                     }
                     orow = a.c_row + dst;
                     oval = a.c_val + dst;
+                } else if (candm) {  // the column's staging slot (tot <= min(cand_k, f_j, m))
+                    orow = a.s_row + a.soff[col];
+                    oval = a.s_val + a.soff[col];
+                    if (tid == 0) {
+                        a.s_cnt[col] = tot;
+                        atomicAdd(a.bin_out, (unsigned long long)tot);
+                    }
                 } else {  // split part: its staging slot (tot <= the 7/8 fill limit)
                     orow = a.stg_row + a.stg_off[idx];
                     oval = a.stg_val + a.stg_off[idx];
@@ -801,9 +811,12 @@ __global__ void __launch_bounds__(NT, (bin_min_blocks<CAP, NT, MODE, GLOBAL, ATO
                                   [](V v) { return (float)v; }, sscan);
                 continue;
             }
-            if (MODE == kPart) {
+            const bool candm = MODE == kFused && a.cand_k > 0;
+            if (MODE == kPart || candm) {
                 // nnz <= the 7/8 fill limit <= stg_cap.  With candidates: statistics of all
-                // entries, then only the part's top-cand_k are sorted and staged.
+                // entries, then only the part's top-cand_k are sorted and staged.  Candidate
+                // mode: the same per output column, into the column's slot.
+                const int64_t sidx = MODE == kPart ? idx : col;
                 int keep = nnz;
                 if (a.cand_k > 0) {
                     const double theta = a.pp.theta;
@@ -819,9 +832,9 @@ __global__ void __launch_bounds__(NT, (bin_min_blocks<CAP, NT, MODE, GLOBAL, ATO
                     const int m = block_sum<NT, int>(mloc, sscan);
                     const double sm = block_sum<NT, double>(sloc, sred);
                     if (tid == 0) {
-                        a.stg_nnz[idx] = nnz;
-                        a.stg_m[idx] = m;
-                        a.stg_s[idx] = sm;
+                        a.stg_nnz[sidx] = nnz;
+                        a.stg_m[sidx] = m;
+                        a.stg_s[sidx] = sm;
                     }
                     if (nnz > a.cand_k) {
                         uint32_t t = 0;
@@ -836,10 +849,18 @@ __global__ void __launch_bounds__(NT, (bin_min_blocks<CAP, NT, MODE, GLOBAL, ATO
                             sscan);
                     }
                 }
-                const int64_t dst = a.stg_off[idx];
-                sort_write<NT, V>(keys, vals, keep, (int)cap, a.stg_row + dst, a.stg_val + dst,
-                                  [](V v) { return (float)v; }, sscan);
-                if (tid == 0) a.stg_cnt[idx] = keep;
+                const int64_t dst = candm ? a.soff[col] : a.stg_off[idx];
+                sort_write<NT, V>(keys, vals, keep, (int)cap, (candm ? a.s_row : a.stg_row) + dst,
+                                  (candm ? a.s_val : a.stg_val) + dst, [](V v) { return (float)v; },
+                                  sscan);
+                if (tid == 0) {
+                    if (candm) {
+                        a.s_cnt[col] = keep;
+                        atomicAdd(a.bin_out, (unsigned long long)keep);
+                    } else {
+                        a.stg_cnt[idx] = keep;
+                    }
+                }
                 continue;
             }
 
