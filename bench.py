@@ -5,9 +5,11 @@ A "step" is one full pass of the hot path over the
 config's iterate A_0: mcl_iterate = flop count + binning, Cohen estimate (+ exact
 symbolic when the P:1076-1077 policy asks), the fused numeric hash SpGEMM whose
 epilogue thresholds / selects / recovers / inflates / renormalises each column, and
-the assembly of A_1.  With N > 1 GPUs (torchrun), the columns are partitioned across
-ranks (A replicated, the paper's intra-node scheme P:401-406) and every step ends
-with the NCCL all-gather that rebuilds A_1 on every rank (strong scaling).
+the assembly of A_1.  With N > 1 GPUs (torchrun), one step is mcl_summa_iterate on the
+north star's pr x pc grid (1x2, 2x2, 2x4 for N = 2, 4, 8; --grid overrides): NCCL panel
+broadcasts, the fused product on each rank's block, the distributed prune (strong
+scaling: the same A_0 whatever N).  --mode colpart runs the column partition with A
+replicated and an all-gather of A_1 (the paper's intra-node scheme P:401-406).
 
 metric / unit: BASELINE.json's metric, made concrete as the expansion throughput in
 GFLOP/s = 2 x multiply-adds/s, where the multiply-adds are the nontrivial products
@@ -272,7 +274,7 @@ def run_gpu(args):
     pr, pc = 1, world
     if mode == "summa":
         from paper_2002_10083_b200.grid import Grid
-        pr, pc = (int(x) for x in args.grid.split("x")) if args.grid else (1, world)
+        pr, pc = (int(x) for x in args.grid.split("x")) if args.grid else default_grid(world)
         uid = [M.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         ctx.set_grid(pr, pc, rank, uid[0])
@@ -498,7 +500,10 @@ def run_gpu(args):
                        "parallelism": "1 GPU" if world == 1 else (
                            (f"2D Sparse-SUMMA {pr}x{pc}: NCCL panel broadcasts, "
                             + ("stages accumulated in the fused kernel, local prune" if pr == 1 else
-                               "stage products + Alg. 2 device merge, distributed prune"))
+                               "stage products + Alg. 2 device merge, distributed prune"
+                               if os.environ.get("MCLX_SUMMA_STAGED") else
+                               "stages accumulated in the fused kernel's candidate mode, "
+                               "distributed prune"))
                            if mode == "summa" else
                            f"column partition x{world} (A replicated) + NCCL all-gather of A_next"),
                        "l2": "inputs larger than L2 (A0 > 126 MB), no flush",
@@ -532,6 +537,12 @@ def run_gpu(args):
     return 0
 
 
+def default_grid(world):
+    """The north star's grids (BASELINE.json north_star: 1x1, 1x2, 2x2 and 2x4) for N = 1, 2,
+    4, 8; any other N runs 1xN."""
+    return {1: (1, 1), 2: (1, 2), 4: (2, 2), 8: (2, 4)}.get(world, (1, world))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -544,8 +555,8 @@ def main():
                     help="untimed MCL iterations before the timed one (1: C3's heaviest, it1)")
     ap.add_argument("--mode", default="summa", choices=["colpart", "summa"],
                     help="N>1: the 2D Sparse-SUMMA (default) or column partition + all-gather")
-    ap.add_argument("--grid", default=None, help="pr x pc for --mode summa, e.g. 2x2 (default "
-                    "1xN: whole columns per rank, stages accumulated in the fused kernel)")
+    ap.add_argument("--grid", default=None, help="pr x pc for --mode summa, e.g. 1x4 (default: the "
+                    "north star's grids 1x2 / 2x2 / 2x4 for N = 2 / 4 / 8, else 1xN)")
     ap.add_argument("--e2e-steps", type=int, default=None,
                     help="pipelined end-to-end steps timed (default: --steps; 0 skips e2e)")
     ap.add_argument("--cpu-flops", type=float, default=5e8)

@@ -251,3 +251,27 @@ def test_clusters_spec_examples():
     assert k == 4 and lab.tolist() == [0, 1, 2, 3]
     P = O.Mat(n, n, np.arange(n + 1, dtype=np.int64), np.array([1, 2, 3, 0], np.int32), np.ones(n))
     assert O.clusters(P)[1] == 1
+
+
+@pytest.mark.parametrize("seed", range(4))
+@pytest.mark.parametrize("nblocks", [2, 3, 7])
+def test_kept_set_within_row_block_candidates(seed, nblocks):
+    """The reading behind the split parts' candidates and the fused 2D SUMMA:
+    cut a column's rows into blocks and keep each block's top-max(S, R) entries by (value
+    desc, row asc); the oracle's kept set lies in their union for every branch.  Random
+    columns with planted ties; block boundaries random."""
+    rng = np.random.default_rng(100 + seed)
+    Cm = _random_columns(seed)
+    for theta, S, R, pct in [(1e-2, 5, 8, 0.9), (0.05, 3, 30, 0.5), (1e-3, 2, 0, 0.9),
+                             (0.0, 1, 0, 0.9), (0.2, 4, 4, 0.99)]:
+        A, _ = O.prune_inflate(Cm, theta, S, R, pct, 2.0)
+        kmax = max(S, R, 1)
+        cuts = np.sort(rng.choice(np.arange(1, Cm.nrows), size=nblocks - 1, replace=False))
+        bounds = np.concatenate([[0], cuts, [Cm.nrows]])
+        for (r, v), (kr, _) in zip(_cols(Cm), _cols(A)):
+            cand = set()
+            for b0, b1 in zip(bounds[:-1], bounds[1:]):
+                sel = (r >= b0) & (r < b1)
+                rb, vb = r[sel], v[sel]
+                cand |= set(rb[np.lexsort((rb, -vb))[:kmax]].tolist())
+            assert set(kr.tolist()) <= cand
