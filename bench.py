@@ -512,6 +512,10 @@ def run_gpu(args):
                                     "symbolic": s0["ms"][2], "fused_numeric": s0["ms"][3],
                                     "assemble": s0["ms"][5]},
                        "ms_raw": s0["ms"],
+                       **({"summa_ms": {"setup_and_broadcast_wait": s0["ms"][3],
+                                        "products": s0["ms"][4], "dist_prune": s0["ms"][7]}}
+                          if mode == "summa" and pr > 1 and not os.environ.get("MCLX_SUMMA_STAGED")
+                          else {}),
                        "bin_cols": s0["bin_cols"], "bin_ms": bin_ms,
                        "bin_flops": s0["bin_flops"], "retries": int(s0["retries"]),
                        "split": {"cols": int(s0["split_cols"]), "items": int(s0["split_items"]),

@@ -114,7 +114,11 @@ typedef struct {
     int64_t bin_flops[MCL_NUM_BINS + 1];
     float ms[8];             /* per stage: 0 flops/bin, 1 estimate, 2 symbolic, 3 numeric
                                 (fused numeric+select+inflate in mcl_iterate), 4 select/inflate
-                                (unfused), 5 assemble, 6 total, 7 numeric launches count      */
+                                (unfused), 5 assemble, 6 total, 7 numeric launches count.
+                                mcl_summa_iterate with pr > 1: 0-2 and 5 the last phase's
+                                distributed prune (stats, top-K cut, kept sums, write),
+                                3 set-up (panels, broadcast wait, stacking, phase plan),
+                                4 products of all phases, 7 distributed prunes of all phases  */
     int64_t peak_bytes;      /* peak scratch bytes held by the context                          */
     int64_t launches;        /* kernels this call launched                                      */
     float bin_ms[MCL_NUM_BINS + 1];          /* device time of each bin's kernel(s) (events)    */

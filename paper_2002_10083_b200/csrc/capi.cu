@@ -2614,7 +2614,7 @@ int mcl_summa_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, 
     std::vector<mcl_csc_t> pieces;
     std::vector<mcl_csc_t> stack;
     int64_t peak_partial = 0, flops = 0, nnz_unpruned = 0;
-    float chaos = 0.f;
+    float chaos = 0.f, prod_ms = 0.f, prune_ms = 0.f;  // accumulating form: ms[4], ms[7]
     float bin_ms[kNumBins + 1] = {};
     int64_t bin_flops[kNumBins + 1] = {}, bin_cols[kNumBins + 1] = {}, bin_nnzb[kNumBins + 1] = {},
             bin_out[kNumBins + 1] = {};
@@ -2772,6 +2772,7 @@ int mcl_summa_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, 
                        std::min(0.5 * phase_budget(c, pin->mem_safety), 2.0 * (double)c->cap_budget),
                        bounds, &est_bytes));
         h = (int)bounds.size() - 1;
+        CK(cudaEventRecord(c->sev[1], c->stream));  // set-up done
         for (int ph = 0; ph < h && rc == MCL_OK; ph++) {
             const int64_t c0 = bounds[ph], c1 = bounds[ph + 1];
             mcl_csc_t Cb, piece;
@@ -2788,6 +2789,7 @@ int mcl_summa_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, 
             }
             if (rc != MCL_OK) break;
             flops += sst.flops;
+            prod_ms += sst.ms[6];
             for (int b = 0; b <= kNumBins; b++) {
                 bin_ms[b] += sst.bin_ms[b];
                 bin_flops[b] += sst.bin_flops[b];
@@ -2813,6 +2815,12 @@ int mcl_summa_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, 
             nnz_unpruned += unpruned;
             free_csc(c, &Cb);
             if (rc != MCL_OK) break;
+            if (st) {
+                float dm = 0.f;
+                CK(cudaEventSynchronize(c->pev[4]));
+                if (cudaEventElapsedTime(&dm, c->pev[0], c->pev[4]) == cudaSuccess) prune_ms += dm;
+                else cudaGetLastError();
+            }
             pieces.push_back(piece);
             chaos = std::max(chaos, ch);
         }
@@ -2862,6 +2870,15 @@ int mcl_summa_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, 
         st->ms[1] = pm[1];  // prune: top-k cut (radix histograms + all-reduces)
         st->ms[2] = pm[2];  // prune: kept sums + all-reduce
         st->ms[5] = pm[3];  // prune: write + assemble
+        st->ms[3] = st->ms[4] = st->ms[7] = -1.f;
+        if (!staged) {
+            if (cudaEventElapsedTime(&st->ms[3], c->sev[0], c->sev[1]) != cudaSuccess) {
+                cudaGetLastError();
+                st->ms[3] = -1.f;
+            }
+            st->ms[4] = prod_ms;
+            st->ms[7] = prune_ms;
+        }
         st->comm_bytes = comm_bytes;
         st->peak_partial = peak_partial;
         st->flops = flops;
