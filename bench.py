@@ -528,7 +528,8 @@ def run_gpu(args):
                                "ms": s0["esc_ms"]},
                        "phases": int(s0["phases"]),
                        "step_ms_min": min(step_ms), "step_ms_max": max(step_ms),
-                       "step_ms_median": float(np.median(step_ms))},
+                       "step_ms_median": float(np.median(step_ms)),
+                       "step_ms": [round(x, 3) for x in step_ms]},
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,

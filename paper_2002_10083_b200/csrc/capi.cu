@@ -7,6 +7,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <ctime>
+#include <functional>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -70,6 +72,7 @@ struct mcl_ctx {
     int force_phases = 0;                     // MCLX_PHASES=h forces h column batches (tests)
     int64_t phase_budget = -1;                // MCLX_PHASE_BUDGET_MB: bytes per batch (else
                                               // mem_safety x free HBM)
+    size_t free_seen = 0;                     // free HBM at the last cudaMemGetInfo (phase_budget)
     int family = -1;                          // MCLX_FAMILY=0/1 forces a kernel family (A/B runs)
 };
 
@@ -85,9 +88,45 @@ int fail(mcl_ctx *c, int code, const char *fmt, ...) {
     return code;
 }
 
+// MCLX_TRACE_SYNC=<ms>: report host syncs slower than <ms> (source line, bytes, wall ms) on
+// stderr -- a diagnostic for host stalls that leave the GPU idle
+static double g_trace_ms = -1.0;
+static void trace_init() {
+    static bool done = false;
+    if (done) return;
+    done = true;
+    if (const char *e = getenv("MCLX_TRACE_SYNC")) g_trace_ms = atof(e);
+}
+static double now_ms() {
+    struct timespec t;
+    clock_gettime(CLOCK_MONOTONIC, &t);
+    return t.tv_sec * 1e3 + t.tv_nsec * 1e-6;
+}
+
+// host gaps between traced calls (the host busy or descheduled while the GPU may idle)
+static double g_trace_last = 0.0;
+static int g_trace_last_line = 0;
+static void trace_gap(int line, double t0) {
+    if (g_trace_last > 0.0 && t0 - g_trace_last > g_trace_ms)
+        fprintf(stderr, "[mclx sync] gap line %d -> %d %.3f ms\n", g_trace_last_line, line,
+                t0 - g_trace_last);
+}
+static void trace_end(int line) {
+    g_trace_last = now_ms();
+    g_trace_last_line = line;
+}
+static void trace_call(int line, double t0) {
+    const double dt = now_ms() - t0;
+    trace_gap(line, t0);
+    if (dt > g_trace_ms) fprintf(stderr, "[mclx sync] call line %d %.3f ms\n", line, dt);
+    trace_end(line);
+}
+
 #define CK(call)                                                                              \
     do {                                                                                      \
+        const double tq_ = g_trace_ms >= 0 ? now_ms() : 0.0;                                  \
         cudaError_t e_ = (call);                                                              \
+        if (g_trace_ms >= 0) trace_call(__LINE__, tq_);                                       \
         if (e_ != cudaSuccess)                                                                \
             return fail(c, MCL_ERR_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #call,         \
                         cudaGetErrorString(e_));                                              \
@@ -103,7 +142,15 @@ void *dalloc(mcl_ctx *c, size_t bytes) {
     if (bytes == 0) bytes = 16;
     void *p = nullptr;
     if (c->alloc) {
+        trace_init();
+        const double t0 = g_trace_ms >= 0 ? now_ms() : 0.0;
         p = c->alloc(c->state, bytes, (void *)c->stream);
+        if (g_trace_ms >= 0) {
+            trace_gap(-1, t0);
+            if (now_ms() - t0 > g_trace_ms)
+                fprintf(stderr, "[mclx sync] alloc bytes %zu %.3f ms\n", bytes, now_ms() - t0);
+            trace_end(-1);
+        }
     } else if (cudaMallocAsync(&p, bytes, c->stream) != cudaSuccess) {
         cudaGetLastError();
         p = nullptr;
@@ -112,8 +159,18 @@ void *dalloc(mcl_ctx *c, size_t bytes) {
 }
 void dfree(mcl_ctx *c, void *p, size_t bytes) {
     if (!p) return;
-    if (c->free_fn) c->free_fn(c->state, p, bytes, (void *)c->stream);
-    else cudaFreeAsync(p, c->stream);
+    if (c->free_fn) {
+        const double t0 = g_trace_ms >= 0 ? now_ms() : 0.0;
+        c->free_fn(c->state, p, bytes, (void *)c->stream);
+        if (g_trace_ms >= 0) {
+            trace_gap(-2, t0);
+            if (now_ms() - t0 > g_trace_ms)
+                fprintf(stderr, "[mclx sync] free bytes %zu %.3f ms\n", bytes, now_ms() - t0);
+            trace_end(-2);
+        }
+    } else {
+        cudaFreeAsync(p, c->stream);
+    }
 }
 
 // Named, growing scratch buffers owned by the context.
@@ -184,30 +241,48 @@ int ensure_pin(mcl_ctx *c, void **buf, size_t *cap, size_t bytes) {
 }
 
 // Copy `bytes` from device to host through the mapped read-back buffer; waits for the stream.
-int readback(mcl_ctx *c, const void *dev, size_t bytes, void *host) {
+int readback_at(int line, mcl_ctx *c, const void *dev, size_t bytes, void *host) {
     if (bytes == 0) return MCL_OK;
     if (!dev) return fail(c, MCL_ERR_INVALID_ARG, "readback from a NULL device pointer");
+    trace_init();
+    const double t0 = g_trace_ms >= 0 ? now_ms() : 0.0;
     RC(ensure_pin(c, &c->pin, &c->pin_bytes, bytes));
     launch_copy_bytes(dev, c->pin, bytes, c->stream);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(c->stream));
     memcpy(host, c->pin, bytes);
+    if (g_trace_ms >= 0) {
+        const double dt = now_ms() - t0;
+        trace_gap(line, t0);
+        if (dt > g_trace_ms) fprintf(stderr, "[mclx sync] readback line %d bytes %zu %.3f ms\n", line, bytes, dt);
+        trace_end(line);
+    }
     return MCL_OK;
 }
+#define readback(...) readback_at(__LINE__, __VA_ARGS__)
 
 // Copy `bytes` from host to device through the mapped upload buffer, stream-ordered (the
 // host buffer may be reused at return; the upload buffer is reused after its copy ran).
-int upload(mcl_ctx *c, const void *host, size_t bytes, void *dev) {
+int upload_at(int line, mcl_ctx *c, const void *host, size_t bytes, void *dev) {
     if (bytes == 0) return MCL_OK;
     if (!dev) return fail(c, MCL_ERR_INVALID_ARG, "upload to a NULL device pointer");
+    trace_init();
+    const double t0 = g_trace_ms >= 0 ? now_ms() : 0.0;
     CK(cudaEventSynchronize(c->up_ev));  // the previous upload's copy has read the buffer
     RC(ensure_pin(c, &c->pin_up, &c->pin_up_bytes, bytes));
     memcpy(c->pin_up, host, bytes);
     launch_copy_bytes(c->pin_up, dev, bytes, c->stream);
     CK(cudaGetLastError());
     CK(cudaEventRecord(c->up_ev, c->stream));
+    if (g_trace_ms >= 0) {
+        const double dt = now_ms() - t0;
+        trace_gap(line, t0);
+        if (dt > g_trace_ms) fprintf(stderr, "[mclx sync] upload line %d bytes %zu %.3f ms\n", line, bytes, dt);
+        trace_end(line);
+    }
     return MCL_OK;
 }
+#define upload(...) upload_at(__LINE__, __VA_ARGS__)
 
 void zero_csc(mcl_csc_t *m) {
     if (m) memset(m, 0, sizeof *m);
@@ -1047,8 +1122,9 @@ int assemble(mcl_ctx *c, int64_t nrows, int64_t n, const int64_t *cnt, const int
 // into h batches of near-equal estimated bytes (bytes_dev: int64 [n], device) so that one
 // batch fits `budget` bytes; h = ceil(total / budget), or c->force_phases.  bounds receives
 // h + 1 column boundaries.  Two small read-backs (the total, the h - 1 cuts).
-int plan_phases(mcl_ctx *c, const int64_t *bytes_dev, int64_t n, double budget,
-                std::vector<int64_t> &bounds, int64_t *total_out) {
+int plan_phases(mcl_ctx *c, const int64_t *bytes_dev, int64_t n,
+                const std::function<double(double)> &budget_of, std::vector<int64_t> &bounds,
+                int64_t *total_out) {
     bounds.assign(1, 0);
     if (n <= 0) {
         bounds.push_back(0);
@@ -1063,8 +1139,9 @@ int plan_phases(mcl_ctx *c, const int64_t *bytes_dev, int64_t n, double budget,
     int64_t total = 0;
     RC(readback(c, prefix + n, sizeof(int64_t), &total));
     if (total_out) *total_out = total;
-    int64_t h = c->force_phases > 0 ? c->force_phases
-                                     : std::max<int64_t>(1, (int64_t)std::ceil((double)total / budget));
+    int64_t h = c->force_phases > 0
+                    ? c->force_phases
+                    : std::max<int64_t>(1, (int64_t)std::ceil((double)total / budget_of((double)total)));
     h = std::min<int64_t>(h, std::min<int64_t>(n, 4096));
     if (h > 1) {
         RC(scratch_t(c, "phase_cut", (size_t)h, &cut));
@@ -1078,14 +1155,20 @@ int plan_phases(mcl_ctx *c, const int64_t *bytes_dev, int64_t n, double budget,
     return MCL_OK;
 }
 
-// bytes a phase may use: MCLX_PHASE_BUDGET_MB, else mem_safety x the device's free memory
-double phase_budget(mcl_ctx *c, double mem_safety) {
+// bytes a phase may use: MCLX_PHASE_BUDGET_MB, else mem_safety x the device's free memory.
+// need (bytes the caller is about to compare with the budget; < 0 unknown): cudaMemGetInfo is
+// a driver round trip of ~5 ms on these boxes (50+ ms at times) during which the GPU sits idle,
+// so the free memory last seen is reused while the need stays within half of its budget.
+double phase_budget(mcl_ctx *c, double mem_safety, double need = -1.0) {
     if (c->phase_budget > 0) return (double)c->phase_budget;
+    if (need >= 0.0 && c->free_seen > 0 && need <= 0.5 * mem_safety * (double)c->free_seen)
+        return std::max(1.0, mem_safety * (double)c->free_seen);
     size_t fr = 0, tot = 0;
     if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
         cudaGetLastError();
         return 1e18;
     }
+    c->free_seen = fr;
     return std::max(1.0, mem_safety * (double)fr);
 }
 
@@ -1773,7 +1856,7 @@ static int iterate_range_impl(mcl_ctx_t c, const mcl_csc_t *A, const mcl_csc_t *
         const double bytes = 16.0 * (double)stot + 16.0 * (double)n;
         // (the free-memory query only for sizable iterations, or an explicit budget)
         if ((bytes > (double)(1 << 30) || c->phase_budget > 0) &&
-            bytes > phase_budget(c, pin->mem_safety))
+            bytes > phase_budget(c, pin->mem_safety, bytes))
             return kNeedPhases;
     }
     RC(scratch_t(c, "s_row", (size_t)std::max<int64_t>(stot, 1), &srow));
@@ -1871,7 +1954,8 @@ int mcl_iterate_range(mcl_ctx_t c, const mcl_csc_t *A, int64_t col_begin, int64_
     CK(launch_kcap(n, f, A->nrows, pp.kmax, bytes, c->stream));
     CK(launch_affine_i64(n, bytes, 16, 16, bytes, false, c->stream));
     std::vector<int64_t> bounds;
-    RC(plan_phases(c, bytes, n, phase_budget(c, pin->mem_safety), bounds, nullptr));
+    RC(plan_phases(c, bytes, n, [&](double need) { return phase_budget(c, pin->mem_safety, need); },
+                   bounds, nullptr));
     const int h = (int)bounds.size() - 1;
     if (h <= 1) {
         const int rc = iterate_range_impl(c, A, A, col_begin, col_end, pin, A_next, st);
@@ -2639,7 +2723,8 @@ int mcl_summa_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, 
             CK(launch_affine_est(nj, pest, 8.0 * 1.3 * 2.0, q == 0 ? 16 : 0, pbytes, c->stream));
         }
         if (pr > 1 && nj > 0) NC(ncclAllReduce(pbytes, pbytes, nj, ncclInt64, ncclMax, c->colc, c->stream));
-        RC(plan_phases(c, pbytes, nj, phase_budget(c, pin->mem_safety), bounds, &est_bytes));
+        RC(plan_phases(c, pbytes, nj, [&](double need) { return phase_budget(c, pin->mem_safety, need); },
+                       bounds, &est_bytes));
         h = (int)bounds.size() - 1;
         // per phase: stage products on the phase's columns, Alg. 2 binary merge, distributed
         // prune / inflate
@@ -2769,7 +2854,10 @@ int mcl_summa_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, 
         CK(launch_affine_i64(nj, pbytes, 16, fused ? 40 : 16, pbytes, false, c->stream));
         if (pr > 1 && nj > 0) NC(ncclAllReduce(pbytes, pbytes, nj, ncclInt64, ncclMax, c->colc, c->stream));
         RC(plan_phases(c, pbytes, nj,
-                       std::min(0.5 * phase_budget(c, pin->mem_safety), 2.0 * (double)c->cap_budget),
+                       [&](double need) {
+                           return std::min(0.5 * phase_budget(c, pin->mem_safety, 2.0 * need),
+                                           2.0 * (double)c->cap_budget);
+                       },
                        bounds, &est_bytes));
         h = (int)bounds.size() - 1;
         CK(cudaEventRecord(c->sev[1], c->stream));  // set-up done
