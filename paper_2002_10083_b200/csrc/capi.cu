@@ -2786,6 +2786,34 @@ int mcl_summa_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, 
         }
     } else {
         if (s > kMaxStages) return fail(c, MCL_ERR_NOT_IMPLEMENTED, "more than %d inner panels", kMaxStages);
+        // Cohen's first layer over A[rows_i, :] is split across the row
+        // communicator: rank (i, j) takes its own block's columns cols_j (while the panels
+        // are in flight), the pc pieces are broadcast on the comm stream after the panels
+        float *Mf = nullptr;
+        const int rk = pin->est_keys;
+        if (pin->estimator != 1) {
+            float *X;
+            RC(scratch_t(c, "cohen_X", (size_t)std::max<int64_t>(mi, 1) * rk, &X));
+            RC(scratch_t(c, "cohen_Mfull", (size_t)std::max<int64_t>(n, 1) * rk, &Mf));
+            CK(launch_cohen_keys(mi, A->row0, rk, pin->seed, X, nullptr, c->stream));
+            CK(launch_cohen_min(nj, A->col_ptr, A->row_idx, 0, X, rk, Mf + A->col0 * rk, nullptr,
+                                c->stream));
+            cudaEvent_t mev[2];
+            for (auto &e : mev) {
+                CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                ready.push_back(e);  // destroyed with the panels' events
+            }
+            CK(cudaEventRecord(mev[0], c->stream));
+            CK(cudaStreamWaitEvent(cs, mev[0], 0));
+            NC(ncclGroupStart());
+            for (int r = 0; r < pc; r++) {
+                const int64_t k0 = cut(n, pc, r), nk = cut(n, pc, r + 1) - k0;
+                if (nk) NC(ncclBroadcast(Mf + k0 * rk, Mf + k0 * rk, nk * rk, ncclFloat32, r, c->rowc, cs));
+            }
+            NC(ncclGroupEnd());
+            CK(cudaEventRecord(mev[1], cs));
+            CK(cudaStreamWaitEvent(c->stream, mev[1], 0));
+        }
         int64_t nnzAi = 0, nnzBj = 0;
         for (int q = 0; q < s; q++) {
             CK(cudaStreamWaitEvent(c->stream, ready[q], 0));
@@ -2871,7 +2899,12 @@ int mcl_summa_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, 
                 RC(scratch_t(c, "cand_nnz", nc1, &co.nnz));
                 RC(scratch_t(c, "cand_m", nc1, &co.m));
                 RC(scratch_t(c, "cand_s", nc1, &co.s));
+                if (Mf) {  // consumed by the phase's estimate
+                    c->cohen_M_pre = Mf;
+                    c->cohen_M_r = rk;
+                }
                 rc = iterate_range_impl(c, &Ai, &Bj, c0, c1, pin, &Cb, &sst, false, &co);
+                c->cohen_M_pre = nullptr;
             } else {
                 rc = spgemm_impl(c, &Ai, &Bj, c0, c1, pin, &Cb, &sst);
             }
