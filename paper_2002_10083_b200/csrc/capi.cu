@@ -1351,13 +1351,13 @@ int dist_prune(mcl_ctx *c, const mcl_csc_t *C, ncclComm_t comm, const PruneParam
     const int64_t n = C->ncols;
     const int64_t n1 = std::max<int64_t>(n, 1);
     const int grid = (int)std::min<int64_t>(n1, (int64_t)c->sms * 8);
-    int64_t *nnz, *m, *K, *kcnt, *soff, *kcap, *scnt;
+    int64_t *nnz, *m, *K, *kcnt, *scnt;
     double *sm, *sums;
     int8_t *mode;
-    int32_t *rem, *done, *rowcut, *srow;
+    int32_t *rem, *done, *rowcut;
     uint32_t *vpre, *rpre;
     unsigned *hist;
-    float *sval, *cmax;
+    float *cmax;
     void *tmp;
     RC(scratch_t(c, "dp_nnz", 3 * n1, &nnz));  // nnz | m | kcnt
     m = nnz + n1;
@@ -1378,8 +1378,6 @@ int dist_prune(mcl_ctx *c, const mcl_csc_t *C, ncclComm_t comm, const PruneParam
     selpos = selflag + n1;
     RC(scratch_t(c, "dp_sel", n1, &sel));
     RC(scratch_t(c, "dp_undone", 2, &undone));
-    RC(scratch_t(c, "kcap", n1, &kcap));
-    RC(scratch_t(c, "soff", n1 + 1, &soff));
     RC(scratch_t(c, "scnt", n1, &scnt));
     RC(scratch_t(c, "chaos_max", 4, &cmax));
     RC(scratch(c, "scan_tmp", scan_tmp_bytes(n + 1), &tmp));
@@ -1431,8 +1429,11 @@ int dist_prune(mcl_ctx *c, const mcl_csc_t *C, ncclComm_t comm, const PruneParam
     CK(cudaEventRecord(c->pev[2], c->stream));
     CK(launch_dp_keepstats(n, C->col_ptr, C->row_idx, C->val, C->row0, mode, vpre, rowcut, pp, kcnt,
                            sums, grid, c->stream));
-    // staging capacity per local column: the local nnz (kept <= local nnz)
-    CK(launch_kcap_cp(n, C->col_ptr, pp.kmax, kcap, c->stream));
+    // the local kept counts lay out the output directly (kcnt is all-reduced below)
+    int64_t *lcnt;
+    RC(scratch_t(c, "dp_lcnt", n1, &lcnt));
+    if (n > 0)
+        CK(cudaMemcpyAsync(lcnt, kcnt, sizeof(int64_t) * n, cudaMemcpyDeviceToDevice, c->stream));
     if (comm) {
         NC(ncclGroupStart());
         NC(ncclAllReduce(kcnt, kcnt, n1, ncclInt64, ncclSum, comm, c->stream));
@@ -1442,24 +1443,31 @@ int dist_prune(mcl_ctx *c, const mcl_csc_t *C, ncclComm_t comm, const PruneParam
                          c->stream));
         NC(ncclGroupEnd());
     }
-    CK(launch_scan_i64(kcap, soff, n, tmp, c->stream));
     CK(cudaEventRecord(c->pev[3], c->stream));
-    int64_t stot = 0;
-    RC(readback(c, soff + n, sizeof(int64_t), &stot));
-    RC(scratch_t(c, "s_row", (size_t)std::max<int64_t>(stot, 1), &srow));
-    RC(scratch_t(c, "s_val", (size_t)std::max<int64_t>(stot, 1), &sval));
+    // the kept entries go straight to the output CSC (col_ptr = scan of the local counts)
+    mcl_csc_t o;
+    zero_csc(&o);
+    OutGuard guard(c, &o);
+    o.col_ptr = (int64_t *)dalloc(c, (size_t)(n + 1) * sizeof(int64_t));
+    if (!o.col_ptr) return fail(c, MCL_ERR_OOM, "cannot allocate col_ptr");
+    CK(launch_scan_i64(lcnt, o.col_ptr, n, tmp, c->stream));
+    int64_t nnz_out = 0;
+    RC(readback(c, o.col_ptr + n, sizeof(int64_t), &nnz_out));
+    RC(alloc_rows_vals(c, &o, nnz_out));
     CK(cudaMemsetAsync(cmax, 0, sizeof(float), c->stream));
     CK(launch_dp_write(n, C->col_ptr, C->row_idx, C->val, C->row0, mode, vpre, rowcut, pp, sums,
-                       kcnt, soff, srow, sval, scnt, nullptr, cmax, grid, c->stream));
-    int64_t nnz_out = 0;
-    RC(assemble(c, C->nrows, n, scnt, soff, srow, sval, out, &nnz_out));
-    out->row0 = C->row0;
-    out->col0 = C->col0;
-    out->n_global = C->n_global;
+                       kcnt, o.col_ptr, o.row_idx, o.val, scnt, nullptr, cmax, grid, c->stream));
+    o.nrows = C->nrows;
+    o.ncols = n;
+    o.row0 = C->row0;
+    o.col0 = C->col0;
+    o.n_global = C->n_global;
     CK(cudaEventRecord(c->pev[4], c->stream));
     float h = 0.f;
     RC(readback(c, cmax, sizeof(float), &h));
     *chaos_out = h;
+    *out = o;
+    guard.release();
     return MCL_OK;
 }
 

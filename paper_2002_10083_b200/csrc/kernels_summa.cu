@@ -382,7 +382,10 @@ __device__ __forceinline__ bool dp_keep(int8_t md, float v, uint32_t grow, doubl
     return false;
 }
 
-// local sums over the kept set: count, sum v, max v, sum v^2, sum v^r
+// local sums over the kept set: count, sum v, max v, sum v^2, sum v^r.  A warp per column,
+// 4 x 32 entries per trip with the loads issued first (rows only for select columns, whose
+// cut has a row tie-break)
+constexpr int kDPU = 4;
 __global__ void __launch_bounds__(kDP) k_dp_keepstats(int64_t ncols, const int64_t *__restrict__ cp,
                                                       const int32_t *__restrict__ rows,
                                                       const float *__restrict__ vals, int64_t row0,
@@ -399,15 +402,25 @@ __global__ void __launch_bounds__(kDP) k_dp_keepstats(int64_t ncols, const int64
         const int32_t rc = rowcut[j];
         int64_t c = 0;
         double sv = 0, mx = 0, sq = 0, sr = 0;
-        for (int64_t i = a + lane; i < b; i += 32) {
-            const float v = vals[i];
-            if (dp_keep(md, v, (uint32_t)(row0 + rows[i]), pp.theta, t, rc)) {
-                const double d = (double)v;
-                c++;
-                sv += d;
-                mx = d > mx ? d : mx;
-                sq += d * d;
-                sr += pow_r(d, pp);
+        for (int64_t c0 = a; c0 < b; c0 += 32 * kDPU) {
+            float v[kDPU];
+            int r[kDPU];
+#pragma unroll
+            for (int u = 0; u < kDPU; u++) {
+                const int64_t i = c0 + u * 32 + lane;
+                v[u] = i < b ? vals[i] : -1.f;
+                r[u] = (md == 1 && i < b) ? rows[i] : 0;
+            }
+#pragma unroll
+            for (int u = 0; u < kDPU; u++) {
+                if (v[u] >= 0.f && dp_keep(md, v[u], (uint32_t)(row0 + r[u]), pp.theta, t, rc)) {
+                    const double d = (double)v[u];
+                    c++;
+                    sv += d;
+                    mx = d > mx ? d : mx;
+                    sq += d * d;
+                    sr += pow_r(d, pp);
+                }
             }
         }
         c = warp_sum(c);
@@ -437,8 +450,8 @@ cudaError_t launch_dp_keepstats(int64_t ncols, const int64_t *cp, const int32_t 
 }
 
 // Write the kept entries of every local column (row order preserved, ballot compaction)
-// with a' = v^r / sum_global v^r; chaos_j = K (max w - sum w^2) from the global sums
-// (sums = [sv][mx][sq][sr], all-reduced; K = global kept count).
+// with a' = v^r / sum_global v^r (one reciprocal per column); chaos_j = K (max w - sum w^2)
+// from the global sums (sums = [sv][mx][sq][sr], all-reduced; K = global kept count).
 __global__ void __launch_bounds__(kDP) k_dp_write(int64_t ncols, const int64_t *__restrict__ cp,
                                                   const int32_t *__restrict__ rows,
                                                   const float *__restrict__ vals, int64_t row0,
@@ -458,26 +471,29 @@ __global__ void __launch_bounds__(kDP) k_dp_write(int64_t ncols, const int64_t *
         const int8_t md = mode[j];
         const uint32_t t = vprefix[j];
         const int32_t rc = rowcut[j];
-        const double sr = gsums[3 * ncols + j];
+        const double inv = 1.0 / gsums[3 * ncols + j];
         const int64_t dst = soff[j];
         int64_t kept = 0;
-        for (int64_t c0 = a; c0 < b; c0 += 32) {
-            const int64_t i = c0 + lane;
-            bool f = false;
-            int r = 0;
-            float v = 0.f;
-            if (i < b) {
-                r = rows[i];
-                v = vals[i];
-                f = dp_keep(md, v, (uint32_t)(row0 + r), pp.theta, t, rc);
+        for (int64_t c0 = a; c0 < b; c0 += 32 * kDPU) {
+            float v[kDPU];
+            int r[kDPU];
+#pragma unroll
+            for (int u = 0; u < kDPU; u++) {
+                const int64_t i = c0 + u * 32 + lane;
+                v[u] = i < b ? vals[i] : -1.f;
+                r[u] = i < b ? rows[i] : 0;
             }
-            const unsigned bal = __ballot_sync(0xffffffffu, f);
-            if (f) {
-                const int64_t pos = dst + kept + __popc(bal & lt);
-                srow[pos] = r;
-                sval[pos] = (float)(pow_r((double)v, pp) / sr);
+#pragma unroll
+            for (int u = 0; u < kDPU; u++) {
+                const bool f = v[u] >= 0.f && dp_keep(md, v[u], (uint32_t)(row0 + r[u]), pp.theta, t, rc);
+                const unsigned bal = __ballot_sync(0xffffffffu, f);
+                if (f) {
+                    const int64_t pos = dst + kept + __popc(bal & lt);
+                    srow[pos] = r[u];
+                    sval[pos] = (float)(pow_r((double)v[u], pp) * inv);
+                }
+                kept += __popc(bal);
             }
-            kept += __popc(bal);
         }
         if (lane == 0) {
             scnt[j] = kept;
