@@ -1410,6 +1410,12 @@ int dist_prune(mcl_ctx *c, const mcl_csc_t *C, ncclComm_t comm, const PruneParam
         RC(readback(c, selflag + n - 1, sizeof(int64_t), &last[1]));
         nsel = last[0] + last[1];
     }
+    // candidate columns hold <= max(S, R) entries per rank, so every global digit count fits
+    // 16 bits: two bins per 32-bit word halve the histogram all-reduces
+    int nranks = 1;
+    if (comm && ncclCommCount(comm, &nranks) != ncclSuccess) nranks = 1 << 20;
+    const int packed = pre && (int64_t)pp.kmax * nranks < 65536 ? 1 : 0;
+    const int hw = packed ? 128 : 256;
     if (nsel > 0) {
         RC(scratch_t(c, "dp_hist", 256 * (size_t)nsel, &hist));
         const int hgrid = (int)std::min<int64_t>(nsel, (int64_t)c->sms * 8);
@@ -1421,9 +1427,9 @@ int dist_prune(mcl_ctx *c, const mcl_csc_t *C, ncclComm_t comm, const PruneParam
                 if (open == 0) break;
             }
             CK(launch_dp_hist(nsel, sel, C->col_ptr, C->row_idx, C->val, C->row0, mode, vpre, rpre,
-                              done, pass, hist, hgrid, c->stream));
-            if (comm) NC(ncclAllReduce(hist, hist, 256 * nsel, ncclUint32, ncclSum, comm, c->stream));
-            CK(launch_dp_digit(nsel, sel, hist, pass, vpre, rpre, rem, done, rowcut, c->stream));
+                              done, pass, hist, hgrid, c->stream, packed));
+            if (comm) NC(ncclAllReduce(hist, hist, hw * nsel, ncclUint32, ncclSum, comm, c->stream));
+            CK(launch_dp_digit(nsel, sel, hist, pass, vpre, rpre, rem, done, rowcut, c->stream, packed));
         }
     }
     CK(cudaEventRecord(c->pev[2], c->stream));

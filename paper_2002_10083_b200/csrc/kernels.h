@@ -303,17 +303,19 @@ cudaError_t launch_dp_stats(int64_t ncols, const int64_t *cp, const float *vals,
 cudaError_t launch_dp_branch(int64_t ncols, const int64_t *nnz, const int64_t *m, const double *sm,
                              const PruneParams &pp, int64_t *K, int8_t *mode, int32_t *rem,
                              uint32_t *prefix, int32_t *rowcut, cudaStream_t s);
+// packed: histograms as 128 words per column, bins b and b + 128 in the low / high 16 bits
+// (the caller guarantees every global count < 2^16: candidate columns, <= ranks x max(S, R))
 cudaError_t launch_dp_hist(int64_t nsel, const int32_t *sel, const int64_t *cp, const int32_t *rows,
                            const float *vals, int64_t row0, const int8_t *mode, const uint32_t *vprefix,
                            const uint32_t *rprefix, const int32_t *done, int pass, unsigned *hist,
-                           int grid, cudaStream_t s);
+                           int grid, cudaStream_t s, int packed = 0);
 cudaError_t launch_dp_sellist(int64_t ncols, const int8_t *mode, int64_t *flag, int64_t *pos,
                               int32_t *sel, void *tmp, cudaStream_t s);
 cudaError_t launch_dp_undone(int64_t nsel, const int32_t *sel, const int32_t *done,
                              unsigned long long *cnt, cudaStream_t s);
 cudaError_t launch_dp_digit(int64_t nsel, const int32_t *sel, const unsigned *hist, int pass,
                             uint32_t *vprefix, uint32_t *rprefix, int32_t *rem, int32_t *done,
-                            int32_t *rowcut, cudaStream_t s);
+                            int32_t *rowcut, cudaStream_t s, int packed = 0);
 cudaError_t launch_dp_keepstats(int64_t ncols, const int64_t *cp, const int32_t *rows,
                                 const float *vals, int64_t row0, const int8_t *mode,
                                 const uint32_t *vprefix, const int32_t *rowcut, const PruneParams &pp,

@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(kDP) k_dp_hist(int64_t nsel, const int32_t *__
                                                  const uint32_t *__restrict__ vprefix,
                                                  const uint32_t *__restrict__ rprefix,
                                                  const int32_t *__restrict__ done, int pass,
-                                                 unsigned *__restrict__ hist) {
+                                                 unsigned *__restrict__ hist, int packed) {
     __shared__ unsigned hs[kDP / 32][256];
     unsigned *h = hs[threadIdx.x >> 5];
     const int lane = lane_id();
@@ -260,19 +260,22 @@ __global__ void __launch_bounds__(kDP) k_dp_hist(int64_t nsel, const int32_t *__
             }
         }
         __syncwarp();
-        for (int i = lane; i < 256; i += 32) hist[li * 256 + i] = h[i];
+        if (packed)  // bins b and b + 128 as the low / high 16 bits (counts < 2^16 summed)
+            for (int i = lane; i < 128; i += 32) hist[li * 128 + i] = h[i] | (h[i + 128] << 16);
+        else
+            for (int i = lane; i < 256; i += 32) hist[li * 256 + i] = h[i];
         __syncwarp();
     }
 }
 cudaError_t launch_dp_hist(int64_t nsel, const int32_t *sel, const int64_t *cp, const int32_t *rows,
                            const float *vals, int64_t row0, const int8_t *mode,
                            const uint32_t *vprefix, const uint32_t *rprefix, const int32_t *done,
-                           int pass, unsigned *hist, int grid, cudaStream_t s) {
+                           int pass, unsigned *hist, int grid, cudaStream_t s, int packed) {
     if (nsel <= 0) return cudaSuccess;
     (void)grid;
     ++g_launches;
     k_dp_hist<<<dp_grid(nsel), kDP, 0, s>>>(nsel, sel, cp, rows, vals, row0, mode, vprefix, rprefix,
-                                             done, pass, hist);
+                                             done, pass, hist, packed);
     return cudaGetLastError();
 }
 
@@ -280,8 +283,9 @@ cudaError_t launch_dp_hist(int64_t nsel, const int32_t *sel, const int64_t *cp, 
 __global__ void k_dp_digit(int64_t nsel, const int32_t *__restrict__ sel,
                            const unsigned *__restrict__ hist, int pass, uint32_t *__restrict__ vprefix,
                            uint32_t *__restrict__ rprefix, int32_t *__restrict__ rem,
-                           int32_t *__restrict__ done, int32_t *__restrict__ rowcut) {
+                           int32_t *__restrict__ done, int32_t *__restrict__ rowcut, int packed) {
     __shared__ int sout[8][4];
+    __shared__ unsigned su[8][256];  // a packed histogram, unpacked
     const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lw = threadIdx.x >> 5;
     const int lane = lane_id();
@@ -289,8 +293,18 @@ __global__ void k_dp_digit(int64_t nsel, const int32_t *__restrict__ sel,
         const int64_t j = sel[li];
         if (done[j]) continue;
         const int r = rem[j];
-        if (pass < 4) find_digit<true>(hist + li * 256, r, sout[lw]);
-        else find_digit<false>(hist + li * 256, r, sout[lw]);
+        const unsigned *hj = hist + li * 256;
+        if (packed) {
+            for (int i = lane; i < 128; i += 32) {
+                const unsigned w2 = hist[li * 128 + i];
+                su[lw][i] = w2 & 0xffffu;
+                su[lw][i + 128] = w2 >> 16;
+            }
+            __syncwarp();
+            hj = su[lw];
+        }
+        if (pass < 4) find_digit<true>(hj, r, sout[lw]);
+        else find_digit<false>(hj, r, sout[lw]);
         __syncwarp();
         if (lane == 0) {
             const int d = sout[lw][0], before = sout[lw][1], eq = sout[lw][2];
@@ -318,12 +332,13 @@ __global__ void k_dp_digit(int64_t nsel, const int32_t *__restrict__ sel,
 }
 cudaError_t launch_dp_digit(int64_t nsel, const int32_t *sel, const unsigned *hist, int pass,
                             uint32_t *vprefix, uint32_t *rprefix, int32_t *rem, int32_t *done,
-                            int32_t *rowcut, cudaStream_t s) {
+                            int32_t *rowcut, cudaStream_t s, int packed) {
     if (nsel <= 0) return cudaSuccess;
     int64_t b = (nsel * 32 + 255) / 256;
     if (b > g_sms * 32) b = g_sms * 32;
     ++g_launches;
-    k_dp_digit<<<(int)b, 256, 0, s>>>(nsel, sel, hist, pass, vprefix, rprefix, rem, done, rowcut);
+    k_dp_digit<<<(int)b, 256, 0, s>>>(nsel, sel, hist, pass, vprefix, rprefix, rem, done, rowcut,
+                                      packed);
     return cudaGetLastError();
 }
 
