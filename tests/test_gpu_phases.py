@@ -117,3 +117,33 @@ def test_iterate_hostmem(name, stages, phases):
     assert st["chaos"] == pytest.approx(info.chaos.max(), rel=1e-3, abs=1e-5)
     assert st["comm_bytes"] >= 8 * A.nnz  # every column panel crossed the host link
     ctx.close()
+
+
+@pytest.mark.parametrize("graph,min_need,part_need", [("C2", 600, 0), ("C1it1", 100, 0),
+                                                      ("rmat14", 200, 0), ("rmat14", 200, 16)])
+def test_summa_candidates_split_path(monkeypatch, graph, min_need, part_need):
+    """The pr > 1 product's candidate mode through the split path -- row-range parts (private /
+    shared tables, and with part_need 16 the dense tiles) stage their top-max(S, R) plus
+    statistics, the stitched columns are cut by k_cand_select, and the distributed prune
+    finishes them -- on a forced 1 x 1 accumulating SUMMA with 2 panels, every column with
+    need > min_need split."""
+    monkeypatch.setenv("MCLX_SUMMA_ACCUM", "1")
+    monkeypatch.setenv("MCLX_SUMMA_STAGES", "2")
+    monkeypatch.setenv("MCLX_SPLIT_MIN_NEED", str(min_need))
+    if part_need:
+        monkeypatch.setenv("MCLX_SPLIT_PART_NEED", str(part_need))
+    if graph == "rmat14":
+        A, prm = f32(O.preprocess(synth.rmat(scale=14, seed=4))), CASES["C1"]
+    else:
+        A, prm = _input(graph)
+    ctx = M.Context()
+    ctx.set_grid(1, 1, 0, M.nccl_unique_id())
+    blk = ctx.block(dev(A), (0, A.nrows), (0, A.ncols))
+    Ag, st = ctx.summa_iterate(blk, _params(prm))
+    Cr, fl = oexp(A)
+    _, info = opi(Cr, *prm, 2.0)
+    kept_parity(host_mat(Ag), Cr, info, prm)
+    assert st["flops"] == int(fl.sum()) and st["nnz_unpruned"] == Cr.nnz
+    assert st["bin_cols"][6] > 0  # columns ran as split parts
+    assert st["chaos"] == pytest.approx(info.chaos.max(), rel=1e-3, abs=1e-5)
+    ctx.close()
