@@ -912,11 +912,38 @@ __global__ void k_cohen_min(int64_t ncols, const int64_t *__restrict__ cp,
 #pragma unroll
         for (int s = 0; s < 16; s++) mn[s] = INFINITY;
         const int64_t q0 = cp[c0 + col], q1 = cp[c0 + col + 1];
-        for (int64_t q = q0 + lane; q < q1; q += 32) {
-            const float *src = in + (int64_t)__ldg(row + q) * r;
+        if ((r & 1) == 0) {
+            // even r: 8-byte key loads (rows of r floats are 8-byte aligned), two entries per
+            // lane per trip so both gathers are in flight together
+            int64_t q = q0 + lane;
+            for (; q + 32 < q1; q += 64) {
+                const float2 *s0 = reinterpret_cast<const float2 *>(in + (int64_t)__ldg(row + q) * r);
+                const float2 *s1 = reinterpret_cast<const float2 *>(in + (int64_t)__ldg(row + q + 32) * r);
 #pragma unroll
-            for (int s = 0; s < 16; s++)
-                if (s < r) mn[s] = fminf(mn[s], __ldg(src + s));
+                for (int s = 0; s < 8; s++)
+                    if (2 * s < r) {
+                        const float2 a = __ldg(s0 + s), b = __ldg(s1 + s);
+                        mn[2 * s] = fminf(mn[2 * s], fminf(a.x, b.x));
+                        mn[2 * s + 1] = fminf(mn[2 * s + 1], fminf(a.y, b.y));
+                    }
+            }
+            if (q < q1) {
+                const float2 *s0 = reinterpret_cast<const float2 *>(in + (int64_t)__ldg(row + q) * r);
+#pragma unroll
+                for (int s = 0; s < 8; s++)
+                    if (2 * s < r) {
+                        const float2 a = __ldg(s0 + s);
+                        mn[2 * s] = fminf(mn[2 * s], a.x);
+                        mn[2 * s + 1] = fminf(mn[2 * s + 1], a.y);
+                    }
+            }
+        } else {
+            for (int64_t q = q0 + lane; q < q1; q += 32) {
+                const float *src = in + (int64_t)__ldg(row + q) * r;
+#pragma unroll
+                for (int s = 0; s < 16; s++)
+                    if (s < r) mn[s] = fminf(mn[s], __ldg(src + s));
+            }
         }
         double sum = 0.0;
 #pragma unroll
