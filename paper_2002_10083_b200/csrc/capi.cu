@@ -1338,6 +1338,12 @@ int alg2_nmerges(int64_t i) {
 struct CandOut {
     int64_t *nnz, *m;
     double *s;
+    // filled by iterate_range_impl: the candidates stay in its staging slots -- column j's at
+    // [start[j], start[j] + count[j]) of (row, val) -- plus their total and the unpruned total
+    const int64_t *start = nullptr, *count = nullptr;
+    const int32_t *row = nullptr;
+    const float *val = nullptr;
+    int64_t total = 0, unpruned = 0;
 };
 
 // Distributed prune / select / recover / inflate of a block column set whose columns are
@@ -1347,7 +1353,8 @@ struct CandOut {
 // branch: the kept set is the column's top-K (K <= max(S, R)) or its entries >= theta when
 // there are at most S of them, and both lie among the row blocks' top-max(S, R).
 int dist_prune(mcl_ctx *c, const mcl_csc_t *C, ncclComm_t comm, const PruneParams &pp,
-               mcl_csc_t *out, float *chaos_out, const CandOut *pre = nullptr) {
+               mcl_csc_t *out, float *chaos_out, const CandOut *pre = nullptr,
+               const int64_t *ccnt = nullptr) {
     const int64_t n = C->ncols;
     const int64_t n1 = std::max<int64_t>(n, 1);
     const int grid = (int)std::min<int64_t>(n1, (int64_t)c->sms * 8);
@@ -1378,8 +1385,8 @@ int dist_prune(mcl_ctx *c, const mcl_csc_t *C, ncclComm_t comm, const PruneParam
     selpos = selflag + n1;
     RC(scratch_t(c, "dp_sel", n1, &sel));
     RC(scratch_t(c, "dp_undone", 2, &undone));
-    RC(scratch_t(c, "scnt", n1, &scnt));
-    RC(scratch_t(c, "chaos_max", 4, &cmax));
+    RC(scratch_t(c, "dp_scnt", n1, &scnt));  // (not "scnt": the candidates' counts may live there)
+    RC(scratch_t(c, "dp_chaos_max", 4, &cmax));
     RC(scratch(c, "scan_tmp", scan_tmp_bytes(n + 1), &tmp));
     CK(cudaEventRecord(c->pev[0], c->stream));
     if (pre) {  // C holds candidates: the statistics of the unpruned columns come with them
@@ -1427,14 +1434,14 @@ int dist_prune(mcl_ctx *c, const mcl_csc_t *C, ncclComm_t comm, const PruneParam
                 if (open == 0) break;
             }
             CK(launch_dp_hist(nsel, sel, C->col_ptr, C->row_idx, C->val, C->row0, mode, vpre, rpre,
-                              done, pass, hist, hgrid, c->stream, packed));
+                              done, pass, hist, hgrid, c->stream, packed, ccnt));
             if (comm) NC(ncclAllReduce(hist, hist, hw * nsel, ncclUint32, ncclSum, comm, c->stream));
             CK(launch_dp_digit(nsel, sel, hist, pass, vpre, rpre, rem, done, rowcut, c->stream, packed));
         }
     }
     CK(cudaEventRecord(c->pev[2], c->stream));
     CK(launch_dp_keepstats(n, C->col_ptr, C->row_idx, C->val, C->row0, mode, vpre, rowcut, pp, kcnt,
-                           sums, grid, c->stream));
+                           sums, grid, c->stream, ccnt));
     // the local kept counts lay out the output directly (kcnt is all-reduced below)
     int64_t *lcnt;
     RC(scratch_t(c, "dp_lcnt", n1, &lcnt));
@@ -1462,7 +1469,7 @@ int dist_prune(mcl_ctx *c, const mcl_csc_t *C, ncclComm_t comm, const PruneParam
     RC(alloc_rows_vals(c, &o, nnz_out));
     CK(cudaMemsetAsync(cmax, 0, sizeof(float), c->stream));
     CK(launch_dp_write(n, C->col_ptr, C->row_idx, C->val, C->row0, mode, vpre, rowcut, pp, sums,
-                       kcnt, o.col_ptr, o.row_idx, o.val, scnt, nullptr, cmax, grid, c->stream));
+                       kcnt, o.col_ptr, o.row_idx, o.val, scnt, nullptr, cmax, grid, c->stream, ccnt));
     o.nrows = C->nrows;
     o.ncols = n;
     o.row0 = C->row0;
@@ -1800,7 +1807,7 @@ constexpr int kNeedPhases = 1;  // iterate_range_impl: the columns do not fit on
 static int iterate_range_impl(mcl_ctx_t c, const mcl_csc_t *A, const mcl_csc_t *B, int64_t col_begin,
                               int64_t col_end, const mcl_params_t *pin, mcl_csc_t *A_next,
                               mcl_stats_t *st, bool check_budget = false,
-                              const CandOut *cand = nullptr) {
+                              CandOut *cand = nullptr) {
     if (!c) return MCL_ERR_INVALID_ARG;
     if (!A_next || !pin) return fail(c, MCL_ERR_INVALID_ARG, "NULL argument");
     zero_csc(A_next);
@@ -1904,14 +1911,30 @@ static int iterate_range_impl(mcl_ctx_t c, const mcl_csc_t *A, const mcl_csc_t *
     RC(run_bins(c, kFused, pr, f, use_exact ? nullptr : est, use_exact ? nnzc : nullptr,
                 p.force_bin, base, st, cf_est));
     CK(cudaEventRecord(c->ev[4], c->stream));
-    // a8: assemble A_next
     int64_t nnz = 0;
     OutGuard guard(c, A_next);
-    RC(assemble(c, A->nrows, n, cnt, soff, srow, sval, A_next, &nnz));
-    A_next->row0 = A->row0;
-    A_next->col0 = B->col0 + col_begin;
-    A_next->n_global = A->n_global ? A->n_global : A->nrows;
-    CK(cudaEventRecord(c->ev[5], c->stream));
+    if (cand) {
+        // the candidates stay in the staging slots (the distributed prune reads them there);
+        // their total and the unpruned total from the statistics, one read-back
+        CK(launch_reduce_i64(cnt, n, tot + 2, c->stream));
+        CK(launch_reduce_i64(cand->nnz, n, tot + 3, c->stream));
+        unsigned long long ht[2] = {0, 0};
+        RC(readback(c, tot + 2, sizeof ht, ht));
+        cand->start = soff;
+        cand->count = cnt;
+        cand->row = srow;
+        cand->val = sval;
+        cand->total = nnz = (int64_t)ht[0];
+        cand->unpruned = (int64_t)ht[1];
+        CK(cudaEventRecord(c->ev[5], c->stream));
+    } else {
+        // a8: assemble A_next
+        RC(assemble(c, A->nrows, n, cnt, soff, srow, sval, A_next, &nnz));
+        A_next->row0 = A->row0;
+        A_next->col0 = B->col0 + col_begin;
+        A_next->n_global = A->n_global ? A->n_global : A->nrows;
+        CK(cudaEventRecord(c->ev[5], c->stream));
+    }
     float hmax = 0.f;
     RC(readback(c, cmax, sizeof(float), &hmax));
     if (st) {
@@ -2932,23 +2955,24 @@ int mcl_summa_iterate(mcl_ctx_t c, const mcl_csc_t *A, const mcl_params_t *pin, 
                 bin_nnzb[b] += sst.bin_nnzb[b];
                 bin_out[b] += sst.bin_out[b];
             }
+            if (fused) {  // the candidates, read in place from the product's staging slots
+                Cb.nrows = mi;
+                Cb.ncols = c1 - c0;
+                Cb.nnz = co.total;
+                Cb.col_ptr = const_cast<int64_t *>(co.start);
+                Cb.row_idx = const_cast<int32_t *>(co.row);
+                Cb.val = const_cast<float *>(co.val);
+            }
             Cb.row0 = A->row0;
             Cb.col0 = A->col0 + c0;
             Cb.n_global = n;
             peak_partial = std::max(peak_partial, Cb.nnz);
-            int64_t unpruned = Cb.nnz;
-            if (fused && c1 > c0) {  // the local block's unpruned entries, from the statistics
-                unsigned long long *tot;
-                RC(scratch_t(c, "tot", 4, &tot));
-                CK(launch_reduce_i64(co.nnz, c1 - c0, tot, c->stream));
-                unsigned long long hu = 0;
-                RC(readback(c, tot, sizeof hu, &hu));
-                unpruned = (int64_t)hu;
-            }
+            const int64_t unpruned = fused ? co.unpruned : Cb.nnz;
             float ch = 0.f;
-            rc = dist_prune(c, &Cb, pr > 1 ? c->colc : nullptr, pp, &piece, &ch, fused ? &co : nullptr);
+            rc = dist_prune(c, &Cb, pr > 1 ? c->colc : nullptr, pp, &piece, &ch, fused ? &co : nullptr,
+                            fused ? co.count : nullptr);
             nnz_unpruned += unpruned;
-            free_csc(c, &Cb);
+            if (!fused) free_csc(c, &Cb);  // (the candidates are the context's scratch)
             if (rc != MCL_OK) break;
             if (st) {
                 float dm = 0.f;

@@ -303,12 +303,14 @@ cudaError_t launch_dp_stats(int64_t ncols, const int64_t *cp, const float *vals,
 cudaError_t launch_dp_branch(int64_t ncols, const int64_t *nnz, const int64_t *m, const double *sm,
                              const PruneParams &pp, int64_t *K, int8_t *mode, int32_t *rem,
                              uint32_t *prefix, int32_t *rowcut, cudaStream_t s);
+// ccnt (dp_hist / dp_keepstats / dp_write): column j's entries are [cp[j], cp[j] + ccnt[j])
+// (staging slots) instead of [cp[j], cp[j + 1]) (compact CSC).
 // packed: histograms as 128 words per column, bins b and b + 128 in the low / high 16 bits
 // (the caller guarantees every global count < 2^16: candidate columns, <= ranks x max(S, R))
 cudaError_t launch_dp_hist(int64_t nsel, const int32_t *sel, const int64_t *cp, const int32_t *rows,
                            const float *vals, int64_t row0, const int8_t *mode, const uint32_t *vprefix,
                            const uint32_t *rprefix, const int32_t *done, int pass, unsigned *hist,
-                           int grid, cudaStream_t s, int packed = 0);
+                           int grid, cudaStream_t s, int packed = 0, const int64_t *ccnt = nullptr);
 cudaError_t launch_dp_sellist(int64_t ncols, const int8_t *mode, int64_t *flag, int64_t *pos,
                               int32_t *sel, void *tmp, cudaStream_t s);
 cudaError_t launch_dp_undone(int64_t nsel, const int32_t *sel, const int32_t *done,
@@ -319,11 +321,13 @@ cudaError_t launch_dp_digit(int64_t nsel, const int32_t *sel, const unsigned *hi
 cudaError_t launch_dp_keepstats(int64_t ncols, const int64_t *cp, const int32_t *rows,
                                 const float *vals, int64_t row0, const int8_t *mode,
                                 const uint32_t *vprefix, const int32_t *rowcut, const PruneParams &pp,
-                                int64_t *kcnt, double *sums, int grid, cudaStream_t s);
+                                int64_t *kcnt, double *sums, int grid, cudaStream_t s,
+                                const int64_t *ccnt = nullptr);
 cudaError_t launch_dp_write(int64_t ncols, const int64_t *cp, const int32_t *rows, const float *vals,
                             int64_t row0, const int8_t *mode, const uint32_t *vprefix,
                             const int32_t *rowcut, const PruneParams &pp, const double *gsums,
                             const int64_t *gkcnt, const int64_t *soff, int32_t *srow, float *sval,
-                            int64_t *scnt, float *chaos, float *chaos_max, int grid, cudaStream_t s);
+                            int64_t *scnt, float *chaos, float *chaos_max, int grid, cudaStream_t s,
+                            const int64_t *ccnt = nullptr);
 
 }  // namespace mclx

@@ -229,7 +229,8 @@ __global__ void __launch_bounds__(kDP) k_dp_hist(int64_t nsel, const int32_t *__
                                                  const uint32_t *__restrict__ vprefix,
                                                  const uint32_t *__restrict__ rprefix,
                                                  const int32_t *__restrict__ done, int pass,
-                                                 unsigned *__restrict__ hist, int packed) {
+                                                 unsigned *__restrict__ hist, int packed,
+                                                 const int64_t *__restrict__ ccnt) {
     __shared__ unsigned hs[kDP / 32][256];
     unsigned *h = hs[threadIdx.x >> 5];
     const int lane = lane_id();
@@ -238,7 +239,7 @@ __global__ void __launch_bounds__(kDP) k_dp_hist(int64_t nsel, const int32_t *__
         for (int i = lane; i < 256; i += 32) h[i] = 0;
         __syncwarp();
         if (!done[j]) {
-            const int64_t a = cp[j], b = cp[j + 1];
+            const int64_t a = cp[j], b = ccnt ? a + ccnt[j] : cp[j + 1];
             if (pass < 4) {
                 const int shift = 24 - 8 * pass;
                 const uint32_t mask = pass == 0 ? 0u : (0xFFFFFFFFu << (32 - 8 * pass));
@@ -270,12 +271,13 @@ __global__ void __launch_bounds__(kDP) k_dp_hist(int64_t nsel, const int32_t *__
 cudaError_t launch_dp_hist(int64_t nsel, const int32_t *sel, const int64_t *cp, const int32_t *rows,
                            const float *vals, int64_t row0, const int8_t *mode,
                            const uint32_t *vprefix, const uint32_t *rprefix, const int32_t *done,
-                           int pass, unsigned *hist, int grid, cudaStream_t s, int packed) {
+                           int pass, unsigned *hist, int grid, cudaStream_t s, int packed,
+                           const int64_t *ccnt) {
     if (nsel <= 0) return cudaSuccess;
     (void)grid;
     ++g_launches;
     k_dp_hist<<<dp_grid(nsel), kDP, 0, s>>>(nsel, sel, cp, rows, vals, row0, mode, vprefix, rprefix,
-                                             done, pass, hist, packed);
+                                             done, pass, hist, packed, ccnt);
     return cudaGetLastError();
 }
 
@@ -408,10 +410,11 @@ __global__ void __launch_bounds__(kDP) k_dp_keepstats(int64_t ncols, const int64
                                                       const uint32_t *__restrict__ vprefix,
                                                       const int32_t *__restrict__ rowcut,
                                                       PruneParams pp, int64_t *__restrict__ kcnt,
-                                                      double *__restrict__ sums /*[4][ncols]*/) {
+                                                      double *__restrict__ sums /*[4][ncols]*/,
+                                                      const int64_t *__restrict__ ccnt) {
     const int lane = lane_id();
     for (int64_t j = dp_warp0(); j < ncols; j += dp_wstride()) {
-        const int64_t a = cp[j], b = cp[j + 1];
+        const int64_t a = cp[j], b = ccnt ? a + ccnt[j] : cp[j + 1];
         const int8_t md = mode[j];
         const uint32_t t = vprefix[j];
         const int32_t rc = rowcut[j];
@@ -455,12 +458,13 @@ __global__ void __launch_bounds__(kDP) k_dp_keepstats(int64_t ncols, const int64
 cudaError_t launch_dp_keepstats(int64_t ncols, const int64_t *cp, const int32_t *rows,
                                 const float *vals, int64_t row0, const int8_t *mode,
                                 const uint32_t *vprefix, const int32_t *rowcut, const PruneParams &pp,
-                                int64_t *kcnt, double *sums, int grid, cudaStream_t s) {
+                                int64_t *kcnt, double *sums, int grid, cudaStream_t s,
+                                const int64_t *ccnt) {
     if (ncols <= 0) return cudaSuccess;
     (void)grid;
     ++g_launches;
     k_dp_keepstats<<<dp_grid(ncols), kDP, 0, s>>>(ncols, cp, rows, vals, row0, mode, vprefix, rowcut,
-                                                   pp, kcnt, sums);
+                                                   pp, kcnt, sums, ccnt);
     return cudaGetLastError();
 }
 
@@ -478,11 +482,11 @@ __global__ void __launch_bounds__(kDP) k_dp_write(int64_t ncols, const int64_t *
                                                   const int64_t *__restrict__ soff,
                                                   int32_t *__restrict__ srow, float *__restrict__ sval,
                                                   int64_t *__restrict__ scnt, float *__restrict__ chaos,
-                                                  float *chaos_max) {
+                                                  float *chaos_max, const int64_t *__restrict__ ccnt) {
     const int lane = lane_id();
     const unsigned lt = (1u << lane) - 1u;
     for (int64_t j = dp_warp0(); j < ncols; j += dp_wstride()) {
-        const int64_t a = cp[j], b = cp[j + 1];
+        const int64_t a = cp[j], b = ccnt ? a + ccnt[j] : cp[j + 1];
         const int8_t md = mode[j];
         const uint32_t t = vprefix[j];
         const int32_t rc = rowcut[j];
@@ -524,12 +528,14 @@ cudaError_t launch_dp_write(int64_t ncols, const int64_t *cp, const int32_t *row
                             int64_t row0, const int8_t *mode, const uint32_t *vprefix,
                             const int32_t *rowcut, const PruneParams &pp, const double *gsums,
                             const int64_t *gkcnt, const int64_t *soff, int32_t *srow, float *sval,
-                            int64_t *scnt, float *chaos, float *chaos_max, int grid, cudaStream_t s) {
+                            int64_t *scnt, float *chaos, float *chaos_max, int grid, cudaStream_t s,
+                            const int64_t *ccnt) {
     if (ncols <= 0) return cudaSuccess;
     (void)grid;
     ++g_launches;
     k_dp_write<<<dp_grid(ncols), kDP, 0, s>>>(ncols, cp, rows, vals, row0, mode, vprefix, rowcut, pp,
-                                               gsums, gkcnt, soff, srow, sval, scnt, chaos, chaos_max);
+                                               gsums, gkcnt, soff, srow, sval, scnt, chaos, chaos_max,
+                                               ccnt);
     return cudaGetLastError();
 }
 
