@@ -235,10 +235,16 @@ int mcl_merge(mcl_ctx_t ctx, int32_t L, const mcl_csc_t *lists, mcl_csc_t *out);
  * of every iterate.  The inner dimension is cut into s = lcm(pr, pc) panels K_q; at stage
  * q rank (i, floor(q pc/s)) broadcasts A[rows_i, K_q] along its row communicator and rank
  * (floor(q pr/s), j) broadcasts A[K_q, cols_j] along its column communicator (NCCL over
- * NVLink), every rank multiplies the two panels (mcl_spgemm) and the stage partials are
- * merged on the device under Alg. 2 (binary merge).  The pruning of a column
- * split over pr ranks exchanges only fixed-size all-reduces (per-column counts and sums,
- * radix-select digit histograms for the exact top-k cut).
+ * NVLink).  Forms of the local product:
+ *   pr = 1: every column of C lives on one rank; all stages accumulate in the fused kernel
+ *     and the prune is local.
+ *   pr > 1 (default): the resident panels are stacked into A[rows_i, :] and A[:, cols_j] and
+ *     ONE fused product in candidate mode yields each column's top-max(S, R) entries plus
+ *     the statistics of all its entries (the stage partials merge in the hash tables).
+ *   pr > 1 with MCLX_SUMMA_STAGED=1: a product per stage (mcl_spgemm) and the Alg. 2 binary
+ *     merge on the device.
+ * The pruning of a column split over pr ranks exchanges only fixed-size all-reduces
+ * (per-column counts and sums, radix-select digit histograms for the exact top-k cut).
  */
 
 /* out = A[r0:r1, c0:c1] (local index ranges) as a block: row ids rebased to r0, row0 / col0
