@@ -273,9 +273,18 @@ __global__ void __launch_bounds__(NT, (bin_min_blocks<CAP, NT, MODE, GLOBAL, ATO
             vals = reinterpret_cast<V *>(dsm + (size_t)CAP * sizeof(int));
             cap = CAP;
         }
-        for (uint32_t i = tid; i < cap; i += NT) {
-            keys[i] = kEmptyKey;
-            if (MODE != kSym) vals[i] = V(0);
+        if constexpr (!GLOBAL) {  // 16-byte stores (CAP is a multiple of 4 NT; dsm is aligned)
+            int4 *k4 = reinterpret_cast<int4 *>(keys);
+            float4 *v4 = reinterpret_cast<float4 *>(vals);
+            for (uint32_t i = tid; i < CAP / 4; i += NT) {
+                k4[i] = make_int4(kEmptyKey, kEmptyKey, kEmptyKey, kEmptyKey);
+                if (MODE != kSym) v4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        } else {
+            for (uint32_t i = tid; i < cap; i += NT) {
+                keys[i] = kEmptyKey;
+                if (MODE != kSym) vals[i] = V(0);
+            }
         }
         __syncthreads();
 
