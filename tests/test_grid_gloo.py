@@ -121,3 +121,20 @@ def test_grid_arithmetic_matches_paper_square_case():
                 c0, c1 = g.cols(n, g.a_owner_col(q))
                 r0, r1 = g.rows(n, g.b_owner_row(q))
                 assert c0 <= k0 < k1 <= c1 and r0 <= k0 < k1 <= r1
+
+
+def test_bench_default_grids_are_the_north_stars():
+    """bench.py --gpus N runs BASELINE.json's grids (1x1, 1x2, 2x2, 2x4); other N run 1xN."""
+    import importlib.util
+    import os
+    spec = importlib.util.spec_from_file_location(
+        "bench_mod", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    saved = os.environ.get("PYTORCH_CUDA_ALLOC_CONF")
+    spec.loader.exec_module(bench)  # (bench.py sets the allocator config; undo it here)
+    if saved is None:
+        os.environ.pop("PYTORCH_CUDA_ALLOC_CONF", None)
+    else:
+        os.environ["PYTORCH_CUDA_ALLOC_CONF"] = saved
+    assert [bench.default_grid(n) for n in (1, 2, 4, 8)] == [(1, 1), (1, 2), (2, 2), (2, 4)]
+    assert bench.default_grid(3) == (1, 3) and bench.default_grid(6) == (1, 6)
