@@ -67,6 +67,7 @@ struct mcl_ctx {
     bool validate = false;                    // MCLX_VALIDATE=1: check input CSC invariants
     bool split_cand = true;                   // MCLX_SPLIT_CAND=0: split parts stage every entry
     int dense_min_P = 64;                     // MCLX_DENSE_MIN_P: split columns of more parts go dense
+    int split_big = 0;                        // MCLX_SPLIT_BIG=1: half the parts, 2x tables (A/B)
     double esc_cf = 1.5;                      // MCLX_ESC_CF: cf below which a small column runs ESC (0: off)
     double esc_iter_cf = 2.0;                 // MCLX_ESC_ITER_CF: ... when the product's cf is below this
     int force_phases = 0;                     // MCLX_PHASES=h forces h column batches (tests)
@@ -453,6 +454,7 @@ int run_split(mcl_ctx *c, const Prod &pr, int nsplit, int32_t *split_list,
         const int P = Pf & ~kSplitFlags;
         return (Pf & kSplitFp64) ? 3
                : (Pf & kSplitDense) ? 2
+               : (Pf & kSplitBig) ? 1
                : priv && priv_ok(Pf) ? 4
                : P <= 32 ? 0 : 1;
     };
@@ -750,6 +752,7 @@ int run_bins(mcl_ctx *c, int mode, const Prod &pr, const int64_t *f, const float
             ca.split_min = c->split_min_need;
             ca.split_part_need = c->split_part_need;
             ca.dense_min_P = c->dense_min_P;
+            ca.split_big = c->split_big;
             ca.split_count = split_count;
             ca.split_list = split_list;
             ca.split_P = split_P;
@@ -1543,6 +1546,7 @@ int mcl_ctx_create(mcl_ctx_t *out, int device, void *stream, mcl_alloc_fn alloc,
     if (const char *e = getenv("MCLX_VALIDATE")) c->validate = atoi(e) != 0;
     if (const char *e = getenv("MCLX_FAMILY")) c->family = atoi(e);
     if (const char *e = getenv("MCLX_SPLIT_CAND")) c->split_cand = atoi(e) != 0;
+    if (const char *e = getenv("MCLX_SPLIT_BIG")) c->split_big = atoi(e) != 0;
     if (const char *e = getenv("MCLX_DENSE_MIN_P")) c->dense_min_P = std::max(1, std::min(64, atoi(e)));
     if (const char *e = getenv("MCLX_ESC_CF")) c->esc_cf = atof(e);
     if (const char *e = getenv("MCLX_ESC_ITER_CF")) c->esc_iter_cf = atof(e);

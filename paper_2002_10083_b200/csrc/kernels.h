@@ -112,7 +112,9 @@ constexpr int kSplitFp64 = 1 << 30;
 constexpr int kSplitShared = 1 << 29;
 // split_P flag: sweep the column's row ranges with dense tiles (kernels_dense.cu)
 constexpr int kSplitDense = 1 << 28;
-constexpr int kSplitFlags = kSplitFp64 | kSplitShared | kSplitDense;
+// split_P flag (MCLX_SPLIT_BIG=1): half as many parts, each in a 2*kPartCap-slot table
+constexpr int kSplitBig = 1 << 27;
+constexpr int kSplitFlags = kSplitFp64 | kSplitShared | kSplitDense | kSplitBig;
 // work items (row-range parts) of a split column from its split_P entry: the dense variants
 // (more than 64 virtual parts, or fp64) sweep kDenseParts ranges, hashed parts min(P, 32)
 __host__ __device__ inline int split_parts(int Pf) {
@@ -203,6 +205,7 @@ struct ClassifyArgs {
     int64_t split_min;       // also split smaller columns with need > split_min (tests)
     int64_t split_part_need; // distinct rows a part is sized for (kPartNeed)
     int dense_min_P;         // virtual part counts above this (<= 64) take the dense sweep
+    int split_big;           // P in [4, 32]: P/2 parts of 2*kPartCap-slot tables (kSplitBig)
     int64_t fp64_terms;      // nnz(B_*j) above which a column accumulates in fp64 (kFp64Terms)
     // low-cf columns (kernels_esc.cu): f_j <= esc_max and f_j < esc_cf x (estimated or exact
     // nnz_j) run the expand-sort-compress kernel; esc_max = 0 disables

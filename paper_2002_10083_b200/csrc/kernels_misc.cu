@@ -426,6 +426,7 @@ __global__ void k_classify(ClassifyArgs c) {
             // long sums (T): only the dense fp64 variant accumulates in fp64
             if (nb > c.fp64_terms) P = (P < 128 ? 128 : P) | kSplitFp64;
             else if (P > c.dense_min_P) P |= kSplitDense;
+            else if (c.split_big && P >= 4 && P <= 32) P = (P >> 1) | kSplitBig;
             // private-slice parts give each of 8 warps 1/(8P) of every segment: below
             // kShortSegment / 2 rows on average the lanes idle, so use the shared table
             else if (f < (int64_t)(kShortSegment / 2) * nb * 8 * P) P |= kSplitShared;
